@@ -1,0 +1,257 @@
+"""Pins of the oracle's Markov model (oracle/model.c) against what the paper and mathematics fix.
+
+Each test pins the oracle to something other than itself: closed forms of the two-state chain,
+a textbook special case (independent warps -> binomial), invariants (row sums, stationarity,
+lumpability, symmetry), a proven bound, a per-warp Monte Carlo simulation of the round process
+that shares nothing with the linear algebra, and power iteration as an independent solver.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+
+def _golden_examples():
+    rows = {}
+    for line in open(__file__.replace("test_oracle_model.py", "golden/model_worked_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        f = line.split()
+        rows[f[0]] = f[1:]
+    return rows
+
+
+def test_w1_closed_form_golden():
+    """P:825-921 with W=1: IPC = 1/(1+Rm L); Rm=1, L=9 -> pi=(0.1,0.9), IPC=0.1."""
+    g = _golden_examples()
+    for case in ("w1_a", "w1_b"):
+        W, rm, L, p0, p1, ipc = g[case]
+        cfg = O.smcfg(L0=float(L), a0=0.0, W=int(W))
+        P, R = O.build_homog(O.kmodel(float(rm)), int(W), cfg)
+        pi = O.stationary(P)
+        assert abs(pi[0] - float(p0)) < 1e-12 and abs(pi[1] - float(p1)) < 1e-12
+        assert abs(O.ipc_homog(1, pi) - float(ipc)) < 1e-12
+
+
+@pytest.mark.parametrize("rm", [0.01, 0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.9, 1.0])
+@pytest.mark.parametrize("L", [2.5, 9.0, 40.0, 400.0])
+def test_w1_closed_form_grid(rm, L):
+    cfg = O.smcfg(L0=L, a0=0.0, W=1)
+    P, _ = O.build_homog(O.kmodel(rm), 1, cfg)
+    assert abs(O.ipc_homog(1, O.stationary(P)) - 1.0 / (1.0 + rm * L)) < 1e-12
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8, 12, 16, 24])
+def test_rm_zero_ipc_one(W):
+    """Rm = 0: no warp ever stalls, gamma_W = 0, Eq.4 gives IPC = 1 exactly."""
+    cfg = O.smcfg(L0=300.0, B=1.0, a0=5.0, W=W)
+    P, _ = O.build_homog(O.kmodel(0.0), W, cfg)
+    assert abs(O.ipc_homog(W, O.stationary(P)) - 1.0) < 1e-12
+
+
+def _rand_cfgs(n, seed=0):
+    rng = np.random.default_rng(seed)
+    for _ in range(n):
+        W = int(rng.integers(1, 17))
+        cfg = O.smcfg(L0=float(rng.uniform(W + 5, 900)), B=float(rng.uniform(0.2, 4)),
+                      a0=float(rng.uniform(0, 3)), b0=float(rng.uniform(0, 50)), W=16)
+        yield W, O.kmodel(float(rng.uniform(0, 1)), r=float(rng.uniform(1, 32))), cfg
+
+
+def test_rows_stochastic_and_stationary():
+    """Every built matrix is row-stochastic (<=1e-12, entries in [0,1]); the LU pi satisfies
+    pi P = pi to 1e-12, pi >= 0, sum 1; power iteration (independent solver) agrees."""
+    for W, k, cfg in _rand_cfgs(120):
+        P, _ = O.build_homog(k, W, cfg)
+        assert np.all(P >= -1e-15) and np.all(P <= 1 + 1e-15)
+        assert np.max(np.abs(P.sum(1) - 1)) < 1e-12
+        pi = O.stationary(P)
+        assert np.max(np.abs(pi @ P - pi)) < 1e-12
+        assert pi.min() > -1e-14 and abs(pi.sum() - 1) < 1e-12
+        Q = 0.5 * (P + np.eye(W + 1))            # lazy chain: same pi, aperiodic
+        v = np.full(W + 1, 1.0 / (W + 1))
+        for _ in range(200000):
+            v2 = v @ Q
+            if np.max(np.abs(v2 - v)) < 1e-15:
+                break
+            v = v2
+        assert np.max(np.abs(v - pi)) < 1e-9
+
+
+def test_joint_rows_stochastic():
+    rng = np.random.default_rng(3)
+    for _ in range(60):
+        w1 = int(rng.integers(1, 9)); w2 = int(rng.integers(1, 17 - w1))
+        cfg = O.smcfg(L0=float(rng.uniform(30, 900)), B=float(rng.uniform(0.2, 4)),
+                      a0=float(rng.uniform(0, 3)), W=16)
+        k1 = O.kmodel(float(rng.uniform(0, 1)), r=float(rng.uniform(1, 32)))
+        k2 = O.kmodel(float(rng.uniform(0, 1)), r=float(rng.uniform(1, 32)))
+        P, _ = O.build_joint(k1, w1, k2, w2, cfg)
+        assert np.max(np.abs(P.sum(1) - 1)) < 1e-12 and P.min() >= -1e-15
+        pi = O.stationary(P)
+        assert np.max(np.abs(pi @ P - pi)) < 1e-12
+
+
+@pytest.mark.parametrize("W,rm,q", [(1, 0.3, 0.1), (5, 0.2, 0.05), (16, 0.1, 1 / 80), (16, 0.9, 0.5)])
+def test_binomial_special_case(W, rm, q):
+    """With a state-independent P_ir = q every warp is an independent two-state chain, so the
+    idle count is Binomial(W, Rm/(Rm+q)) (textbook); pins the Eq.2 convolution (R3)."""
+    cfg = O.smcfg(W=W, pir_mode=1, const_q=q)
+    P, _ = O.build_homog(O.kmodel(rm), W, cfg)
+    pi = O.stationary(P)
+    p = rm / (rm + q)
+    ref = np.array([math.comb(W, i) * p**i * (1 - p) ** (W - i) for i in range(W + 1)])
+    assert np.max(np.abs(pi - ref)) < 1e-13
+
+
+def test_ipc_bound_constant_latency():
+    """Proven bound for constant L: IPC <= min(1, W/(1 + Rm L)) (SURVEY §8(c) pins)."""
+    rng = np.random.default_rng(5)
+    for _ in range(80):
+        W = int(rng.integers(1, 17)); rm = float(rng.uniform(0.01, 1)); L = float(rng.uniform(W + 1, 1000))
+        P, _ = O.build_homog(O.kmodel(rm), W, O.smcfg(L0=L, a0=0.0, W=W))
+        ipc = O.ipc_homog(W, O.stationary(P))
+        assert ipc <= min(1.0, W / (1 + rm * L)) + 1e-12
+
+
+@pytest.mark.parametrize("W", [4, 8, 12, 16])
+def test_lumpability(W):
+    """Identical kernels split (w1, w2): lumping joint states by p+q gives the homogeneous chain
+    (matrix level, 1e-12) and C = homogeneous IPC at W = w1 + w2 (1e-12), with L depending on
+    the total outstanding requests."""
+    k = O.kmodel(0.15, r=4.0)
+    cfg = O.smcfg(L0=200.0, B=2.0, a0=1.5, b0=10.0, W=16)
+    Ph, _ = O.build_homog(k, W, cfg)
+    ipc_h = O.ipc_homog(W, O.stationary(Ph))
+    for w1 in range(1, W):
+        w2 = W - w1
+        P, R = O.build_joint(k, w1, k, w2, cfg)
+        # lump: from any (p,q) with p+q = i, total mass into {p'+q' = j} equals Ph[i, j]
+        for p in range(w1 + 1):
+            for q in range(w2 + 1):
+                s = p * (w2 + 1) + q
+                lumped = np.zeros(W + 1)
+                for pp in range(w1 + 1):
+                    for qq in range(w2 + 1):
+                        lumped[pp + qq] += P[s, pp * (w2 + 1) + qq]
+                assert np.max(np.abs(lumped - Ph[p + q])) < 1e-12
+        _, _, c = O.ipc_joint(w1, w2, O.stationary(P), R)
+        assert abs(c - ipc_h) < 1e-12
+
+
+def test_symmetry():
+    k1, k2 = O.kmodel(0.3, r=2.0), O.kmodel(0.05, r=8.0)
+    cfg = O.smcfg(L0=300.0, B=1.0, a0=2.0, W=16)
+    P, R = O.build_joint(k1, 6, k2, 10, cfg)
+    a1, a2, _ = O.ipc_joint(6, 10, O.stationary(P), R)
+    P, R = O.build_joint(k2, 10, k1, 6, cfg)
+    b1, b2, _ = O.ipc_joint(10, 6, O.stationary(P), R)
+    assert abs(a1 - b2) < 1e-12 and abs(a2 - b1) < 1e-12
+    P, R = O.build_joint(k1, 8, k1, 8, cfg)
+    x1, x2, _ = O.ipc_joint(8, 8, O.stationary(P), R)
+    assert abs(x1 - x2) < 1e-12
+
+
+def test_cp_unit_checks():
+    """Eq.1 unit values."""
+    assert O.cp([1.0, 1.0], [1.0, 1.0]) == 0.5
+    assert O.cp([0.5, 0.5], [1.0, 1.0]) == 0.0
+    assert O.cp([1.0], [1.0]) == 0.0
+
+
+def _simulate(ws, rms, rs, cfg, rounds, seed):
+    """Per-warp Monte Carlo of the round process: each ready warp issues one
+    instruction and then stalls with probability Rm; each idle warp returns with probability
+    P_ir = min(1, R/L) evaluated in the current state; time advances by the round duration
+    R = max(#ready, 1).  Returns long-run instructions/cycle and batch-means sigma."""
+    rng = np.random.default_rng(seed)
+    idle = [np.zeros(w, bool) for w in ws]
+    nb = 50
+    per = rounds // nb
+    inst_b, cyc_b = np.zeros(nb), np.zeros(nb)
+    for b in range(nb):
+        inst = cyc = 0.0
+        for _ in range(per):
+            nidle = [int(x.sum()) for x in idle]
+            ready = sum(w - n for w, n in zip(ws, nidle))
+            R = max(ready, 1)
+            n_out = sum(n * r for n, r in zip(nidle, rs))
+            L = O.latency(cfg, n_out, sum(nidle))
+            pir = min(1.0, R / L)
+            for k in range(len(ws)):
+                u = rng.random(ws[k])
+                was_idle = idle[k]
+                inst += float((~was_idle).sum())
+                idle[k] = np.where(was_idle, u >= pir, u < rms[k])
+            cyc += R
+        inst_b[b], cyc_b[b] = inst, cyc
+    ipc = inst_b.sum() / cyc_b.sum()
+    sig = np.std(inst_b / cyc_b, ddof=1) / math.sqrt(nb)
+    return ipc, sig
+
+
+@pytest.mark.parametrize("W,rm,L", [(8, 0.3, 50.0), (16, 0.1, 80.0), (1, 0.5, 10.0), (4, 0.2, 20.0)])
+def test_monte_carlo_homogeneous(W, rm, L):
+    cfg = O.smcfg(L0=L, a0=0.0, W=W)
+    P, _ = O.build_homog(O.kmodel(rm), W, cfg)
+    model = O.ipc_homog(W, O.stationary(P))
+    mc, sig = _simulate([W], [rm], [1.0], cfg, 100000, seed=W)
+    assert abs(mc - model) <= 3.5 * sig + 1e-4, (mc, model, sig)
+
+
+def test_monte_carlo_joint():
+    cfg = O.smcfg(L0=120.0, B=1.0, a0=2.0, W=16)
+    k1, k2 = O.kmodel(0.25, r=2.0), O.kmodel(0.05, r=1.0)
+    P, R = O.build_joint(k1, 6, k2, 10, cfg)
+    a, b, c = O.ipc_joint(6, 10, O.stationary(P), R)
+    mc, sig = _simulate([6, 10], [0.25, 0.05], [2.0, 1.0], cfg, 100000, seed=11)
+    assert abs(mc - c) <= 3.5 * sig + 1e-4, (mc, c, sig)
+
+
+def test_survey_scratch_values():
+    """Cross-check values computed under readings R1-R7 by an independent scratch script
+    (SURVEY §8(c) 'Scratch cross-check values'; 12 significant digits)."""
+    def homog(W, rm, L0, a0):
+        cfg = O.smcfg(L0=L0, B=1.0, a0=a0, W=16)
+        P, _ = O.build_homog(O.kmodel(rm, r=1.0), W, cfg)
+        return O.ipc_homog(W, O.stationary(P))
+    assert abs(homog(16, 0.1, 80.0, 0.0) - 0.996182773483) < 1e-11
+    assert abs(homog(16, 0.05, 400.0, 4.0) - 0.634428535579) < 1e-11
+    assert abs(homog(8, 0.3, 50.0, 0.0) - 0.481613332960) < 1e-11
+    s1, s2 = homog(16, 0.25, 300.0, 20.0), homog(16, 0.02, 300.0, 20.0)
+    assert abs(s1 - 0.102855393019) < 1e-11 and abs(s2 - 0.960397950576) < 1e-11
+    cfg = O.smcfg(L0=300.0, B=1.0, a0=20.0, W=16)
+    P, R = O.build_joint(O.kmodel(0.25), 8, O.kmodel(0.02), 8, cfg)
+    a, b, c = O.ipc_joint(8, 8, O.stationary(P), R)
+    assert abs(a - 0.053138785523) < 1e-11 and abs(b - 0.569158160684) < 1e-11
+    assert abs(c - 0.622296946207) < 1e-11
+    assert abs(O.cp([a, b], [s1, s2]) - 0.098500773047) < 1e-11
+    cfg = O.smcfg(L0=100.0, a0=0.0, W=16)
+    P, R = O.build_joint(O.kmodel(0.5), 2, O.kmodel(0.01), 6, cfg)
+    a, b, c = O.ipc_joint(2, 6, O.stationary(P), R)
+    assert abs(a - 0.035643329673) < 1e-11 and abs(b - 0.963965632837) < 1e-11
+    assert abs(c - 0.999608962510) < 1e-11
+    s1, s2 = homog(16, 0.5, 100.0, 0.0), homog(16, 0.01, 100.0, 0.0)
+    assert abs(O.cp([a, b], [s1, s2]) - 0.072696509857) < 1e-11
+
+
+def test_predict_consistency():
+    """or_predict composes the pieces: joint IPCs, solo IPCs at b_max, CP (Eq.1), dT (Eq.8)."""
+    cfg = O.smcfg(L0=300.0, B=1.0, a0=2.0, W=16)
+    k1, k2 = O.kmodel(0.3, r=2.0, ipb=5000.0, wpb=8), O.kmodel(0.02, r=1.0, ipb=20000.0, wpb=4)
+    r = O.predict(k1, 4, 8, k2, 8, 16, 4, cfg)
+    assert r.status == 0
+    s1, _ = O.solo_ipc(k1, 8, 4, cfg)
+    s2, _ = O.solo_ipc(k2, 16, 4, cfg)
+    assert r.solo1 == s1 and r.solo2 == s2
+    assert abs(r.cp - O.cp([r.ipc1, r.ipc2], [s1, s2])) < 1e-15
+    assert abs(r.dT - abs(5000 * 4 / r.ipc1 - 20000 * 8 / r.ipc2)) < 1e-9 * r.dT
+    assert O.predict(k1, 8, 8, k2, 8, 16, 4, cfg).status == 2      # 16 + 8 warps > W_v
+
+
+def test_reducible_chain_rejected():
+    """R22: Rm=1 with P_ir clamped to 1 makes the chain an involution; the guard L > W rejects."""
+    with pytest.raises(ValueError):
+        O.build_homog(O.kmodel(1.0), 16, O.smcfg(L0=10.0, a0=0.0, W=16))
