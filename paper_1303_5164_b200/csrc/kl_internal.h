@@ -1,0 +1,103 @@
+// kl_internal.h -- device/host shared structures of libkl (product path; not used by oracle/).
+#pragma once
+#include <cstdint>
+#include "../../include/kl.h"
+
+// ---------------------------------------------------------------------------------------------
+// Slice control block (one per submitted kernel instance, device memory).
+// A kernel's virtual block range [0, len) is consumed by work-pulling persistent blocks; the
+// 64-bit `word` linearises every fetch and every stop:
+//   bits [31:0]  next   : next virtual block to hand out (absolute)
+//   bits [62:32] stop_at: absolute slice boundary after which the current launch stops
+//   bit  63      stop   : stop requested for the current launch
+// Fetch = atomicAdd(word, chunk); stop = CAS that sets stop/stop_at = first slice boundary at or
+// after `next`.  Hence every handed-out block below the final limit runs exactly once and
+// [limit, len) stays pending (every block in exactly one co-schedule).
+// ---------------------------------------------------------------------------------------------
+struct KlCtl {
+    unsigned long long word;
+    uint32_t len;
+    uint32_t exited;      // blocks of the current launch that finished (admitted or not)
+    uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
+    uint32_t admitted;    // admitted blocks of the current launch
+    uint32_t executed;    // virtual blocks executed in the current launch
+    uint32_t pad0;
+    unsigned long long t0;  // earliest admitted-block start (globaltimer ns), current launch
+    uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
+    uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
+};
+
+// Host-mapped (pinned) record written by the last block of a launch.
+struct KlLaunchRec {
+    uint32_t end;         // first virtual block not executed (absolute)
+    uint32_t exhausted;   // end == len
+    uint32_t executed, admitted, max_per_sm, pad;
+    unsigned long long t0, t1;
+    volatile uint32_t done;
+    uint32_t pad2;
+};
+
+struct KlLaunch {
+    KlCtl* ctl;
+    KlCtl* partner;                 // stopped when this kernel drains (nullptr: solo phase)
+    uint32_t cap;                   // admitted blocks per SM (0 = no cap)
+    uint32_t chunk;                 // virtual blocks per fetch
+    uint32_t start;                 // this launch's first virtual block
+    uint32_t partner_start, partner_slice;
+    uint32_t n_sms;
+    KlLaunchRec* rec;
+    unsigned long long* counters;   // kl_counters on the device (may be null)
+    uint32_t* audit;                // per-virtual-block execution counts (may be null)
+    unsigned long long tag;
+};
+
+// ---- kernel-side entry points exported by kl_kernels.cu / kl_mm.cu ---------------------------
+struct KlKindInfo {
+    int threads;          // threads per block
+    int dyn_smem;         // dynamic shared memory per block
+    int regs;             // registers per thread (persistent variant)
+    int static_smem;
+    int tmem_cols;
+    int bmax;             // occupancy calculator, solo
+    int default_chunk;
+};
+
+// Query attributes of the persistent variant of `kind` (needs a CUDA device).
+int kl_dev_kind_info(int kind, KlKindInfo* out);
+// Prepare per-instance device state (e.g. TMA descriptors for MM); `blob` receives up to
+// 512 bytes of launch-time parameter data stored with the instance.
+int kl_dev_prepare(int kind, const void* args, uint32_t args_bytes, void* blob, uint32_t blob_cap);
+// Launch the persistent slice launcher for `kind` with `grid` blocks.
+int kl_dev_launch_persistent(int kind, const void* blob, const KlLaunch& L, uint32_t grid,
+                             void* stream);
+// Launch a plain grid of n_blocks with blockIdx rectified by offset.
+int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n_blocks,
+                        void* stream);
+
+// ---- model kernels (kl_model.cu) ---------------------------------------------------------
+struct KlModelKind {       // per-kind model inputs, device table
+    double rm, r, ipb;
+    int32_t wpb, bsolo, pad0, pad1;
+};
+struct KlModelCfg {
+    double L0, B, a0, b0;
+    int32_t W, n_sched, latency_mode, n_cand;
+};
+struct KlCand {            // one candidate, and its grouping for the fused selection
+    int32_t k1, k2;
+    uint32_t b1, b2;
+    int32_t pair;          // pair index (selection groups; -1: prediction only)
+    int32_t warps;         // b1*wpb1 + b2*wpb2 (tie-break)
+};
+struct KlDecision {
+    int32_t cand;          // chosen candidate index, -1 = none (solo)
+    int32_t n_pairs;
+    double cp;
+    volatile int32_t done;
+    int32_t pad;
+};
+// Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy
+// selection (a9) and writes *dec.  `done_counter` must be zero on entry (reset by the kernel).
+int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands,
+                       kl_prediction* preds, int n_pairs, const int32_t* pair_rank,
+                       uint32_t* done_counter, KlDecision* dec, void* stream);

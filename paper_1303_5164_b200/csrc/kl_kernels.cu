@@ -1,0 +1,616 @@
+// kl_kernels.cu -- sm_100a slice launcher and the paper's benchmark kernels (product path).
+//
+// Slicing: a slice is a contiguous range of a kernel's thread blocks launched with
+// its block index rectified by an offset.  On B200 a phase launches ONE persistent grid per
+// kernel (cap x n_SM blocks); each admitted block pulls virtual block ids from the kernel's
+// slice control word and runs Body::block(vb) -- index rectification as a kernel parameter
+// instead of Fermi SASS rewriting.  Occupancy control (P:258-267 via slice sizes on
+// Fermi) becomes a per-SM admission cap read from %smid.
+//
+// Every body computes exactly the definition in oracle/kernels.c (independently written); the
+// per-output operation order never depends on the slicing, so sliced == unsliced bit for bit.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstring>
+#include "kl_internal.h"
+
+namespace {
+
+__device__ __forceinline__ uint32_t smid_u32() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ------------------------------------------------------------------------------------------
+// Benchmark bodies.  Interface: Params (kernel args), kThreads, kChunk (default virtual blocks
+// per fetch), State + init/fini (per persistent block), block(vb) (one virtual thread block).
+// ------------------------------------------------------------------------------------------
+struct Empty {};
+
+// PC: 256 threads; dependent loads through the read-only path.
+struct BodyPC {
+    using Params = kl_args_pc;
+    using State = Empty;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        uint32_t t = vb * 256u + threadIdx.x;
+        if (t >= a.n_threads) return;
+        uint32_t p = (t * 2654435761u) % a.n_nodes;
+        uint32_t acc = 0;
+        for (uint32_t h = 0; h < a.hops; ++h) {
+            p = (uint32_t)__ldg(a.next + p);
+            acc += p;
+        }
+        a.out[t] = (int32_t)p;
+        a.acc[t] = acc;
+    }
+};
+
+// SAD: one warp per 16x16 macroblock; the 48x48 clamped reference window is staged in
+// shared memory, the current block lives in registers; lane l owns displacement column dx = l
+// and sweeps all 33 dy with vabsdiff4 (4 pixels per instruction); column dx = 32 is spread over
+// the lanes afterwards.
+__device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+struct BodySAD {
+    using Params = kl_args_sad;
+    using State = Empty;
+    static constexpr int kThreads = 32, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        __shared__ uint32_t win[48 * 12];
+        __shared__ uint32_t curs[64];
+        const int W = a.width, H = a.height, mbw = W / 16, n_mb = mbw * (H / 16);
+        if ((int)vb >= n_mb) return;   // padding blocks of the paper's 8048-block grid
+        const int lane = threadIdx.x;
+        const int mx = vb % mbw, my = vb / mbw;
+        const int x0 = mx * 16 - 16, y0 = my * 16 - 16;
+        const bool inner = (x0 >= 0) && (x0 + 48 <= W) && (y0 >= 0) && (y0 + 48 <= H);
+        for (int i = lane; i < 48 * 12; i += 32) {
+            int y = i / 12, wc = i % 12;
+            if (inner) {
+                win[i] = *reinterpret_cast<const uint32_t*>(a.ref + (size_t)(y0 + y) * W + x0 + wc * 4);
+            } else {
+                int gy = min(max(y0 + y, 0), H - 1);
+                uint32_t v = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    int gx = min(max(x0 + wc * 4 + b, 0), W - 1);
+                    v |= (uint32_t)a.ref[(size_t)gy * W + gx] << (8 * b);
+                }
+                win[i] = v;
+            }
+        }
+        for (int i = lane; i < 64; i += 32)
+            curs[i] = *reinterpret_cast<const uint32_t*>(a.cur + (size_t)(my * 16 + i / 4) * W + mx * 16 + (i % 4) * 4);
+        __syncwarp();
+        uint32_t cur[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) cur[i] = curs[i];
+        uint32_t acc[33];
+#pragma unroll
+        for (int i = 0; i < 33; ++i) acc[i] = 0;
+        const int wo = lane >> 2, sh = (lane & 3) * 8;
+#pragma unroll
+        for (int y = 0; y < 48; ++y) {
+            const uint32_t* row = win + y * 12 + wo;
+            uint32_t w0 = row[0], w1 = row[1], w2 = row[2], w3 = row[3], w4 = row[4];
+            uint32_t q0 = __funnelshift_r(w0, w1, sh), q1 = __funnelshift_r(w1, w2, sh);
+            uint32_t q2 = __funnelshift_r(w2, w3, sh), q3 = __funnelshift_r(w3, w4, sh);
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int dy = y - r;
+                if (dy >= 0 && dy <= 32) {
+                    uint32_t s = vsad4(q0, cur[r * 4 + 0], acc[dy]);
+                    s = vsad4(q1, cur[r * 4 + 1], s);
+                    s = vsad4(q2, cur[r * 4 + 2], s);
+                    acc[dy] = vsad4(q3, cur[r * 4 + 3], s);
+                }
+            }
+        }
+        uint16_t* o = a.out + (size_t)vb * 1089;
+#pragma unroll
+        for (int dy = 0; dy < 33; ++dy) o[dy * 33 + lane] = (uint16_t)acc[dy];
+        // displacement column dx = 32: lane l computes dy = l, lane 0 also dy = 32
+        for (int dy = lane; dy < 33; dy += 32) {
+            uint32_t s = 0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const uint32_t* row = win + (dy + r) * 12 + 8;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) s = vsad4(row[i], cur[r * 4 + i], s);
+            }
+            o[dy * 33 + 32] = (uint16_t)s;
+        }
+        __syncwarp();
+    }
+};
+
+// SPMV (CUSP CSR-vector): one warp per row, 8 rows per block, butterfly reduction.
+struct BodySPMV {
+    using Params = kl_args_spmv;
+    using State = Empty;
+    static constexpr int kThreads = 256, kChunk = 8, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int row = (int)vb * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+        if (row >= a.n_rows) return;
+        const int s = __ldg(a.rowptr + row), e = __ldg(a.rowptr + row + 1);
+        float sum = 0.f;
+        for (int j = s + lane; j < e; j += 32) sum = fmaf(__ldg(a.vals + j), __ldg(a.x + __ldg(a.cols + j)), sum);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == 0) a.y[row] = sum;
+    }
+};
+
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z
+// neighbours ride a register queue, x/y neighbours come through L1.
+struct BodyST {
+    using Params = kl_args_st;
+    using State = Empty;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int nx = a.nx, ny = a.ny, nz = a.nz;
+        const int gx = (nx + 31) / 32, gy = (ny + 3) / 4;
+        const int bx = vb % gx, by = (vb / gx) % gy, bz = vb / (gx * gy);
+        const int x = bx * 32 + (threadIdx.x & 31), y = by * 4 + (threadIdx.x >> 5);
+        if (x >= nx || y >= ny) return;
+        const int z0 = bz * 64, z1 = min(z0 + 64, nz);
+        const size_t sz = (size_t)nx * ny;
+        const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
+        const float* in = a.in;
+        size_t f = (size_t)z0 * sz + (size_t)y * nx + x;
+        float zm = z0 > 0 ? __ldg(in + f - sz) : 0.f;
+        float c = __ldg(in + f);
+        for (int z = z0; z < z1; ++z, f += sz) {
+            float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
+            if (!ixy || z == 0 || z == nz - 1) {
+                a.out[f] = c;
+            } else {
+                float s = zm + zp;
+                s = s + __ldg(in + f - nx);
+                s = s + __ldg(in + f + nx);
+                s = s + __ldg(in + f - 1);
+                s = s + __ldg(in + f + 1);
+                a.out[f] = fmaf(a.c1, s, -(a.c0 * c));
+            }
+            zm = c;
+            c = zp;
+        }
+    }
+};
+
+// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks;
+// phase reduced to [-1/2, 1/2] turns before the MUFU sin/cos.
+struct BodyMRIQ {
+    using Params = kl_args_mriq;
+    using State = Empty;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        __shared__ float skx[256], sky[256], skz[256], sph[256];
+        const int i = (int)vb * 256 + threadIdx.x;
+        const bool live = i < a.num_x;
+        const float x = live ? __ldg(a.x + i) : 0.f, y = live ? __ldg(a.y + i) : 0.f,
+                    z = live ? __ldg(a.z + i) : 0.f;
+        float qr = 0.f, qi = 0.f;
+        const float two_pi = 6.28318530717958647692f;
+        for (int k0 = 0; k0 < a.num_k; k0 += 256) {
+            const int n = min(256, a.num_k - k0);
+            __syncthreads();
+            if ((int)threadIdx.x < n) {
+                skx[threadIdx.x] = __ldg(a.kx + k0 + threadIdx.x);
+                sky[threadIdx.x] = __ldg(a.ky + k0 + threadIdx.x);
+                skz[threadIdx.x] = __ldg(a.kz + k0 + threadIdx.x);
+                sph[threadIdx.x] = __ldg(a.phimag + k0 + threadIdx.x);
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int k = 0; k < n; ++k) {
+                float t = fmaf(skx[k], x, fmaf(sky[k], y, skz[k] * z));
+                t = t - rintf(t);
+                float s, c;
+                __sincosf(two_pi * t, &s, &c);
+                qr = fmaf(sph[k], c, qr);
+                qi = fmaf(sph[k], s, qi);
+            }
+        }
+        if (live) {
+            a.qr[i] = qr;
+            a.qi[i] = qi;
+        }
+    }
+};
+
+// BS (SDK BlackScholes): 128 threads x 5 float4 = 2560 options per block.
+__device__ __forceinline__ float cnd_f(float d) {
+    const float A1 = 0.31938153f, A2 = -0.356563782f, A3 = 1.781477937f, A4 = -1.821255978f,
+                A5 = 1.330274429f, RSQRT2PI = 0.39894228040143267793994605993438f;
+    float K = 1.0f / (1.0f + 0.2316419f * fabsf(d));
+    float c = RSQRT2PI * expf(-0.5f * d * d) * (K * (A1 + K * (A2 + K * (A3 + K * (A4 + K * A5)))));
+    return d > 0.f ? 1.0f - c : c;
+}
+__device__ __forceinline__ void bs_one(float S, float X, float T, float R, float V, float& call, float& put) {
+    float sqrtT = sqrtf(T);
+    float d1 = (logf(S / X) + (R + 0.5f * V * V) * T) / (V * sqrtT);
+    float d2 = d1 - V * sqrtT;
+    float c1 = cnd_f(d1), c2 = cnd_f(d2);
+    float e = expf(-R * T);
+    call = S * c1 - X * e * c2;
+    put = X * e * (1.0f - c2) - S * (1.0f - c1);
+}
+struct BodyBS {
+    using Params = kl_args_bs;
+    using State = Empty;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int64_t n4 = a.n / 4;
+        const float4* S = reinterpret_cast<const float4*>(a.S);
+        const float4* X = reinterpret_cast<const float4*>(a.X);
+        const float4* T = reinterpret_cast<const float4*>(a.T);
+        float4* C = reinterpret_cast<float4*>(a.call);
+        float4* P = reinterpret_cast<float4*>(a.put);
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            int64_t i = (int64_t)vb * 640 + j * 128 + threadIdx.x;
+            if (i >= n4) break;
+            float4 s = __ldg(S + i), x = __ldg(X + i), t = __ldg(T + i), c, p;
+            bs_one(s.x, x.x, t.x, a.R, a.V, c.x, p.x);
+            bs_one(s.y, x.y, t.y, a.R, a.V, c.y, p.y);
+            bs_one(s.z, x.z, t.z, a.R, a.V, c.z, p.z);
+            bs_one(s.w, x.w, t.w, a.R, a.V, c.w, p.w);
+            C[i] = c;
+            P[i] = p;
+        }
+    }
+};
+
+// TEA: 32 cycles per 64-bit block; uint4 = two blocks; 1280 blocks per thread block.
+__device__ __forceinline__ void tea_enc(uint32_t& v0, uint32_t& v1, uint32_t k0, uint32_t k1, uint32_t k2, uint32_t k3) {
+    uint32_t sum = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        sum += 0x9E3779B9u;
+        v0 += ((v1 << 4) + k0) ^ (v1 + sum) ^ ((v1 >> 5) + k1);
+        v1 += ((v0 << 4) + k2) ^ (v0 + sum) ^ ((v0 >> 5) + k3);
+    }
+}
+struct BodyTEA {
+    using Params = kl_args_tea;
+    using State = Empty;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int64_t n2 = a.n / 2;
+        const uint4* in = reinterpret_cast<const uint4*>(a.in);
+        uint4* out = reinterpret_cast<uint4*>(a.out);
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            int64_t i = (int64_t)vb * 640 + j * 128 + threadIdx.x;
+            if (i >= n2) break;
+            uint4 v = __ldg(in + i);
+            tea_enc(v.x, v.y, a.key[0], a.key[1], a.key[2], a.key[3]);
+            tea_enc(v.z, v.w, a.key[0], a.key[1], a.key[2], a.key[3]);
+            out[i] = v;
+        }
+    }
+};
+
+// MatrixAdd: 16x16 threads per block over a (n/16) x (n/16) grid.
+struct BodyMATADD {
+    using Params = kl_args_matadd;
+    using State = Empty;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int g = a.n / 16, bx = vb % g, by = vb / g;
+        const int i = (by * 16 + (threadIdx.x >> 4)) * a.n + bx * 16 + (threadIdx.x & 15);
+        a.C[i] = a.A[i] + a.B[i];
+    }
+};
+
+// Synthetic streaming kernel: 4 float4 per thread, `fmas` dependent FMAs each.
+struct BodySYNTH {
+    using Params = kl_args_synth;
+    using State = Empty;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    __device__ static void init(const Params&, State&, char*) {}
+    __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        const int64_t n4 = a.n / 4;
+        const float4* x = reinterpret_cast<const float4*>(a.x);
+        float4* y = reinterpret_cast<float4*>(a.y);
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t i = (int64_t)vb * 1024 + j * 256 + threadIdx.x;
+            v[j] = i < n4 ? __ldg(x + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int c = 0; c < a.fmas; ++c) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[j].x = fmaf(v[j].x, a.a, a.b); v[j].y = fmaf(v[j].y, a.a, a.b);
+                v[j].z = fmaf(v[j].z, a.a, a.b); v[j].w = fmaf(v[j].w, a.a, a.b);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t i = (int64_t)vb * 1024 + j * 256 + threadIdx.x;
+            if (i < n4) y[i] = v[j];
+        }
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+// Slice launcher.
+// ------------------------------------------------------------------------------------------
+// Stop the partner's current launch at its first slice boundary at or after its current
+// position (Alg.1 l.9: the co-schedule is kept only while both kernels still have blocks).
+__device__ void stop_at_boundary(KlCtl* p, uint32_t pstart, uint32_t pslice) {
+    unsigned long long old = atomicAdd(&p->word, 0ull);
+    for (;;) {
+        if (old >> 63) return;
+        uint32_t nx = (uint32_t)old;
+        uint32_t rel = nx > pstart ? nx - pstart : 0u;
+        uint32_t sl = pslice ? pslice : 1u;
+        unsigned long long sa = (unsigned long long)pstart + ((unsigned long long)(rel + sl - 1) / sl) * sl;
+        if (sa < nx) sa = nx;
+        if (sa > 0x7fffffffull) sa = 0x7fffffffull;
+        unsigned long long nw = (old & 0xffffffffull) | (sa << 32) | (1ull << 63);
+        unsigned long long prev = atomicCAS(&p->word, old, nw);
+        if (prev == old) return;
+        old = prev;
+    }
+}
+
+__device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
+    KlCtl* ctl = L.ctl;
+    __threadfence();
+    unsigned long long w = atomicAdd(&ctl->word, 0ull);
+    uint32_t lim = len;
+    if (w >> 63) lim = min(lim, (uint32_t)((w >> 32) & 0x7fffffffu));
+    uint32_t executed = atomicExch(&ctl->executed, 0u);
+    uint32_t admitted = atomicExch(&ctl->admitted, 0u);
+    uint32_t mx = 0;
+    for (uint32_t s = 0; s < L.n_sms && s < KL_MAX_SMS; ++s) {
+        mx = max(mx, ctl->sm_hwm[s]);
+        ctl->sm_hwm[s] = 0;
+    }
+    unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
+    unsigned long long t1 = gtimer();
+    atomicExch(&ctl->word, (unsigned long long)lim);   // next = lim, stop cleared
+    atomicExch(&ctl->exited, 0u);
+    const bool exh = (lim == len);
+    if (L.counters) {
+        atomicAdd(&L.counters[1], (unsigned long long)executed);
+        if (exh) {
+            atomicAdd(&L.counters[0], 1ull);
+            atomicAdd(&L.counters[4], L.tag);
+        }
+        if (admitted) atomicMin(reinterpret_cast<long long*>(&L.counters[2]), (long long)t0);
+        atomicMax(reinterpret_cast<long long*>(&L.counters[3]), (long long)t1);
+    }
+    KlLaunchRec* r = L.rec;
+    if (r) {
+        r->end = lim;
+        r->exhausted = exh ? 1u : 0u;
+        r->executed = executed;
+        r->admitted = admitted;
+        r->max_per_sm = mx;
+        r->t0 = t0;
+        r->t1 = t1;
+        __threadfence_system();
+        r->done = 1u;
+        __threadfence_system();
+    }
+}
+
+template <class Body>
+__global__ void __launch_bounds__(Body::kThreads)
+k_persistent(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
+    extern __shared__ __align__(1024) char dsmem[];
+    __shared__ uint32_t s_vb[2], s_end[2], s_adm;
+    KlCtl* ctl = L.ctl;
+    const uint32_t len = ctl->len;
+    uint32_t sm = 0;
+    if (threadIdx.x == 0) {
+        uint32_t adm = 1;
+        sm = smid_u32();
+        if (L.cap) {
+            uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
+            if (c >= L.cap) {
+                atomicSub(&ctl->sm_count[sm], 1u);
+                adm = 0;
+            } else {
+                atomicMax(&ctl->sm_hwm[sm], c + 1);
+            }
+        }
+        if (adm) {
+            atomicAdd(&ctl->admitted, 1u);
+            atomicMin(&ctl->t0, gtimer());
+        }
+        s_adm = adm;
+    }
+    __syncthreads();
+    if (s_adm) {
+        typename Body::State st;
+        Body::init(P, st, dsmem);
+        uint32_t nexec = 0;
+        for (uint32_t it = 0;; ++it) {
+            if (threadIdx.x == 0) {
+                unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                uint32_t vb = (uint32_t)old;
+                uint32_t lim = len;
+                if (old >> 63) lim = min(lim, (uint32_t)((old >> 32) & 0x7fffffffu));
+                uint32_t end = vb < lim ? min(vb + L.chunk, lim) : vb;
+                if (vb >= len && lim == len && L.partner) {
+                    if (atomicCAS(&ctl->drained, 0u, 1u) == 0u)
+                        stop_at_boundary(L.partner, L.partner_start, L.partner_slice);
+                }
+                s_vb[it & 1] = vb;
+                s_end[it & 1] = end;
+            }
+            __syncthreads();
+            const uint32_t vb = s_vb[it & 1], end = s_end[it & 1];
+            if (vb >= end) break;
+            for (uint32_t v = vb; v < end; ++v) {
+                Body::block(P, st, dsmem, v);
+                if (L.audit && threadIdx.x == 0) atomicAdd(L.audit + v, 1u);
+            }
+            nexec += end - vb;
+        }
+        Body::fini(P, st, dsmem);
+        if (threadIdx.x == 0) {
+            atomicAdd(&ctl->executed, nexec);
+            if (L.cap) atomicSub(&ctl->sm_count[sm], 1u);
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        uint32_t e = atomicAdd(&ctl->exited, 1u);
+        if (e == gridDim.x - 1) finalize_launch(L, len);
+    }
+}
+
+// Plain grid: blockIdx rectified by the slice offset.
+template <class Body>
+__global__ void __launch_bounds__(Body::kThreads)
+k_plain(const __grid_constant__ typename Body::Params P, uint32_t offset) {
+    extern __shared__ __align__(1024) char dsmem[];
+    typename Body::State st;
+    Body::init(P, st, dsmem);
+    Body::block(P, st, dsmem, offset + blockIdx.x);
+    Body::fini(P, st, dsmem);
+}
+
+template <class Body>
+int info_of(KlKindInfo* o) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_persistent<Body>);
+    if (e != cudaSuccess) return (int)e;
+    if (Body::kDynSmem > 48 * 1024) {
+        e = cudaFuncSetAttribute(k_persistent<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaFuncSetAttribute(k_plain<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
+        if (e != cudaSuccess) return (int)e;
+    }
+    int nb = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<Body>, Body::kThreads, Body::kDynSmem);
+    if (e != cudaSuccess) return (int)e;
+    o->threads = Body::kThreads;
+    o->dyn_smem = Body::kDynSmem;
+    o->regs = fa.numRegs;
+    o->static_smem = (int)fa.sharedSizeBytes;
+    o->tmem_cols = 0;
+    o->bmax = nb;
+    o->default_chunk = Body::kChunk;
+    return 0;
+}
+
+template <class Body>
+int launch_persistent(const void* blob, const KlLaunch& L, uint32_t grid, void* stream) {
+    const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
+    k_persistent<Body><<<grid, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, L);
+    return (int)cudaGetLastError();
+}
+
+template <class Body>
+int launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream) {
+    const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
+    if (n == 0) return 0;
+    k_plain<Body><<<n, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, offset);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+// MM lives in kl_mm.cu (tcgen05); these are its entry points.
+int kl_mm_info(KlKindInfo* o);
+int kl_mm_prepare(const void* args, uint32_t bytes, void* blob, uint32_t cap);
+int kl_mm_launch_persistent(const void* blob, const KlLaunch& L, uint32_t grid, void* stream);
+int kl_mm_launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream);
+
+#define KL_DISPATCH(kind, FN, ...)                                   \
+    switch (kind) {                                                  \
+        case KL_PC: return FN<BodyPC>(__VA_ARGS__);                  \
+        case KL_SAD: return FN<BodySAD>(__VA_ARGS__);                \
+        case KL_SPMV: return FN<BodySPMV>(__VA_ARGS__);              \
+        case KL_ST: return FN<BodyST>(__VA_ARGS__);                  \
+        case KL_MRIQ: return FN<BodyMRIQ>(__VA_ARGS__);              \
+        case KL_BS: return FN<BodyBS>(__VA_ARGS__);                  \
+        case KL_TEA: return FN<BodyTEA>(__VA_ARGS__);                \
+        case KL_MATADD: return FN<BodyMATADD>(__VA_ARGS__);          \
+        case KL_SYNTH: return FN<BodySYNTH>(__VA_ARGS__);            \
+        default: return -1;                                          \
+    }
+
+static const uint32_t kArgBytes[KL_NKINDS] = {
+    sizeof(kl_args_pc), sizeof(kl_args_sad), sizeof(kl_args_spmv), sizeof(kl_args_st),
+    sizeof(kl_args_mm), sizeof(kl_args_mriq), sizeof(kl_args_bs), sizeof(kl_args_tea),
+    sizeof(kl_args_matadd), sizeof(kl_args_synth)};
+
+uint32_t kl_args_size(int kind) { return (kind >= 0 && kind < KL_NKINDS) ? kArgBytes[kind] : 0u; }
+
+int kl_dev_kind_info(int kind, KlKindInfo* out) {
+    if (kind == KL_MM) return kl_mm_info(out);
+    KL_DISPATCH(kind, info_of, out);
+}
+
+int kl_dev_prepare(int kind, const void* args, uint32_t bytes, void* blob, uint32_t cap) {
+    if (kind < 0 || kind >= KL_NKINDS || bytes != kArgBytes[kind]) return -1;
+    if (kind == KL_MM) return kl_mm_prepare(args, bytes, blob, cap);
+    if (bytes > cap) return -1;
+    std::memcpy(blob, args, bytes);
+    return 0;
+}
+
+int kl_dev_launch_persistent(int kind, const void* blob, const KlLaunch& L, uint32_t grid, void* stream) {
+    if (kind == KL_MM) return kl_mm_launch_persistent(blob, L, grid, stream);
+    KL_DISPATCH(kind, launch_persistent, blob, L, grid, stream);
+}
+
+int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n, void* stream) {
+    if (kind == KL_MM) return kl_mm_launch_plain(blob, offset, n, stream);
+    KL_DISPATCH(kind, launch_plain, blob, offset, n, stream);
+}
+
+// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
+__global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        KlCtl* c = pool + slots_lens[2 * i];
+        c->word = 0ull;
+        c->len = slots_lens[2 * i + 1];
+        c->exited = 0;
+        c->drained = 0;
+        c->admitted = 0;
+        c->executed = 0;
+        c->t0 = ~0ull;
+    }
+}
+
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream) {
+    if (n <= 0) return 0;
+    k_ctl_init<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pool, slots_lens, n);
+    return (int)cudaGetLastError();
+}

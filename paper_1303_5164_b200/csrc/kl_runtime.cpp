@@ -1,0 +1,902 @@
+// kl_runtime.cpp -- host runtime behind include/kl.h (product path).
+//
+// Implements Alg.1 and Proc. FindCoSchedule over the pending set R:
+//   candidate pairs -> PUR/MUR pruning (AND reading R9, halving R10/R24)
+//   -> maximal occupancy splits (a5, R7) -> batched device model (kl_model.cu, cached per
+//   (kind1, kind2, b1, b2)) -> selection a9 (device-fused on a cache miss, host otherwise; the
+//   two are the same rules) -> one co-schedule phase on two lanes (streams) of persistent slice
+//   launchers (kl_kernels.cu), retired when both lanes report through host-mapped records.
+#include <cuda_runtime.h>
+#include <immintrin.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kl_internal.h"
+
+uint32_t kl_args_size(int kind);
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream);
+
+namespace {
+
+constexpr int kCtlPool = 16384;
+constexpr int kBlob = 512;
+constexpr int kMaxCand = 8192;
+
+// Pre-calibration defaults of the model inputs per kind (replaced by the B200 ncu calibration,
+// profiles/kl_profile_b200.json, passed through kl_config.profiles).  PUR/MUR default to the
+// paper's C2050 values (tb:benchmarks).
+const kl_profile kDefaultProfiles[KL_NKINDS] = {
+    /* PC   */ {0.25, 32.0, 720.0, 0.0096, 0.1404, 0, 0, 0, 0, 0, 1},
+    /* SAD  */ {0.03, 4.0, 3600.0, 0.1498, 0.1120, 0, 0, 0, 0, 0, 1},
+    /* SPMV */ {0.30, 8.0, 200.0, 0.3464, 0.003, 0, 0, 0, 0, 0, 1},
+    /* ST   */ {0.15, 4.0, 3072.0, 0.3629, 0.1156, 0, 0, 0, 0, 0, 1},
+    /* MM   */ {0.01, 1.0, 12000.0, 0.5804, 0.0161, 0, 0, 0, 0, 0, 1},
+    /* MRIQ */ {0.001, 1.0, 196608.0, 0.8539, 0.0002, 0, 0, 0, 0, 0, 1},
+    /* BS   */ {0.03, 16.0, 4800.0, 0.8642, 0.0604, 0, 0, 0, 0, 0, 1},
+    /* TEA  */ {0.01, 16.0, 15360.0, 0.9978, 0.0196, 0, 0, 0, 0, 0, 1},
+    /* MATADD*/ {0.30, 4.0, 80.0, 0.1, 0.1, 0, 0, 0, 0, 0, 1},
+    /* SYNTH*/ {0.10, 16.0, 320.0, 0.5, 0.5, 0, 0, 0, 0, 0, 1},
+};
+
+struct Inst {
+    uint64_t id = 0, seq = 0, tag = 0;
+    int kind = 0;
+    uint32_t grid = 0;
+    alignas(128) unsigned char blob[kBlob];
+    int slot = -1;
+    uint32_t next = 0;
+    bool done = false;
+    uint32_t* audit = nullptr;
+};
+
+struct Lane {
+    cudaStream_t s = nullptr;
+    bool own = false;
+    KlLaunchRec* rec = nullptr;
+    Inst* inst = nullptr;
+    uint32_t cap = 0, slice = 0, start = 0;
+    int partner_kind = -1;
+};
+
+struct Decision {
+    bool solo = true;
+    int ia = 0, ib = -1;            // indices into R
+    uint32_t b1 = 0, b2 = 0;
+    double cp = 0.0;
+    int n_cand = 0;
+};
+
+inline double band(double x, double y) { return 1e-12 * std::max(1.0, std::max(std::fabs(x), std::fabs(y))); }
+
+inline uint64_t cache_key(int k1, int k2, uint32_t b1, uint32_t b2) {
+    return (((uint64_t)k1 * 16 + (uint64_t)k2) * 1024 + b1) * 1024 + b2;
+}
+
+}  // namespace
+
+struct kl_ctx {
+    int device = -1;
+    bool host_only = true, poisoned = false;
+    std::string err;
+    kl_config cfg{};
+    kl_profile prof[KL_NKINDS]{};
+    KlKindInfo info[KL_NKINDS]{};
+    bool info_ok[KL_NKINDS]{};
+    int n_sms = 148, max_warps = 64, max_blocks = 32, max_regs = 65536, max_smem = 233472;
+    Lane lane[2];
+    cudaStream_t ctrl = nullptr;
+    cudaEvent_t init_ev = nullptr;
+    KlCtl* ctl_pool = nullptr;
+    std::vector<int> free_slots;
+    uint32_t* init_pinned = nullptr;   // mapped (slot, len) pairs awaiting k_ctl_init
+    int n_init = 0;
+    std::vector<std::unique_ptr<Inst>> insts;
+    std::unordered_map<uint64_t, Inst*> by_id;
+    std::vector<Inst*> R;              // pending set, arrival order (Alg.1 l.1)
+    uint64_t next_id = 1, seq = 0;
+    // model batch buffers
+    KlModelKind* mk_pinned = nullptr;
+    KlModelKind* mk_dev = nullptr;
+    KlCand* cand_pinned = nullptr;
+    KlCand* cand_dev = nullptr;
+    int32_t* off_pinned = nullptr;
+    int32_t* off_dev = nullptr;
+    kl_prediction* pred_dev = nullptr;
+    kl_prediction* pred_pinned = nullptr;
+    uint32_t* done_dev = nullptr;
+    KlDecision* dec_dev = nullptr;
+    KlDecision* dec_pinned = nullptr;
+    std::unordered_map<uint64_t, kl_prediction> cache;
+    int64_t model_batches = 0, model_cands = 0;
+    // phases
+    bool in_flight = false;
+    int64_t phases = 0;
+    double phase_cp = 0.0;
+    std::vector<kl_trace_rec> trace;
+    int64_t* counters = nullptr;
+
+    kl_status fail(kl_status st, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        if (st == KL_ECUDA) poisoned = true;
+        return st;
+    }
+};
+
+#define KL_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return ctx->fail(KL_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+#define KL_LIVE(ctx)                                                                         \
+    do {                                                                                     \
+        if (!(ctx)) return KL_EINVAL;                                                        \
+        if ((ctx)->poisoned) return KL_ECUDA;                                                \
+    } while (0)
+
+namespace {
+
+// ---- occupancy (a5) -------------------------------------------------------------
+// 0 fits, else 1 warps | 2 blocks | 3 registers | 4 smem | 5 TMEM
+int fits(const kl_ctx* c, const kl_profile& p1, uint32_t b1, const kl_profile* p2, uint32_t b2) {
+    const kl_profile* ps[2] = {&p1, p2};
+    uint32_t bs[2] = {b1, b2};
+    long warps = 0, blocks = 0, regs = 0, smem = 0, tmem = 0;
+    for (int i = 0; i < 2; ++i) {
+        if (!ps[i] || bs[i] == 0) continue;
+        long rw = ((long)ps[i]->regs * 32 + 255) / 256 * 256;
+        warps += (long)bs[i] * ps[i]->wpb;
+        blocks += bs[i];
+        regs += (long)bs[i] * ps[i]->wpb * rw;
+        smem += (long)bs[i] * (ps[i]->smem + 1024);
+        tmem += (long)bs[i] * ps[i]->tmem;
+    }
+    if (warps > c->max_warps) return 1;
+    if (blocks > c->max_blocks) return 2;
+    if (regs > c->max_regs) return 3;
+    if (smem > c->max_smem) return 4;
+    if (tmem > 512) return 5;
+    return 0;
+}
+
+// Candidate blocks-per-SM levels (a5; R14): whole warps per virtual SM.
+std::vector<uint32_t> levels(const kl_ctx* c, const kl_profile& p) {
+    std::vector<uint32_t> ok, out;
+    const int ns = c->cfg.n_sched;
+    for (int b = 1; b <= p.bmax; ++b)
+        if ((b * p.wpb) % ns == 0) ok.push_back((uint32_t)b);
+    if (c->cfg.level_mode == 0) return ok;
+    for (int q = 1; q <= 4; ++q) {
+        int t = (q * p.bmax + 3) / 4;
+        for (uint32_t b : ok)
+            if ((int)b >= t) {
+                if (std::find(out.begin(), out.end(), b) == out.end()) out.push_back(b);
+                break;
+            }
+    }
+    return out;
+}
+
+uint32_t solo_level(const kl_ctx* c, const kl_profile& p) {
+    std::vector<uint32_t> l;
+    const int ns = c->cfg.n_sched;
+    for (int b = p.bmax; b >= 1; --b)
+        if ((b * p.wpb) % ns == 0) return (uint32_t)b;
+    return 0;
+}
+
+// Maximal feasible splits (R7): feasible (b1,b2) not dominated by another feasible level pair.
+std::vector<std::pair<uint32_t, uint32_t>> maximal_splits(const kl_ctx* c, const kl_profile& p1, const kl_profile& p2) {
+    auto l1 = levels(c, p1), l2 = levels(c, p2);
+    std::vector<std::pair<uint32_t, uint32_t>> feas, out;
+    for (uint32_t a : l1)
+        for (uint32_t b : l2)
+            if (fits(c, p1, a, &p2, b) == 0) feas.push_back({a, b});
+    for (auto& f : feas) {
+        bool dom = false;
+        for (auto& g : feas)
+            if (g != f && g.first >= f.first && g.second >= f.second) { dom = true; break; }
+        if (!dom) out.push_back(f);
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+bool pruned(const kl_profile& a, const kl_profile& b, double ap, double am) {
+    return std::fabs(a.pur - b.pur) < ap && std::fabs(a.mur - b.mur) < am;   // R9: AND, strict
+}
+
+bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb) {
+    double t = band(a.dT, b.dT);
+    if (a.dT < b.dT - t) return true;
+    if (a.dT > b.dT + t) return false;
+    t = band(a.c, b.c);
+    if (a.c > b.c + t) return true;
+    if (a.c < b.c - t) return false;
+    if (ca.warps != cb.warps) return ca.warps > cb.warps;
+    return ca.b1 < cb.b1;
+}
+
+void fill_model_kinds(kl_ctx* c) {
+    for (int k = 0; k < KL_NKINDS; ++k) {
+        const kl_profile& p = c->prof[k];
+        KlModelKind m{};
+        m.rm = p.rm;
+        m.r = p.r;
+        m.ipb = p.ipb;
+        m.wpb = p.wpb;
+        m.bsolo = (int)solo_level(c, p);
+        c->mk_pinned[k] = m;
+    }
+}
+
+KlModelCfg model_cfg(const kl_ctx* c, int n) {
+    KlModelCfg m{};
+    m.L0 = c->cfg.L0;
+    m.B = c->cfg.B;
+    m.a0 = c->cfg.a0;
+    m.b0 = c->cfg.b0;
+    m.W = 64 / c->cfg.n_sched;   // virtual SM warps
+    m.n_sched = c->cfg.n_sched;
+    m.latency_mode = c->cfg.latency_mode;
+    m.n_cand = n;
+    return m;
+}
+
+// Run the device model over cand_pinned[0..n); n_pairs > 0 fuses the selection.
+kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
+    if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
+    fill_model_kinds(ctx);
+    KL_CUDA(cudaMemcpyAsync(ctx->mk_dev, ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaMemcpyHostToDevice, ctx->ctrl));
+    KL_CUDA(cudaMemcpyAsync(ctx->cand_dev, ctx->cand_pinned, sizeof(KlCand) * n, cudaMemcpyHostToDevice, ctx->ctrl));
+    if (n_pairs > 0)
+        KL_CUDA(cudaMemcpyAsync(ctx->off_dev, ctx->off_pinned, sizeof(int32_t) * (n_pairs + 1), cudaMemcpyHostToDevice, ctx->ctrl));
+    int rc = kl_dev_model_batch(ctx->mk_dev, model_cfg(ctx, n), ctx->cand_dev, ctx->pred_dev, n_pairs, ctx->off_dev,
+                                ctx->done_dev, ctx->dec_dev, ctx->ctrl);
+    if (rc) return ctx->fail(KL_ECUDA, "model batch launch: %s", cudaGetErrorString((cudaError_t)rc));
+    KL_CUDA(cudaMemcpyAsync(ctx->pred_pinned, ctx->pred_dev, sizeof(kl_prediction) * n, cudaMemcpyDeviceToHost, ctx->ctrl));
+    if (n_pairs > 0)
+        KL_CUDA(cudaMemcpyAsync(ctx->dec_pinned, ctx->dec_dev, sizeof(KlDecision), cudaMemcpyDeviceToHost, ctx->ctrl));
+    KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
+    ctx->model_batches++;
+    ctx->model_cands += n;
+    for (int i = 0; i < n; ++i) {
+        const KlCand& cd = ctx->cand_pinned[i];
+        ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)] = ctx->pred_pinned[i];
+    }
+    if (dec_out) *dec_out = *ctx->dec_pinned;
+    return KL_OK;
+}
+
+// Proc. FindCoSchedule over R.
+kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
+    *d = Decision{};
+    auto& R = ctx->R;
+    if (R.empty()) return ctx->fail(KL_ENOTFOUND, "nothing pending");
+    // representatives: first two instances of each kind, arrival order
+    std::vector<int> reps;
+    int seen_k[KL_NKINDS] = {0};
+    for (int i = 0; i < (int)R.size(); ++i)
+        if (seen_k[R[i]->kind] < 2) { reps.push_back(i); seen_k[R[i]->kind]++; }
+    std::vector<std::pair<int, int>> pairs;
+    bool seen_pair[KL_NKINDS][KL_NKINDS] = {};
+    for (size_t a = 0; a < reps.size(); ++a)
+        for (size_t b = a + 1; b < reps.size(); ++b) {
+            int ka = R[reps[a]]->kind, kb = R[reps[b]]->kind;
+            int lo = std::min(ka, kb), hi = std::max(ka, kb);
+            if (seen_pair[lo][hi]) continue;
+            seen_pair[lo][hi] = true;
+            pairs.push_back({reps[a], reps[b]});
+        }
+    // pruning with relaxation
+    double ap = ctx->cfg.alpha_p, am = ctx->cfg.alpha_m;
+    std::vector<std::pair<int, int>> keep;
+    for (int it = 0; it < 10; ++it) {
+        if (it == 9) ap = am = 0.0;
+        keep.clear();
+        for (auto& pq : pairs)
+            if (!pruned(ctx->prof[R[pq.first]->kind], ctx->prof[R[pq.second]->kind], ap, am)) keep.push_back(pq);
+        if (!keep.empty() || pairs.empty()) break;
+        ap *= 0.5;
+        am *= 0.5;
+    }
+    // candidates: maximal splits of each kept pair
+    int n = 0, np = 0;
+    bool missing = false;
+    std::vector<std::pair<int, int>> pair_of_group;
+    for (auto& pq : keep) {
+        const int k1 = R[pq.first]->kind, k2 = R[pq.second]->kind;
+        auto ms = maximal_splits(ctx, ctx->prof[k1], ctx->prof[k2]);
+        if (ms.empty()) continue;
+        ctx->off_pinned[np] = n;
+        for (auto& s : ms) {
+            if (n >= kMaxCand) return ctx->fail(KL_ENOMEM, "candidate space too large");
+            KlCand cd{};
+            cd.k1 = k1;
+            cd.k2 = k2;
+            cd.b1 = s.first;
+            cd.b2 = s.second;
+            cd.pair = np;
+            cd.warps = (int)s.first * ctx->prof[k1].wpb + (int)s.second * ctx->prof[k2].wpb;
+            ctx->cand_pinned[n++] = cd;
+            if (!ctx->cache.count(cache_key(k1, k2, s.first, s.second))) missing = true;
+        }
+        pair_of_group.push_back(pq);
+        ++np;
+    }
+    ctx->off_pinned[np] = n;
+    d->n_cand = n;
+    int best = -1;
+    double bcp = 0.0;
+    if (n > 0 && missing) {
+        if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context cannot run the model");
+        KlDecision dec{};
+        kl_status st = run_model(ctx, n, np, &dec);
+        if (st) return st;
+        best = dec.cand;
+        bcp = dec.cp;
+    } else if (n > 0) {
+        // host selection with the same rules as the fused device selection
+        for (int p = 0; p < np; ++p) {
+            int bi = -1;
+            kl_prediction bp{};
+            for (int i = ctx->off_pinned[p]; i < ctx->off_pinned[p + 1]; ++i) {
+                const KlCand& cd = ctx->cand_pinned[i];
+                const kl_prediction& a = ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)];
+                if (a.status != 0) continue;
+                if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi])) { bi = i; bp = a; }
+            }
+            if (bi < 0) continue;
+            if (best < 0 || bp.cp > bcp + band(bp.cp, bcp)) { best = bi; bcp = bp.cp; }
+        }
+        if (best >= 0 && !(bcp > 1e-12)) best = -1;
+    }
+    if (best < 0) {   // solo: oldest pending kernel at its solo maximum occupancy (R25)
+        d->solo = true;
+        d->ia = 0;
+        d->b1 = solo_level(ctx, ctx->prof[R[0]->kind]);
+        d->cp = 0.0;
+        return KL_OK;
+    }
+    const KlCand& cd = ctx->cand_pinned[best];
+    d->solo = false;
+    d->ia = pair_of_group[cd.pair].first;
+    d->ib = pair_of_group[cd.pair].second;
+    d->b1 = cd.b1;
+    d->b2 = cd.b2;
+    d->cp = bcp;
+    return KL_OK;
+}
+
+uint32_t slice_of(const kl_ctx* c, const kl_profile& p, uint32_t b, int m) {
+    return (uint32_t)std::max(1, m) * b * (uint32_t)c->n_sms;
+}
+
+kl_status flush_ctl_init(kl_ctx* ctx) {
+    if (ctx->n_init == 0) return KL_OK;
+    int rc = kl_dev_ctl_init(ctx->ctl_pool, ctx->init_pinned, ctx->n_init, ctx->ctrl);
+    if (rc) return ctx->fail(KL_ECUDA, "ctl init: %s", cudaGetErrorString((cudaError_t)rc));
+    KL_CUDA(cudaEventRecord(ctx->init_ev, ctx->ctrl));
+    KL_CUDA(cudaStreamWaitEvent(ctx->lane[0].s, ctx->init_ev, 0));
+    KL_CUDA(cudaStreamWaitEvent(ctx->lane[1].s, ctx->init_ev, 0));
+    // the mapped init list is read by the kernel: wait before it can be overwritten
+    KL_CUDA(cudaEventSynchronize(ctx->init_ev));
+    ctx->n_init = 0;
+    return KL_OK;
+}
+
+kl_status launch_lane(kl_ctx* ctx, int li, Inst* k, uint32_t cap, uint32_t slice, Inst* partner,
+                      uint32_t partner_slice, double cp) {
+    Lane& ln = ctx->lane[li];
+    const KlKindInfo& inf = ctx->info[k->kind];
+    KlLaunch L{};
+    L.ctl = ctx->ctl_pool + k->slot;
+    L.partner = partner ? ctx->ctl_pool + partner->slot : nullptr;
+    L.cap = cap;
+    L.chunk = (uint32_t)(ctx->cfg.chunk > 0 ? ctx->cfg.chunk : inf.default_chunk);
+    L.start = k->next;
+    L.partner_start = partner ? partner->next : 0;
+    L.partner_slice = partner_slice;
+    L.n_sms = (uint32_t)ctx->n_sms;
+    L.rec = ln.rec;
+    L.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
+    L.audit = k->audit;
+    L.tag = k->tag;
+    const uint32_t per_sm = cap ? cap : (uint32_t)inf.bmax;
+    uint32_t grid = per_sm * (uint32_t)ctx->n_sms;
+    const uint32_t remaining = k->grid - k->next;
+    if (grid > remaining) grid = std::max(1u, remaining);
+    ln.rec->done = 0;
+    ln.inst = k;
+    ln.cap = cap;
+    ln.slice = slice;
+    ln.start = k->next;
+    ln.partner_kind = partner ? partner->kind : -1;
+    int rc = kl_dev_launch_persistent(k->kind, k->blob, L, grid, ln.s);
+    if (rc) return ctx->fail(KL_ECUDA, "launch kind %d: %s", k->kind, cudaGetErrorString((cudaError_t)rc));
+    (void)cp;
+    return KL_OK;
+}
+
+kl_status retire_phase(kl_ctx* ctx) {
+    if (!ctx->in_flight) return KL_OK;
+    for (int li = 0; li < 2; ++li) {
+        Lane& ln = ctx->lane[li];
+        if (!ln.inst) continue;
+        uint64_t spins = 0;
+        while (!ln.rec->done) {
+            _mm_pause();
+            if ((++spins & 0xFFFF) == 0) {
+                cudaError_t e = cudaStreamQuery(ln.s);
+                if (e != cudaSuccess && e != cudaErrorNotReady)
+                    return ctx->fail(KL_ECUDA, "phase %lld lane %d: %s", (long long)ctx->phases, li, cudaGetErrorString(e));
+                if (e == cudaSuccess && !ln.rec->done)
+                    return ctx->fail(KL_ECUDA, "phase %lld lane %d finished without a record", (long long)ctx->phases, li);
+            }
+        }
+    }
+    for (int li = 0; li < 2; ++li) {
+        Lane& ln = ctx->lane[li];
+        if (!ln.inst) continue;
+        Inst* k = ln.inst;
+        const KlLaunchRec& r = *ln.rec;
+        kl_trace_rec t{};
+        t.id = k->id;
+        t.kind = k->kind;
+        t.lane = li;
+        t.cap = ln.cap;
+        t.slice = ln.slice;
+        t.start = ln.start;
+        t.end = r.end;
+        t.executed = r.executed;
+        t.admitted = r.admitted;
+        t.max_per_sm = r.max_per_sm;
+        t.exhausted = r.exhausted;
+        t.t0_ns = (int64_t)r.t0;
+        t.t1_ns = (int64_t)r.t1;
+        t.phase = (int32_t)ctx->phases;
+        t.partner_kind = ln.partner_kind;
+        t.cp = ctx->phase_cp;
+        ctx->trace.push_back(t);
+        k->next = r.end;
+        if (r.exhausted) {
+            k->done = true;
+            ctx->free_slots.push_back(k->slot);
+        }
+        ln.inst = nullptr;
+    }
+    auto& R = ctx->R;
+    R.erase(std::remove_if(R.begin(), R.end(), [](Inst* k) { return k->done; }), R.end());
+    ctx->in_flight = false;
+    ctx->phases++;
+    return KL_OK;
+}
+
+kl_status launch_phase(kl_ctx* ctx, const Decision& d, kl_coschedule* out) {
+    kl_status st = flush_ctl_init(ctx);
+    if (st) return st;
+    Inst* k1 = ctx->R[d.ia];
+    Inst* k2 = d.solo ? nullptr : ctx->R[d.ib];
+    const kl_profile& p1 = ctx->prof[k1->kind];
+    int m = std::max(1, p1.m_min);
+    if (k2) m = std::max(m, ctx->prof[k2->kind].m_min);
+    const uint32_t s1 = slice_of(ctx, p1, d.b1, m);
+    const uint32_t s2 = k2 ? slice_of(ctx, ctx->prof[k2->kind], d.b2, m) : 0;
+    ctx->phase_cp = d.cp;
+    if (k2) {
+        st = launch_lane(ctx, 0, k1, d.b1, s1, k2, s2, d.cp);
+        if (!st) st = launch_lane(ctx, 1, k2, d.b2, s2, k1, s1, d.cp);
+    } else {
+        st = launch_lane(ctx, 0, k1, 0, s1, nullptr, 0, 0.0);
+    }
+    if (st) return st;
+    ctx->in_flight = true;
+    if (out) {
+        *out = kl_coschedule{};
+        out->id1 = k1->id;
+        out->id2 = k2 ? k2->id : 0;
+        out->kind1 = k1->kind;
+        out->kind2 = k2 ? k2->kind : -1;
+        out->b1 = d.b1;
+        out->b2 = d.b2;
+        out->size1 = s1;
+        out->size2 = s2;
+        out->cp = d.cp;
+        out->solo = d.solo ? 1 : 0;
+        out->n_candidates = d.n_cand;
+    }
+    return KL_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+int kl_abi_version(void) { return KL_ABI_VERSION; }
+
+int kl_struct_sizes(uint32_t* out, int n) {
+    const uint32_t s[] = {sizeof(kl_config), sizeof(kl_profile), sizeof(kl_kernel_desc), sizeof(kl_slice_plan),
+                          sizeof(kl_candidate), sizeof(kl_prediction), sizeof(kl_coschedule), sizeof(kl_counters),
+                          sizeof(kl_trace_rec), sizeof(kl_args_pc), sizeof(kl_args_sad), sizeof(kl_args_spmv),
+                          sizeof(kl_args_st), sizeof(kl_args_mm), sizeof(kl_args_mriq), sizeof(kl_args_bs),
+                          sizeof(kl_args_tea), sizeof(kl_args_matadd), sizeof(kl_args_synth)};
+    int m = (int)(sizeof(s) / sizeof(s[0]));
+    if (n < m) m = n;
+    for (int i = 0; i < m; ++i) out[i] = s[i];
+    return m;
+}
+
+kl_status kl_config_default(kl_config* c) {
+    if (!c) return KL_EINVAL;
+    *c = kl_config{};
+    c->alpha_p = 0.4;          // P:1503-1504 (C2050 defaults)
+    c->alpha_m = 0.1;
+    c->p_percent = 2.0;
+    c->L0 = 800.0;             // cycles; calibrated on B200
+    c->B = 0.26;               // 32-B sectors per cycle per virtual SM at 1.34 GHz
+    c->a0 = 1.0;
+    c->b0 = 0.0;
+    c->n_sched = 4;            // B200: 4 SMSPs per SM -> W_v = 16
+    return KL_OK;
+}
+
+const char* kl_last_error(const kl_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
+    if (!out) return KL_EINVAL;
+    *out = nullptr;
+    auto ctx = std::make_unique<kl_ctx>();
+    if (cfg_in) ctx->cfg = *cfg_in;
+    else kl_config_default(&ctx->cfg);
+    kl_config& cfg = ctx->cfg;
+    if (cfg.n_sched <= 0 || 64 % cfg.n_sched) return KL_EINVAL;
+    for (int k = 0; k < KL_NKINDS; ++k) ctx->prof[k] = cfg.profiles ? cfg.profiles[k] : kDefaultProfiles[k];
+    cfg.profiles = nullptr;
+    ctx->device = device;
+    ctx->host_only = device < 0;
+    if (!ctx->host_only) {
+        kl_ctx* c = ctx.get();
+        {
+            kl_ctx* ctx = c;   // for KL_CUDA
+            KL_CUDA(cudaSetDevice(device));
+            cudaDeviceProp prop;
+            KL_CUDA(cudaGetDeviceProperties(&prop, device));
+            ctx->n_sms = prop.multiProcessorCount;
+            ctx->max_warps = prop.maxThreadsPerMultiProcessor / 32;
+            ctx->max_blocks = prop.maxBlocksPerMultiProcessor;
+            ctx->max_regs = prop.regsPerMultiprocessor;
+            ctx->max_smem = (int)prop.sharedMemPerMultiprocessor;
+            if (ctx->n_sms > KL_MAX_SMS) return KL_EINVAL;
+            for (int k = 0; k < KL_NKINDS; ++k) {
+                int rc = kl_dev_kind_info(k, &ctx->info[k]);
+                ctx->info_ok[k] = (rc == 0);
+                if (rc && rc != -2) {
+                    cudaGetLastError();
+                }
+                if (ctx->info_ok[k]) {
+                    kl_profile& p = ctx->prof[k];
+                    const KlKindInfo& in = ctx->info[k];
+                    if (!p.wpb) p.wpb = in.threads / 32;
+                    if (!p.regs) p.regs = in.regs;
+                    if (!p.smem) p.smem = in.static_smem + in.dyn_smem;
+                    if (!p.tmem) p.tmem = in.tmem_cols;
+                    if (!p.bmax) p.bmax = in.bmax;
+                }
+            }
+            for (int li = 0; li < 2; ++li) {
+                void* s = li == 0 ? cfg.stream_a : cfg.stream_b;
+                if (s) {
+                    ctx->lane[li].s = (cudaStream_t)s;
+                } else {
+                    KL_CUDA(cudaStreamCreateWithFlags(&ctx->lane[li].s, cudaStreamNonBlocking));
+                    ctx->lane[li].own = true;
+                }
+                KL_CUDA(cudaHostAlloc(&ctx->lane[li].rec, sizeof(KlLaunchRec), cudaHostAllocMapped));
+                std::memset(ctx->lane[li].rec, 0, sizeof(KlLaunchRec));
+            }
+            KL_CUDA(cudaStreamCreateWithFlags(&ctx->ctrl, cudaStreamNonBlocking));
+            KL_CUDA(cudaEventCreateWithFlags(&ctx->init_ev, cudaEventDisableTiming));
+            KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
+            KL_CUDA(cudaMemset(ctx->ctl_pool, 0, sizeof(KlCtl) * kCtlPool));
+            KL_CUDA(cudaHostAlloc(&ctx->init_pinned, sizeof(uint32_t) * 2 * kCtlPool, cudaHostAllocMapped));
+            KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocDefault));
+            KL_CUDA(cudaMalloc(&ctx->mk_dev, sizeof(KlModelKind) * KL_NKINDS));
+            KL_CUDA(cudaHostAlloc(&ctx->cand_pinned, sizeof(KlCand) * kMaxCand, cudaHostAllocDefault));
+            KL_CUDA(cudaMalloc(&ctx->cand_dev, sizeof(KlCand) * kMaxCand));
+            KL_CUDA(cudaHostAlloc(&ctx->off_pinned, sizeof(int32_t) * (kMaxCand + 1), cudaHostAllocDefault));
+            KL_CUDA(cudaMalloc(&ctx->off_dev, sizeof(int32_t) * (kMaxCand + 1)));
+            KL_CUDA(cudaMalloc(&ctx->pred_dev, sizeof(kl_prediction) * kMaxCand));
+            KL_CUDA(cudaHostAlloc(&ctx->pred_pinned, sizeof(kl_prediction) * kMaxCand, cudaHostAllocDefault));
+            KL_CUDA(cudaMalloc(&ctx->done_dev, sizeof(uint32_t)));
+            KL_CUDA(cudaMemset(ctx->done_dev, 0, sizeof(uint32_t)));
+            KL_CUDA(cudaMalloc(&ctx->dec_dev, sizeof(KlDecision)));
+            KL_CUDA(cudaHostAlloc(&ctx->dec_pinned, sizeof(KlDecision), cudaHostAllocDefault));
+        }
+    } else {
+        ctx->cand_pinned = new KlCand[kMaxCand];
+        ctx->off_pinned = new int32_t[kMaxCand + 1];
+    }
+    if (cfg.max_regs_per_sm) ctx->max_regs = cfg.max_regs_per_sm;
+    if (cfg.max_smem_per_sm) ctx->max_smem = cfg.max_smem_per_sm;
+    if (cfg.max_warps_per_sm) ctx->max_warps = cfg.max_warps_per_sm;
+    if (cfg.max_blocks_per_sm) ctx->max_blocks = cfg.max_blocks_per_sm;
+    if (cfg.n_sms > 0) ctx->n_sms = cfg.n_sms;
+    ctx->counters = cfg.counters_dev;
+    for (int s = kCtlPool - 1; s >= 0; --s) ctx->free_slots.push_back(s);
+    *out = ctx.release();
+    return KL_OK;
+}
+
+kl_status kl_destroy(kl_ctx* ctx) {
+    if (!ctx) return KL_EINVAL;
+    if (!ctx->host_only) {
+        if (!ctx->poisoned) {
+            for (auto& l : ctx->lane) if (l.s) cudaStreamSynchronize(l.s);
+            if (ctx->ctrl) cudaStreamSynchronize(ctx->ctrl);
+        }
+        for (auto& l : ctx->lane) {
+            if (l.own && l.s) cudaStreamDestroy(l.s);
+            if (l.rec) cudaFreeHost(l.rec);
+        }
+        for (auto& k : ctx->insts) if (k->audit) cudaFree(k->audit);
+        if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
+        if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
+        cudaFree(ctx->ctl_pool);
+        cudaFreeHost(ctx->init_pinned);
+        cudaFreeHost(ctx->mk_pinned);
+        cudaFree(ctx->mk_dev);
+        cudaFreeHost(ctx->cand_pinned);
+        cudaFree(ctx->cand_dev);
+        cudaFreeHost(ctx->off_pinned);
+        cudaFree(ctx->off_dev);
+        cudaFree(ctx->pred_dev);
+        cudaFreeHost(ctx->pred_pinned);
+        cudaFree(ctx->done_dev);
+        cudaFree(ctx->dec_dev);
+        cudaFreeHost(ctx->dec_pinned);
+    } else {
+        delete[] ctx->cand_pinned;
+        delete[] ctx->off_pinned;
+    }
+    delete ctx;
+    return KL_OK;
+}
+
+kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
+    KL_LIVE(ctx);
+    if (!d || d->kind < 0 || d->kind >= KL_NKINDS) return ctx->fail(KL_EINVAL, "bad kind");
+    if (d->grid_blocks == 0 || d->grid_blocks >= 0x7fffffffu) return ctx->fail(KL_EINVAL, "grid_blocks out of range");
+    if (!d->args || d->args_bytes != kl_args_size(d->kind))
+        return ctx->fail(KL_EINVAL, "args_bytes %u != sizeof(kl_args) %u for kind %d", d->args_bytes, kl_args_size(d->kind), d->kind);
+    if (d->profile) {
+        const kl_profile& p = *d->profile;
+        if (!(p.rm >= 0.0 && p.rm <= 1.0)) return ctx->fail(KL_EINVAL, "Rm outside [0,1]");
+        ctx->prof[d->kind] = p;
+        ctx->cache.clear();
+    }
+    if (!ctx->host_only && !ctx->info_ok[d->kind]) return ctx->fail(KL_EINVAL, "kind %d not available in this build", d->kind);
+    if (ctx->free_slots.empty()) return ctx->fail(KL_ENOMEM, "slice control pool exhausted");
+    auto k = std::make_unique<Inst>();
+    k->id = ctx->next_id++;
+    k->seq = ctx->seq++;
+    k->kind = d->kind;
+    k->grid = d->grid_blocks;
+    k->tag = d->tag;
+    if (!ctx->host_only) {
+        if (kl_dev_prepare(d->kind, d->args, d->args_bytes, k->blob, kBlob))
+            return ctx->fail(KL_EINVAL, "cannot prepare args of kind %d", d->kind);
+        k->slot = ctx->free_slots.back();
+        ctx->free_slots.pop_back();
+        ctx->init_pinned[2 * ctx->n_init] = (uint32_t)k->slot;
+        ctx->init_pinned[2 * ctx->n_init + 1] = d->grid_blocks;
+        ctx->n_init++;
+        if (ctx->cfg.audit) {
+            KL_CUDA(cudaMalloc(&k->audit, sizeof(uint32_t) * d->grid_blocks));
+            KL_CUDA(cudaMemset(k->audit, 0, sizeof(uint32_t) * d->grid_blocks));
+        }
+    } else {
+        std::memcpy(k->blob, d->args, d->args_bytes);
+    }
+    Inst* raw = k.get();
+    ctx->by_id[raw->id] = raw;
+    ctx->R.push_back(raw);
+    ctx->insts.push_back(std::move(k));
+    if (out_id) *out_id = raw->id;
+    return KL_OK;
+}
+
+kl_status kl_slice(kl_ctx* ctx, uint64_t id, uint32_t b, uint32_t slice_blocks, kl_slice_plan* out) {
+    KL_LIVE(ctx);
+    auto it = ctx->by_id.find(id);
+    if (it == ctx->by_id.end()) return ctx->fail(KL_ENOTFOUND, "unknown id %llu", (unsigned long long)id);
+    if (!out || b == 0) return ctx->fail(KL_EINVAL, "blocks_per_sm must be >= 1");
+    const Inst* k = it->second;
+    const kl_profile& p = ctx->prof[k->kind];
+    int code = fits(ctx, p, b, nullptr, 0);
+    if (code) {
+        static const char* names[] = {"", "warps", "blocks", "registers", "smem", "TMEM"};
+        return ctx->fail(KL_EINFEASIBLE, "%u blocks/SM of kind %d exceed %s", b, k->kind, names[code]);
+    }
+    uint32_t s = slice_blocks ? slice_blocks : slice_of(ctx, p, b, std::max(1, p.m_min));
+    out->slice_blocks = s;
+    out->n_slices = (k->grid + s - 1) / s;
+    out->blocks_per_sm = b;
+    out->waves = (s + b * ctx->n_sms - 1) / (b * ctx->n_sms);
+    return KL_OK;
+}
+
+kl_status kl_predict(kl_ctx* ctx, const kl_candidate* c, size_t n, kl_prediction* out) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    if (n > (size_t)kMaxCand || (n && (!c || !out))) return ctx->fail(KL_EINVAL, "bad candidate list");
+    for (size_t i = 0; i < n; ++i) {
+        if (c[i].k1 < 0 || c[i].k1 >= KL_NKINDS || c[i].k2 < 0 || c[i].k2 >= KL_NKINDS)
+            return ctx->fail(KL_EINVAL, "bad kind in candidate %zu", i);
+        const kl_profile &p1 = ctx->prof[c[i].k1], &p2 = ctx->prof[c[i].k2];
+        if (!(p1.rm >= 0 && p1.rm <= 1 && p2.rm >= 0 && p2.rm <= 1)) return ctx->fail(KL_EINVAL, "Rm outside [0,1]");
+        KlCand cd{};
+        cd.k1 = c[i].k1;
+        cd.k2 = c[i].k2;
+        cd.b1 = c[i].b1;
+        cd.b2 = c[i].b2;
+        cd.pair = -1;
+        ctx->cand_pinned[i] = cd;
+    }
+    if (n == 0) return KL_OK;
+    kl_status st = run_model(ctx, (int)n, 0, nullptr);
+    if (st) return st;
+    std::memcpy(out, ctx->pred_pinned, sizeof(kl_prediction) * n);
+    return KL_OK;
+}
+
+kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out) {
+    KL_LIVE(ctx);
+    if (ctx->in_flight) return ctx->fail(KL_EBUSY, "a phase is in flight");
+    Decision d;
+    kl_status st = find_co_schedule(ctx, &d);
+    if (st) return st;
+    if (out) {
+        *out = kl_coschedule{};
+        Inst* k1 = ctx->R[d.ia];
+        Inst* k2 = d.solo ? nullptr : ctx->R[d.ib];
+        out->id1 = k1->id;
+        out->id2 = k2 ? k2->id : 0;
+        out->kind1 = k1->kind;
+        out->kind2 = k2 ? k2->kind : -1;
+        out->b1 = d.b1;
+        out->b2 = d.b2;
+        int m = std::max(1, ctx->prof[k1->kind].m_min);
+        if (k2) m = std::max(m, ctx->prof[k2->kind].m_min);
+        out->size1 = slice_of(ctx, ctx->prof[k1->kind], d.b1, m);
+        out->size2 = k2 ? slice_of(ctx, ctx->prof[k2->kind], d.b2, m) : 0;
+        out->cp = d.cp;
+        out->solo = d.solo;
+        out->n_candidates = d.n_cand;
+    }
+    return KL_OK;
+}
+
+kl_status kl_schedule(kl_ctx* ctx, kl_coschedule* out) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    kl_status st = retire_phase(ctx);
+    if (st) return st;
+    if (ctx->R.empty()) return ctx->fail(KL_ENOTFOUND, "nothing pending");
+    Decision d;
+    st = find_co_schedule(ctx, &d);
+    if (st) return st;
+    return launch_phase(ctx, d, out);
+}
+
+kl_status kl_sync(kl_ctx* ctx, kl_counters* out) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    for (;;) {
+        kl_status st = retire_phase(ctx);
+        if (st) return st;
+        if (ctx->R.empty()) break;
+        Decision d;
+        st = find_co_schedule(ctx, &d);
+        if (st) return st;
+        st = launch_phase(ctx, d, nullptr);
+        if (st) return st;
+    }
+    KL_CUDA(cudaStreamSynchronize(ctx->lane[0].s));
+    KL_CUDA(cudaStreamSynchronize(ctx->lane[1].s));
+    if (out) {
+        *out = kl_counters{};
+        if (ctx->counters) {
+            KL_CUDA(cudaMemcpyAsync(out, ctx->counters, sizeof(kl_counters), cudaMemcpyDeviceToHost, ctx->ctrl));
+            KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
+        }
+        out->phases = ctx->phases;
+    }
+    return KL_OK;
+}
+
+kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* d, void* stream, uint32_t off, uint32_t n) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    if (!d || d->kind < 0 || d->kind >= KL_NKINDS || !d->args || d->args_bytes != kl_args_size(d->kind))
+        return ctx->fail(KL_EINVAL, "bad descriptor");
+    if ((uint64_t)off + n > d->grid_blocks) return ctx->fail(KL_EINVAL, "slice beyond grid");
+    alignas(128) unsigned char blob[kBlob];
+    if (kl_dev_prepare(d->kind, d->args, d->args_bytes, blob, kBlob)) return ctx->fail(KL_EINVAL, "cannot prepare args");
+    int rc = kl_dev_launch_plain(d->kind, blob, off, n, stream);
+    if (rc) return ctx->fail(KL_ECUDA, "plain launch: %s", cudaGetErrorString((cudaError_t)rc));
+    return KL_OK;
+}
+
+kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out) {
+    KL_LIVE(ctx);
+    if (kind < 0 || kind >= KL_NKINDS || !out) return KL_EINVAL;
+    *out = ctx->prof[kind];
+    return KL_OK;
+}
+
+kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p) {
+    KL_LIVE(ctx);
+    if (kind < 0 || kind >= KL_NKINDS || !p) return KL_EINVAL;
+    if (!(p->rm >= 0.0 && p->rm <= 1.0)) return ctx->fail(KL_EINVAL, "Rm outside [0,1]");
+    kl_profile q = *p;
+    const kl_profile& cur = ctx->prof[kind];
+    if (!q.wpb) q.wpb = cur.wpb;
+    if (!q.regs) q.regs = cur.regs;
+    if (!q.smem) q.smem = cur.smem;
+    if (!q.tmem) q.tmem = cur.tmem;
+    if (!q.bmax) q.bmax = cur.bmax;
+    if (!q.m_min) q.m_min = cur.m_min;
+    ctx->prof[kind] = q;
+    ctx->cache.clear();
+    return KL_OK;
+}
+
+kl_status kl_reset_model_cache(kl_ctx* ctx) {
+    KL_LIVE(ctx);
+    ctx->cache.clear();
+    return KL_OK;
+}
+
+kl_status kl_reset_counters(kl_ctx* ctx) {
+    KL_LIVE(ctx);
+    if (ctx->host_only || !ctx->counters) return KL_OK;
+    static const int64_t init[8] = {0, 0, INT64_MAX, 0, 0, 0, 0, 0};
+    KL_CUDA(cudaMemcpyAsync(ctx->counters, init, 5 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->ctrl));
+    KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
+    return KL_OK;
+}
+
+kl_status kl_trace(kl_ctx* ctx, kl_trace_rec* out, size_t cap, size_t* n_out) {
+    KL_LIVE(ctx);
+    size_t n = std::min(cap, ctx->trace.size());
+    if (out && n) std::memcpy(out, ctx->trace.data(), n * sizeof(kl_trace_rec));
+    if (n_out) *n_out = ctx->trace.size();
+    return KL_OK;
+}
+
+kl_status kl_audit(kl_ctx* ctx, uint64_t id, uint32_t* host_out, size_t n) {
+    KL_LIVE(ctx);
+    auto it = ctx->by_id.find(id);
+    if (it == ctx->by_id.end()) return ctx->fail(KL_ENOTFOUND, "unknown id");
+    const Inst* k = it->second;
+    if (!k->audit) return ctx->fail(KL_EINVAL, "audit disabled (config.audit = 0)");
+    if (!host_out || n < k->grid) return ctx->fail(KL_EINVAL, "audit buffer too small");
+    for (auto& l : ctx->lane) KL_CUDA(cudaStreamSynchronize(l.s));
+    KL_CUDA(cudaMemcpy(host_out, k->audit, sizeof(uint32_t) * k->grid, cudaMemcpyDeviceToHost));
+    return KL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+"""End-to-end GPU tests of sliced, co-scheduled execution through the C ABI.
+
+C1 (BASELINE.json configs[0]): PC + BS, 64 blocks each, exhaustive model search; mixed small
+queues of every kind; the stop-at-slice-boundary protocol under stress.  Checks: outputs vs the
+oracle, coverage audit (every block exactly once), contiguous slice ranges per kernel,
+per-SM residency never above the admission cap, device counters."""
+import numpy as np
+import pytest
+import torch
+
+import kl_inputs as G
+import oracle as O
+import paper_1303_5164_b200 as K
+from paper_1303_5164_b200.workload import Instance
+from kl_check import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_queue(ctx, insts, counters=None):
+    for i in insts:
+        for o in i.outputs.values():
+            o.fill_(0)
+    torch.cuda.synchronize()
+    ids = [ctx.submit(i.kind, i.grid, i.args, tag=n + 1) for n, i in enumerate(insts)]
+    c = ctx.sync()
+    return ids, c
+
+
+def _check_trace(ctx, ids, insts):
+    tr = ctx.trace()
+    by = {}
+    for t in tr:
+        by.setdefault(t.id, []).append(t)
+    for kid, inst in zip(ids, insts):
+        recs = sorted(by[kid], key=lambda t: t.phase)
+        pos = 0
+        for t in recs:
+            assert t.start == pos, (inst.kind, t.start, pos)
+            assert t.end >= t.start and t.executed == t.end - t.start
+            if not t.exhausted:                      # stopped at a slice boundary
+                assert (t.end - t.start) % t.slice == 0, (inst.kind, t.start, t.end, t.slice)
+            if t.cap:
+                assert t.max_per_sm <= t.cap, (inst.kind, t.max_per_sm, t.cap)
+            pos = t.end
+        assert pos == inst.grid and recs[-1].exhausted
+        counts = ctx.audit(kid, inst.grid)
+        assert np.all(counts == 1), (inst.kind, counts.min(), counts.max())
+    return tr
+
+
+def test_c1_pc_bs_pair():
+    K.build()
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctx = K.Context(device=0, audit=1, counters=counters)
+    ctx.reset_counters()
+    ds = [G.gen("PC", "small"), G.gen("BS", "small")]
+    insts = [Instance(d, "cuda") for d in ds]
+    ids, c = _run_queue(ctx, insts)
+    for d, i in zip(ds, insts):
+        compare(d["kind"], i.result(), O.run_kernel(d))
+    tr = _check_trace(ctx, ids, insts)
+    assert c.kernels_done == 2 and c.blocks_done == sum(i.grid for i in insts)
+    assert c.checksum == 1 + 2 and c.t_end_ns > c.t_start_ns
+    assert any(t.partner_kind >= 0 for t in tr) or all(t.partner_kind < 0 for t in tr)
+    ctx.close()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_mixed_queue_parity(seed):
+    K.build()
+    ctx = K.Context(device=0, audit=1, alpha_p=0.0, alpha_m=0.0)
+    kinds = ["PC", "SAD", "SPMV", "ST", "MRIQ", "BS", "TEA", "SYNTH", "MATADD"]
+    rng = np.random.default_rng(seed)
+    order = [str(k) for k in rng.permutation(kinds * 2)]
+    ds = {k: G.gen(k, "small") for k in kinds}
+    refs = {k: O.run_kernel(ds[k]) for k in kinds}
+    shared = {}
+    insts = []
+    for k in order:
+        inst = Instance(ds[k], "cuda", inputs=shared.get(k))
+        shared[k] = inst.inputs
+        insts.append(inst)
+    ids, c = _run_queue(ctx, insts)
+    for i in insts:
+        compare(i.kind, i.result(), refs[i.kind])
+    _check_trace(ctx, ids, insts)
+    ctx.close()
+
+
+def test_stop_protocol_stress():
+    """A long kernel paired with short ones at 1-wave slices is stopped and resumed many times;
+    every block still runs exactly once and the result is unchanged."""
+    K.build()
+    profs = None
+    ctx = K.Context(device=0, audit=1, alpha_p=0.0, alpha_m=0.0, chunk=1)
+    long_d = G.gen("SYNTH", {"n": 256 * 4 * 4 * 3000, "fmas": 64})
+    short = [G.gen("TEA", {"n": 1280 * 150}, seed=s) for s in range(6)] + \
+            [G.gen("PC", {"n_nodes": 1 << 14, "n_threads": 256 * 300, "hops": 10}, seed=s) for s in range(6)]
+    insts = [Instance(long_d, "cuda")] + [Instance(d, "cuda") for d in short]
+    ids, c = _run_queue(ctx, insts)
+    _check_trace(ctx, ids, insts)
+    compare("SYNTH", insts[0].result(), O.run_kernel(long_d))
+    for d, i in zip(short, insts[1:]):
+        compare(d["kind"], i.result(), O.run_kernel(d))
+    ctx.close()
