@@ -1,0 +1,536 @@
+#!/usr/bin/env python
+"""Kernel-queue throughput of the B200-native Kernelet hot path (BASELINE.json metric).
+
+One step = one pass of the whole hot path over one batch of synthetic input: submit the queue
+(Alg.1 l.2-3), per-kind profiles, pruning, the batched Markov model on the device (the model
+cache is cleared every step so the model runs every step), greedy selection, sliced co-scheduled
+execution on two lanes with offset-remapped persistent blocks, completion counters, and for N > 1
+the NCCL all-gather of the per-GPU counters.
+
+Default workload (N=1): BASELINE configs[1] -- the paper's eight-kernel ALL mix (tb:workloads,
+P:1196) at paper sizes (tb:description), 4 instances of each kernel = 32 kernels per
+GPU, round-robin arrival order, all pending at t=0.  For N GPUs each rank runs its
+own shard of a 32*N-kernel queue (mix-preserving round robin): weak scaling, no cross-GPU data.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import kl_inputs as G  # noqa: E402
+
+ALL = G.MIXES["ALL"]
+METRIC = "kernel-queue throughput (kernels/s) & speedup vs sequential, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kernelet", choices=["kernelet", "reference"])
+    ap.add_argument("--instances", type=int, default=4, help="instances of each ALL-mix kernel per GPU")
+    ap.add_argument("--size", default="paper", choices=["paper", "small"])
+    ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--profile", default=os.path.join(ROOT, "profiles", "kl_profile_b200.json"))
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+# Algorithmic work per kernel: bytes that must cross HBM, or the
+# arithmetic the method must do, per instance at the given size.  Used for the roofline.
+# ---------------------------------------------------------------------------------------------
+def algorithmic_work(kind: str, p: dict) -> dict:
+    if kind == "PC":      # one 32-B DRAM sector per dependent load + 8 B of output per thread
+        return {"bound": "hbm", "bytes": p["n_threads"] * (p["hops"] * 32 + 8)}
+    if kind == "SAD":     # 4 pixel |diff|-accumulates per vabsdiff4; ALU-bound
+        n_mb = (p["width"] // 16) * (p["height"] // 16)
+        return {"bound": "alu", "ops": n_mb * 1089 * 256 / 4, "bytes": 2 * p["width"] * p["height"] + n_mb * 1089 * 2}
+    if kind == "SPMV":
+        nnz = p["n_rows"] * (p["nnz_min"] + p["nnz_max"]) / 2
+        return {"bound": "hbm", "bytes": nnz * 8 + (p["n_rows"] + 1) * 4 + p["n_cols"] * 4 + p["n_rows"] * 4}
+    if kind == "ST":
+        return {"bound": "hbm", "bytes": 2 * 4 * p["nx"] * p["ny"] * p["nz"]}
+    if kind == "MM":
+        return {"bound": "tensor", "flops": 2.0 * p["M"] * p["N"] * p["K"],
+                "bytes": 2 * (p["M"] * p["K"] + p["N"] * p["K"]) + 4 * p["M"] * p["N"]}
+    if kind == "MRIQ":    # sin + cos per (voxel, k): MUFU-bound
+        return {"bound": "alu", "ops": 2.0 * p["num_x"] * p["num_k"], "bytes": 5 * 4 * p["num_x"]}
+    if kind == "BS":
+        return {"bound": "hbm", "bytes": 5 * 4 * p["n"]}
+    if kind == "TEA":     # 32 cycles x ~10 integer ops per 64-bit block
+        return {"bound": "alu", "ops": p["n"] * 32 * 2 * 5.0, "bytes": 16 * p["n"]}
+    return {"bound": "hbm", "bytes": 0}
+
+
+def alu_peak(kind: str, sm_mhz: float, n_sm: int = 148) -> tuple[float, str]:
+    """ALU-pipe peaks from unit counts x clock: MUFU 16/clk/SM (sin, cos);
+    integer ALU pipe 64 lanes/clk/SM (IADD3/LOP3/SHF/VABSDIFF4)."""
+    f = sm_mhz * 1e6
+    if kind == "MRIQ":
+        return 16 * n_sm * f, "MUFU ops/s (16/clk/SM)"
+    return 64 * n_sm * f, "int ALU ops/s (64/clk/SM)"
+
+
+# ---------------------------------------------------------------------------------------------
+class Clocks:
+    """Sample nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and "Active" in s[4 + i]
+                          and s[4 + i].strip() == "Active"})
+        loaded = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------------
+def build_queue(rank: int, world: int, instances: int) -> list[str]:
+    """Global queue of 32*world kernels (instances x ALL per GPU), sharded round robin so every
+    GPU keeps the mix."""
+    gq = [e["kind"] for e in G.queue("ALL", len(ALL) * instances * world, order="round_robin")]
+    return gq[rank::world]
+
+
+def load_profiles(path: str):
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("profiles"), d.get("config", {})
+    return None, {}
+
+
+def run_kernelet(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1303_5164_b200 as K
+    from paper_1303_5164_b200.workload import Instance, inputs_to_device
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    K.lib()
+    kinds = build_queue(rank, world, args.instances)
+    profiles, kcfg = load_profiles(args.profile)
+    t_gen = time.time()
+    data = {k: G.gen(k, args.size) for k in sorted(set(kinds))}
+    inputs = {k: inputs_to_device(data[k], dev) for k in data}
+    insts = [Instance(data[k], dev, inputs=inputs[k]) for k in kinds]
+    t_gen = time.time() - t_gen
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    lane_a = torch.cuda.Stream(device=dev)
+    lane_b = torch.cuda.Stream(device=dev)
+    cfg = dict(kcfg)
+    ctx = K.Context(device=local_rank, profiles=profiles, streams=(lane_a, lane_b), counters=counters, **cfg)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126.5 MiB)
+    gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev)
+
+    def one_step():
+        ctx.reset_model_cache()
+        ctx.reset_counters()
+        counters[5] = rank
+        counters[6] = world
+        ids = [ctx.submit(i.kind, i.grid, i.args, tag=n + 1) for n, i in enumerate(insts)]
+        c = ctx.sync()
+        if world > 1:
+            with torch.cuda.stream(lane_a):
+                dist.all_gather_into_tensor(gathered, counters)
+        return ids, c
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up (also the parity sample of this run)
+    for _ in range(args.warmup):
+        flush.zero_()
+        barrier()
+        one_step()
+    torch.cuda.synchronize(dev)
+    parity = sample_parity(insts, data) if rank == 0 else {}
+    n_trace0 = len(ctx.trace())
+
+    step_ms, dev_ms, cnts = [], [], []
+    with Clocks(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(lane_a)
+            ids, c = one_step()
+            e1.record(lane_a)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            dev_ms.append((c.t_end_ns - c.t_start_ns) / 1e6)
+            cnts.append(c)
+        barrier()
+    trace = ctx.trace()[n_trace0:]
+    launches = len(trace) + 2 * args.steps      # lane launches + model batch + ctl init per step
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    c_last = cnts[-1]
+    assert c_last.kernels_done == len(insts), (c_last.kernels_done, len(insts))
+    if world > 1:
+        g = gathered.view(world, 8).cpu()
+        assert int(g[:, 0].sum()) == len(insts) * world      # NCCL-gathered completion counters
+
+    res = {
+        "value": len(insts) * world * args.steps / (total_ms / 1e3),
+        "ms_per_step": total_ms / args.steps,
+        "device_ms_per_step": statistics.median(dev_ms),
+        "phases_per_step": c_last.phases,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "parity": parity,
+        "setup_s": round(t_gen, 1),
+    }
+    phase_kinds = [(K.KINDS[tr.kind], tr.cap, K.KINDS[tr.partner_kind] if tr.partner_kind >= 0 else None)
+                   for tr in trace[: max(1, len(trace) // args.steps)]]
+    res["schedule_first_step"] = phase_kinds
+
+    if not args.no_baselines:
+        res["baselines"] = baselines(ctx, insts, dev, flush, barrier, args)
+        res["e2e"] = e2e(ctx, insts, data, dev, barrier, args, world, rank, lane_a, lane_b)
+        res["per_kernel"] = per_kernel(ctx, insts, data, dev, flush, barrier)
+    ctx.close()
+    return res
+
+
+def sample_parity(insts, data, per_kind: int = 64) -> dict:
+    """Sampled outputs of every kind vs the oracle at full size (tests/kl_check tolerances)."""
+    import oracle as O
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from kl_check import compare
+    out, seen = {}, set()
+    rng = np.random.default_rng(5)
+    for inst in insts:
+        k = inst.kind
+        if k in seen:
+            continue
+        seen.add(k)
+        res = inst.result()
+        first = next(iter(res.values()))
+        n = first.size if k != "TEA" else first.size // 2
+        idx = np.sort(rng.choice(n, size=min(per_kind, n), replace=False))
+        ref = O.run_kernel(data[k], idx)
+        try:
+            errs = compare(k, res, ref, idx=idx)
+            out[k] = {"ok": True, "max_err": max(errs.values()) if errs else 0.0, "n": int(idx.size)}
+        except AssertionError as e:
+            out[k] = {"ok": False, "err": str(e)[:200]}
+    return out
+
+
+def _time_streams(fn, dev, flush, barrier, reps=3):
+    import torch
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        barrier()
+        s = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fn(s, e0)
+        e1.record(s)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def baselines(ctx, insts, dev, flush, barrier, args) -> dict:
+    """Sequential (one stream, full grids at max occupancy, back to back) and plain multi-stream
+    (round robin over S streams, full grids, no slicing) executions of the same kernels."""
+    import torch
+    out = {}
+
+    def seq(s, e0):
+        for i in insts:
+            ctx.run_plain(i.kind, i.grid, i.args, s)
+
+    ms = _time_streams(seq, dev, flush, barrier)
+    out["sequential"] = {"ms_per_step": ms, "kernels_per_s": len(insts) / (ms / 1e3)}
+    for S in (2, 4, 8):
+        streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
+
+        def ms_fn(s, e0, streams=streams):
+            evs = []
+            for st in streams:
+                st.wait_event(e0)
+            for n, i in enumerate(insts):
+                ctx.run_plain(i.kind, i.grid, i.args, streams[n % len(streams)])
+            for st in streams:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                s.wait_event(ev)
+
+        ms = _time_streams(ms_fn, dev, flush, barrier)
+        out[f"multistream{S}"] = {"ms_per_step": ms, "kernels_per_s": len(insts) / (ms / 1e3)}
+    return out
+
+
+def per_kernel(ctx, insts, data, dev, flush, barrier) -> dict:
+    """Solo plain launch of one instance of each kind: duration, algorithmic rate, roofline."""
+    import torch
+    out, seen = {}, set()
+    for i in insts:
+        if i.kind in seen:
+            continue
+        seen.add(i.kind)
+        ms = _time_streams(lambda s, e0, i=i: ctx.run_plain(i.kind, i.grid, i.args, s), dev, flush, barrier, reps=5)
+        w = algorithmic_work(i.kind, data[i.kind]["params"])
+        out[i.kind] = {"ms": ms, **w}
+    return out
+
+
+def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b) -> dict:
+    """Same metric through the public API with HOST buffers: every step copies the step's inputs
+    (one set per kind, shared by its instances) from pinned host memory and reads the completion
+    counters back."""
+    import torch
+    from paper_1303_5164_b200.workload import INPUTS
+    host = {}
+    for k in {i.kind for i in insts}:
+        host[k] = {n: t.cpu().pin_memory() for n, t in insts[[i.kind for i in insts].index(k)].inputs.items()}
+    h2d = sum(t.numel() * t.element_size() for d in host.values() for t in d.values())
+    ts = []
+    for _ in range(max(2, min(args.steps, 3))):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lane)
+        with torch.cuda.stream(lane):
+            done = set()
+            for i in insts:
+                if i.kind in done:
+                    continue
+                done.add(i.kind)
+                for n, t in i.inputs.items():
+                    t.copy_(host[i.kind][n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(lane)
+        lane_b.wait_event(ev)            # kernels on either lane start after their inputs landed
+        ctx.reset_model_cache()
+        ctx.reset_counters()
+        for n, i in enumerate(insts):
+            ctx.submit(i.kind, i.grid, i.args, tag=n + 1)
+        c = ctx.sync()
+        res = ctx.counters.cpu()        # D2H read of the step's result
+        e1.record(lane)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+        assert int(res[0]) == len(insts)
+    ms = statistics.median(ts)
+    return {"value": len(insts) * world / (ms / 1e3), "unit": "kernels/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": 64, "ms_per_step": ms}
+
+
+# ---------------------------------------------------------------------------------------------
+class OracleLeg:
+    """The oracle as it stands, on the host cores: every kind's outputs on a fixed strided sample
+    (fraction f of the elements) plus the oracle's full Alg.1 decision sequence (model + search)
+    for the queue; throughput = kernels-equivalent of work done / wall time."""
+
+    def __init__(self, kinds: list[str], size: str):
+        import oracle as O
+        O.build()
+        self.O = O
+        self.kinds = kinds
+        self.cores = os.cpu_count() or 1
+        self.data = {k: G.gen(k, size) for k in sorted(set(kinds))}
+        self.sizes = {}
+        for k, d in self.data.items():
+            p = d["params"]
+            self.sizes[k] = {"PC": lambda: p["n_threads"], "SPMV": lambda: p["n_rows"], "MRIQ": lambda: p["num_x"],
+                             "BS": lambda: p["n"], "TEA": lambda: p["n"],
+                             "SAD": lambda: (p["width"] // 16) * (p["height"] // 16) * 1089,
+                             "ST": lambda: p["nx"] * p["ny"] * p["nz"], "MM": lambda: p["M"] * p["N"]}[k]()
+        self.profs = _oracle_profiles()
+
+    def run(self, target_s: float) -> dict:
+        frac = 1e-4
+        t0 = time.time()
+        _oracle_sample(self.O, self.data, self.sizes, frac, self.cores)
+        probe = max(time.time() - t0, 1e-3)
+        frac = min(1.0, frac * target_s / probe)
+        t0 = time.time()
+        _oracle_sample(self.O, self.data, self.sizes, frac, self.cores)
+        t_k = time.time() - t0
+        t0 = time.time()
+        if self.profs:
+            q = [{"kind": k, "blocks": 1000} for k in self.kinds]
+            self.O.alg1_makespan(q, self.profs, self.O.smcfg(W=16))
+        t_s = time.time() - t0
+        n_equiv = frac * len(self.kinds)
+        return {"value": n_equiv / (t_k + t_s), "unit": "kernels/s", "cores": self.cores, "kind": "oracle",
+                "sample": f"{frac:.2e} of every output element of the {len(self.kinds)}-kernel queue (strided, "
+                          f"{self.cores} threads) + the oracle's Alg.1/FindCoSchedule decision sequence; "
+                          f"{t_k + t_s:.1f} s wall"}
+
+
+def cpu_oracle_leg(kinds: list[str], size: str, target_s: float = 15.0) -> dict:
+    return OracleLeg(kinds, size).run(target_s)
+
+
+def _oracle_sample(O, data, sizes, frac, cores):
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = []
+    for k, d in data.items():
+        n = sizes[k]
+        m = max(1, int(n * frac))
+        idx = np.linspace(0, n - 1, m).astype(np.int64)
+        for chunk in np.array_split(idx, cores):
+            if chunk.size:
+                jobs.append((d, chunk))
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(lambda j: O.run_kernel(j[0], j[1]), jobs))
+
+
+def _oracle_profiles():
+    path = os.path.join(ROOT, "profiles", "kl_profile_b200.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))["profiles"]
+    return {k: v for k, v in d.items() if k in ALL}
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    config = {"workload": f"ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels, "
+                          f"{args.size} sizes, all pending at t=0)", "global_kernels": len(ALL) * args.instances * world,
+              "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
+              "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        kinds = build_queue(0, 1, args.instances)
+        leg = OracleLeg(kinds, args.size)
+        vals = []
+        for s in range(args.warmup + args.steps):
+            r = leg.run(target_s=max(2.0, 60.0 / (args.warmup + args.steps)))
+            if s >= args.warmup:
+                vals.append(r["value"])
+        v = statistics.median(vals)
+        line = {"metric": METRIC, "value": v, "unit": "kernels/s", "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32/f64/u32 (per kernel)", "data": "synthetic", "config": config,
+                "cpu_baseline": {**r, "value": v}, "e2e": {"value": v, "unit": "kernels/s", "h2d_bytes_per_step": 0,
+                                                          "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_kernelet(args, rank, world, local_rank)
+    if rank == 0:
+        bl = res.get("baselines", {})
+        seq = bl.get("sequential", {}).get("kernels_per_s")
+        ms4 = max((v["kernels_per_s"] for k, v in bl.items() if k.startswith("multistream")), default=None)
+        pk = res.get("per_kernel", {})
+        sm_mhz = (res["clocks"].get("sm_mhz") or 1965.0)
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+        roof_all = {}
+        for k, v in pk.items():
+            if v["bound"] == "hbm":
+                a = v["bytes"] / (v["ms"] / 1e3) / 1e9
+                roof_all[k] = {"bound": "hbm", "achieved": a, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": a / peaks["hbm_gbs"], "ms": v["ms"]}
+            elif v["bound"] == "tensor":
+                a = v["flops"] / (v["ms"] / 1e3) / 1e12
+                roof_all[k] = {"bound": "tensor", "achieved": a, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                               "frac": a / peaks["bf16_tflops"], "ms": v["ms"]}
+            else:
+                pk_, what = alu_peak(k, sm_mhz)
+                a = v["ops"] / (v["ms"] / 1e3)
+                roof_all[k] = {"bound": "alu", "achieved": a / 1e12, "peak": pk_ / 1e12, "unit": f"T{what}",
+                               "frac": a / pk_, "ms": v["ms"]}
+        dom = max(pk, key=lambda k: pk[k]["ms"] * sum(1 for x in build_queue(0, 1, args.instances) if x == k)) if pk else None
+        roof = dict(roof_all[dom], kernel=dom, traffic=None) if dom else None
+        line = {"metric": METRIC, "value": res["value"], "unit": "kernels/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32/bf16->f32/u32/u8 (per kernel); model f64",
+                "data": "synthetic", "config": config, "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
+                "e2e": res.get("e2e"), "roofline": roof,
+                "speedup_vs_sequential": res["value"] / world / seq if seq else None,
+                "speedup_vs_multistream": res["value"] / world / ms4 if ms4 else None,
+                "baselines": bl, "roofline_all": roof_all, "device_ms_per_step": res["device_ms_per_step"],
+                "phases_per_step": res["phases_per_step"], "parity": res["parity"],
+                "schedule_first_step": res["schedule_first_step"]}
+        if not args.no_cpu and world == 1:
+            line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances), args.size)
+        print(json.dumps(line))
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(line, f, indent=1)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

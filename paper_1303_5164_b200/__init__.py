@@ -22,7 +22,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libkl.so in-tree with nvcc for sm_100a (cross-compiles without a GPU)."""
     srcs = [os.path.join(_HERE, s) for s in SOURCES]
-    deps = srcs + [os.path.join(_HERE, "csrc", "kl_internal.h"), os.path.join(_ROOT, "include", "kl.h")]
+    deps = srcs + [os.path.join(_HERE, "csrc", h) for h in ("kl_internal.h", "kl_launcher.cuh")] + [os.path.join(_ROOT, "include", "kl.h")]
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= max(map(os.path.getmtime, deps)):
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")

@@ -19,7 +19,7 @@ from kl_check import compare
 
 pytestmark = pytest.mark.gpu
 
-KINDS = ["PC", "SAD", "SPMV", "ST", "MRIQ", "BS", "TEA", "MATADD", "SYNTH"]
+KINDS = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA", "MATADD", "SYNTH"]
 
 
 @pytest.fixture(scope="module")
@@ -104,10 +104,11 @@ def test_laplacian_mode_exact(ctx):
     assert np.array_equal(res["out"], ref["out"])
 
 
-def test_integer_modes_exact(ctx):
-    for kind in ("SPMV",):
-        d = G.gen(kind, "small", mode="int")
-        inst = Instance(d, "cuda")
-        res = _run_plain(ctx, inst)
-        ref = O.run_kernel(d)
-        assert np.array_equal(res["y"], ref["y"])
+@pytest.mark.parametrize("kind,field", [("SPMV", "y"), ("MM", "C")])
+def test_integer_modes_exact(ctx, kind, field):
+    """Small-integer inputs make every partial sum exact in fp32: bit-exact vs the oracle."""
+    d = G.gen(kind, "small", mode="int")
+    inst = Instance(d, "cuda")
+    res = _run_plain(ctx, inst)
+    ref = O.run_kernel(d)
+    assert np.array_equal(res[field], ref[field])

@@ -70,7 +70,7 @@ def test_c1_pc_bs_pair():
 def test_mixed_queue_parity(seed):
     K.build()
     ctx = K.Context(device=0, audit=1, alpha_p=0.0, alpha_m=0.0)
-    kinds = ["PC", "SAD", "SPMV", "ST", "MRIQ", "BS", "TEA", "SYNTH", "MATADD"]
+    kinds = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA", "SYNTH", "MATADD"]
     rng = np.random.default_rng(seed)
     order = [str(k) for k in rng.permutation(kinds * 2)]
     ds = {k: G.gen(k, "small") for k in kinds}
