@@ -1,0 +1,188 @@
+#!/usr/bin/env python
+"""B200 calibration of the model inputs (A24; PUR/MUR P:675-694; p% rule P:496-502).
+
+Two modes, run on the GPU box:
+  python tools/calibrate.py target      # one plain full-grid launch of each kind (ncu target)
+  python tools/calibrate.py run         # everything: ncu pass (subprocess), timing, p% sweep,
+                                        # dependent-load latency -> profiles/kl_profile_b200.json
+
+Per kind (solo, plain launch at max occupancy, paper size):
+  I   = smsp__inst_executed.sum / grid_blocks                         (warp instructions / block)
+  Rm  = (global ld + st SASS instructions) / smsp__inst_executed.sum  (memory instruction ratio)
+  r   = L1 global-load sectors per request                            (requests per memory instr)
+  PUR = smsp__inst_executed.sum / (sm__cycles_elapsed.avg * 4 * n_SM)  (issue slots, R15)
+  MUR = (dram read + write bytes) / (duration * measured HBM peak)    (R23)
+  IPC = smsp__inst_executed.avg.per_cycle_active                      (virtual-SM IPC)
+The latency constants: L0 from a dependent-load chain (one PC block, many hops, HBM-resident
+array), B = measured HBM bandwidth in 32-B sectors per cycle per virtual SM at the loaded clock.
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+KINDS = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA", "SYNTH"]
+METRICS = ["smsp__inst_executed.sum", "smsp__sass_inst_executed_op_global_ld.sum",
+           "smsp__sass_inst_executed_op_global_st.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+           "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__time_duration.sum", "sm__cycles_elapsed.avg", "smsp__inst_executed.avg.per_cycle_active",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+           "launch__occupancy_limit_registers", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"]
+
+
+def _setup():
+    import torch
+
+    import kl_inputs as G
+    import paper_1303_5164_b200 as K
+    from paper_1303_5164_b200.workload import Instance
+    K.lib()
+    ctx = K.Context(device=0)
+    insts = {k: Instance(G.gen(k, "paper"), "cuda") for k in KINDS}
+    torch.cuda.synchronize()
+    return ctx, insts
+
+
+def target():
+    import torch
+    ctx, insts = _setup()
+    for k in KINDS:
+        i = insts[k]
+        ctx.run_plain(k, i.grid, i.args, 0)
+        torch.cuda.synchronize()
+    print("target done")
+
+
+def _time(ctx, inst, slices=None, reps=5):
+    import torch
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if slices is None:
+            ctx.run_plain(inst.kind, inst.grid, inst.args, 0)
+        else:
+            for off, n in slices:
+                ctx.run_plain(inst.kind, inst.grid, inst.args, 0, off, n)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def run(out_path):
+    import numpy as np
+    import torch
+
+    import kl_inputs as G
+    import paper_1303_5164_b200 as K
+    from paper_1303_5164_b200.workload import Instance
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    # ---- ncu pass in a subprocess ------------------------------------------------------------
+    log = os.path.join(ROOT, "gpurun_out", "calib_ncu.csv")
+    cmd = ["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k", "regex:k_plain", "--csv",
+           "--log-file", log, sys.executable, os.path.abspath(__file__), "target"]
+    t0 = time.time()
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    print("ncu pass", round(time.time() - t0, 1), "s rc", r.returncode, r.stderr[-500:])
+    rows = list(csv.DictReader(io.StringIO("".join(l for l in open(log) if not l.startswith("==")))))
+    per = {}
+    for row in rows:
+        name = row.get("Kernel Name", "")
+        kind = next((k for k in KINDS if f"Body{k}E" in name or f"Body{k}>" in name or f"Body{k}" in name.split("<")[-1][:12]), None)
+        for k in KINDS:
+            if f"Body{k}" in name:
+                kind = k
+        if kind is None:
+            continue
+        v = row["Metric Value"].replace(",", "")
+        try:
+            per.setdefault(kind, {})[row["Metric Name"]] = float(v)
+        except ValueError:
+            per.setdefault(kind, {})[row["Metric Name"]] = v
+    # ---- timing, p% sweep, latency ------------------------------------------------------------
+    ctx, insts = _setup()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    hbm = peaks["hbm_gbs"] * 1e9
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    profiles, measured = {}, {}
+    clk_mhz = []
+    for k in KINDS:
+        i = insts[k]
+        m = per.get(k, {})
+        prof = ctx.get_profile(k)
+        t_ns = _time(ctx, i)
+        inst_tot = m.get("smsp__inst_executed.sum", 0.0)
+        mem = m.get("smsp__sass_inst_executed_op_global_ld.sum", 0.0) + m.get("smsp__sass_inst_executed_op_global_st.sum", 0.0)
+        req = m.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", 0.0)
+        sec = m.get("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", 0.0)
+        cyc = m.get("sm__cycles_elapsed.avg", 0.0)
+        dur = m.get("gpu__time_duration.sum", t_ns * 1e6) * 1e-9
+        dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        if cyc and dur:
+            clk_mhz.append(cyc / dur / 1e6)
+        # p% rule: smallest m (waves of bmax x n_SM blocks) with T_s/T_ns - 1 <= 2 %
+        wave = max(1, prof.bmax) * n_sm
+        m_min, sweep = None, {}
+        for mw in (1, 2, 4, 8, 16, 32):
+            s = mw * wave
+            if s >= i.grid:
+                sweep[mw] = 0.0
+                m_min = m_min or mw
+                break
+            sl = [(o, min(s, i.grid - o)) for o in range(0, i.grid, s)]
+            ov = _time(ctx, i, sl, reps=3) / t_ns - 1.0
+            sweep[mw] = ov
+            if m_min is None and ov <= 0.02:
+                m_min = mw
+        profiles[k] = {
+            "rm": (mem / inst_tot) if inst_tot else prof.rm,
+            "r": (sec / req) if req else 1.0,
+            "ipb": inst_tot / i.grid if inst_tot else prof.ipb,
+            "pur": inst_tot / (cyc * 4 * n_sm) if cyc else prof.pur,
+            "mur": dram / (dur * hbm) if dur else prof.mur,
+            "wpb": prof.wpb, "regs": prof.regs, "smem": prof.smem, "tmem": prof.tmem, "bmax": prof.bmax,
+            "m_min": int(m_min or 32),
+        }
+        measured[k] = {"ms_solo": t_ns, "ipc_vsm": m.get("smsp__inst_executed.avg.per_cycle_active"),
+                       "warps_active_pct": m.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                       "dram_bytes": dram, "ncu_duration_ms": dur * 1e3, "slicing_overhead": sweep,
+                       "grid": i.grid, "raw": m}
+        print(k, json.dumps(profiles[k]), "solo ms", round(t_ns, 4), "overheads", sweep, flush=True)
+    # ---- dependent-load latency L0: one block of 256 chains through an HBM-resident array ---
+    d = G.gen("PC", {"n_nodes": 256 << 20, "n_threads": 256, "hops": 4096})
+    pc = Instance(d, "cuda")
+    t = _time(ctx, pc, reps=3)
+    clock = (sorted(clk_mhz)[len(clk_mhz) // 2] if clk_mhz else 1965.0)
+    L0_ns = t * 1e6 / 4096
+    L0 = L0_ns * clock / 1e3
+    B = hbm / 32.0 / (n_sm * 4) / (clock * 1e6)      # sectors / cycle / virtual SM
+    cfg = {"L0": L0, "B": B, "a0": 1.0, "b0": 0.0}
+    out = {"device": torch.cuda.get_device_name(0), "n_sm": n_sm, "clock_mhz_under_ncu": clock,
+           "latency_ns": L0_ns, "config": cfg, "profiles": profiles, "measured": measured,
+           "how": "tools/calibrate.py run (ncu solo pass + CUDA-event timing + slice sweep + PC chain)",
+           "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    with open(out_path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", out_path, "L0", L0, "cycles", "B", B)
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1] if len(sys.argv) > 1 else "run"
+    if mode == "target":
+        target()
+    else:
+        run(sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "kl_profile_b200.json"))
