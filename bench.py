@@ -144,11 +144,17 @@ def build_queue(rank: int, world: int, instances: int) -> list[str]:
     return gq[rank::world]
 
 
+MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min")
+
+
 def load_profiles(path: str):
+    """Calibrated model inputs (tools/calibrate.py).  Resource fields (warps, registers, shared
+    memory, TMEM, b_max) are left to the runtime, which reads them from the compiled kernels."""
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return d.get("profiles"), d.get("config", {})
+        profs = {k: {f: v[f] for f in MODEL_FIELDS if f in v} for k, v in d.get("profiles", {}).items()}
+        return profs, d.get("config", {})
     return None, {}
 
 

@@ -137,8 +137,8 @@ typedef struct {
     int32_t audit;             /* 1: count executions per virtual block (coverage audit) */
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
-    void* stream_a;            /* lane A cudaStream_t (NULL: library-created) */
-    void* stream_b;            /* lane B */
+    void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
+    void* stream_b;            /* optional cudaStream_t: second stream of the launch pool      */
     int64_t* counters_dev;     /* caller-owned device int64[8] (kl_counters), or NULL */
 } kl_config;
 
@@ -149,6 +149,8 @@ typedef struct {
     uint32_t args_bytes;       /* sizeof that struct */
     const kl_profile* profile; /* NULL = table */
     uint64_t tag;              /* user tag, summed into the completion checksum */
+    void* ready_event;         /* cudaEvent_t every launch of the kernel waits on (its inputs
+                                  landed: the kernel's arrival), or NULL */
 } kl_kernel_desc;
 
 typedef struct { uint32_t slice_blocks, n_slices, blocks_per_sm, waves; } kl_slice_plan;
@@ -165,13 +167,23 @@ typedef struct {
 typedef struct {
     int64_t kernels_done, blocks_done, t_start_ns, t_end_ns, checksum, rank, world, phases;
 } kl_counters;
-typedef struct {               /* one executed phase lane (trace / residency evidence) */
+typedef struct {               /* runtime statistics since kl_create */
+    int64_t decisions;         /* FindCoSchedule decisions */
+    int64_t launches;          /* persistent slice launches */
+    int64_t stops;             /* stop requests (re-plans that changed a running kernel) */
+    int64_t model_batches, model_candidates;
+    int64_t device_launches;   /* every kernel launched by the library (incl. model, stop, init) */
+    int64_t decide_ns;         /* host time spent in FindCoSchedule */
+    int64_t pad;
+} kl_stats;
+typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;
-    int32_t kind, lane;
+    int32_t kind, lane;        /* lane = stream of the launch pool */
     uint32_t cap, slice, start, end, executed, admitted, max_per_sm, exhausted;
-    int64_t t0_ns, t1_ns;
-    int32_t phase, partner_kind;
-    double cp;
+    int64_t t0_ns, t1_ns;      /* first admitted block start, last block end (globaltimer) */
+    int32_t phase;             /* index of the FindCoSchedule decision that launched it */
+    int32_t partner_kind;      /* kind co-scheduled by that decision, -1 = solo */
+    double cp;                 /* predicted CP of that decision */
 } kl_trace_rec;
 
 /* ---- calls -------------------------------------------------------------------------------- */
@@ -190,8 +202,10 @@ kl_status kl_slice(kl_ctx* ctx, uint64_t id, uint32_t blocks_per_sm, uint32_t sl
                    kl_slice_plan* out);
 /* Batched model on the device: one prediction per candidate. */
 kl_status kl_predict(kl_ctx* ctx, const kl_candidate* cands, size_t n, kl_prediction* out);
-/* FindCoSchedule over the pending set + launch of one co-schedule phase on the two
- * lanes (non-blocking; a previous phase is retired first).  KL_ENOTFOUND if R is empty. */
+/* One step of Alg.1: wait for the next scheduling event (a kernel ran out of thread blocks, or
+ * the first call), run FindCoSchedule over the pending set and reconcile the running
+ * co-schedule with it (launch / stop at a slice boundary); returns without waiting for the
+ * kernels.  KL_ENOTFOUND once R is empty. */
 kl_status kl_schedule(kl_ctx* ctx, kl_coschedule* out);
 /* Drive Alg.1 until R is empty, wait for the device, return this GPU's counters. */
 kl_status kl_sync(kl_ctx* ctx, kl_counters* out);
@@ -212,9 +226,10 @@ kl_status kl_audit(kl_ctx* ctx, uint64_t id, uint32_t* host_out, size_t n);
 /* FindCoSchedule decision only (no launch) for the current pending set; runs the device model
  * on a prediction-cache miss.  KL_EBUSY while a phase is in flight. */
 kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out);
+kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out);
 /* ABI self-check: writes sizeof() of kl_config, kl_profile, kl_kernel_desc, kl_slice_plan,
- * kl_candidate, kl_prediction, kl_coschedule, kl_counters, kl_trace_rec, then the ten kl_args_*
- * structs in kl_kind order (19 values) into out[0..n); returns how many it wrote. */
+ * kl_candidate, kl_prediction, kl_coschedule, kl_counters, kl_trace_rec, kl_stats, then the ten
+ * kl_args_* structs in kl_kind order (20 values) into out[0..n); returns how many it wrote. */
 int kl_struct_sizes(uint32_t* out, int n);
 
 #ifdef __cplusplus

@@ -111,7 +111,7 @@ class Config(C.Structure):
 
 class KernelDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("grid_blocks", C.c_uint32), ("args", _vp), ("args_bytes", C.c_uint32),
-                ("profile", C.POINTER(Profile)), ("tag", C.c_uint64)]
+                ("profile", C.POINTER(Profile)), ("tag", C.c_uint64), ("ready_event", _vp)]
 
 
 class SlicePlan(C.Structure):
@@ -140,6 +140,11 @@ class Counters(C.Structure):
                                          "checksum", "rank", "world", "phases")]
 
 
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("decisions", "launches", "stops", "model_batches", "model_candidates",
+                                         "device_launches", "decide_ns", "pad")]
+
+
 class TraceRec(C.Structure):
     _fields_ = [("id", C.c_uint64), ("kind", C.c_int32), ("lane", C.c_int32), ("cap", C.c_uint32),
                 ("slice", C.c_uint32), ("start", C.c_uint32), ("end", C.c_uint32), ("executed", C.c_uint32),
@@ -151,9 +156,9 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
-           "Counters", "TraceRec", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
+           "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
 
 _lib = None
@@ -188,6 +193,7 @@ def lib() -> C.CDLL:
     L.kl_trace.argtypes = [_vp, P(TraceRec), C.c_size_t, P(C.c_size_t)]
     L.kl_audit.argtypes = [_vp, C.c_uint64, P(C.c_uint32), C.c_size_t]
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
+    L.kl_stats_get.argtypes = [_vp, P(Stats)]
     for s in ABI_SYMBOLS:
         if s not in ("kl_abi_version", "kl_last_error", "kl_struct_sizes"):
             getattr(L, s).restype = C.c_int
@@ -270,10 +276,14 @@ class Context:
         self.close()
 
     # -- ABI calls --
-    def submit(self, kind, grid_blocks: int, args, tag: int = 0, profile: Profile | None = None) -> int:
+    def submit(self, kind, grid_blocks: int, args, tag: int = 0, profile: Profile | None = None,
+               ready_event=None) -> int:
+        """Alg.1 l.2-3: add a kernel to R.  `ready_event` (torch.cuda.Event or raw cudaEvent_t)
+        is waited on by every launch of the kernel (its inputs have landed)."""
         kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
+        ev = getattr(ready_event, "cuda_event", ready_event) if ready_event is not None else None
         d = KernelDesc(kid, grid_blocks, C.cast(C.pointer(args), _vp), C.sizeof(args),
-                       C.pointer(profile) if profile is not None else None, tag)
+                       C.pointer(profile) if profile is not None else None, tag, ev)
         out = C.c_uint64()
         self._check(self._L.kl_submit(self._h, C.byref(d), C.byref(out)))
         self._keep[out.value] = args
@@ -315,7 +325,7 @@ class Context:
 
     def run_plain(self, kind, grid_blocks: int, args, stream=0, offset: int = 0, n_blocks: int | None = None):
         kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
-        d = KernelDesc(kid, grid_blocks, C.cast(C.pointer(args), _vp), C.sizeof(args), None, 0)
+        d = KernelDesc(kid, grid_blocks, C.cast(C.pointer(args), _vp), C.sizeof(args), None, 0, None)
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         n = grid_blocks - offset if n_blocks is None else n_blocks
         self._check(self._L.kl_run_plain(self._h, C.byref(d), s, offset, n))
@@ -341,6 +351,11 @@ class Context:
         arr = (TraceRec * max(n.value, 1))()
         self._check(self._L.kl_trace(self._h, arr, n.value, C.byref(n)))
         return list(arr)[: n.value]
+
+    def stats(self) -> Stats:
+        s = Stats()
+        self._check(self._L.kl_stats_get(self._h, C.byref(s)))
+        return s
 
     def audit(self, kid: int, n: int):
         """Per-virtual-block execution counts of kernel `kid` (coverage audit)."""

@@ -6,14 +6,33 @@
 // ---------------------------------------------------------------------------------------------
 // Slice control block (one per submitted kernel instance, device memory).
 // A kernel's virtual block range [0, len) is consumed by work-pulling persistent blocks; the
-// 64-bit `word` linearises every fetch and every stop:
-//   bits [31:0]  next   : next virtual block to hand out (absolute)
-//   bits [62:32] stop_at: absolute slice boundary after which the current launch stops
-//   bit  63      stop   : stop requested for the current launch
-// Fetch = atomicAdd(word, chunk); stop = CAS that sets stop/stop_at = first slice boundary at or
-// after `next`.  Hence every handed-out block below the final limit runs exactly once and
-// [limit, len) stays pending (every block in exactly one co-schedule).
+// 64-bit `word` linearises every fetch and every stop of the current launch:
+//   bits [0,28)  next    : next virtual block to hand out (absolute)
+//   bits [28,56) stop_at : absolute slice boundary at which the current launch stops
+//   bits [56,63) epoch   : launch counter of this kernel (mod 128)
+//   bit  63      stop    : stop requested for the current launch
+// Fetch = atomicAdd(word, chunk); stop = CAS (only for the expected epoch) setting stop_at to the
+// first slice boundary at or after `next` (at least one slice into the launch).  Hence every
+// handed-out block below the final limit runs exactly once and [limit, len) stays pending
+// (every thread block in exactly one co-schedule).  len < 2^27.
 // ---------------------------------------------------------------------------------------------
+#define KL_W_NEXT_BITS 28
+#define KL_W_MASK28 ((1ull << 28) - 1ull)
+#define KL_W_STOP (1ull << 63)
+#define KL_MAX_GRID (1u << 27)
+#if defined(__CUDACC__)
+#define KL_HD __host__ __device__ __forceinline__
+#else
+#define KL_HD inline
+#endif
+KL_HD uint32_t kl_w_next(unsigned long long w) { return (uint32_t)(w & KL_W_MASK28); }
+KL_HD uint32_t kl_w_stop_at(unsigned long long w) { return (uint32_t)((w >> 28) & KL_W_MASK28); }
+KL_HD uint32_t kl_w_epoch(unsigned long long w) { return (uint32_t)((w >> 56) & 0x7full); }
+KL_HD unsigned long long kl_w_make(uint32_t next, uint32_t stop_at, uint32_t epoch, bool stop) {
+    return ((unsigned long long)next & KL_W_MASK28) | (((unsigned long long)stop_at & KL_W_MASK28) << 28) |
+           (((unsigned long long)epoch & 0x7full) << 56) | (stop ? KL_W_STOP : 0ull);
+}
+
 struct KlCtl {
     unsigned long long word;
     uint32_t len;
@@ -21,30 +40,30 @@ struct KlCtl {
     uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
     uint32_t admitted;    // admitted blocks of the current launch
     uint32_t executed;    // virtual blocks executed in the current launch
-    uint32_t pad0;
+    uint32_t base;        // first virtual block of the current launch (slice boundaries)
     unsigned long long t0;  // earliest admitted-block start (globaltimer ns), current launch
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
 };
 
-// Host-mapped (pinned) record written by the last block of a launch.
+// Host-mapped (pinned) record of one launch: `drained` is raised by the first block that finds
+// the kernel's range exhausted, the rest by the launch's last block.
 struct KlLaunchRec {
+    volatile uint32_t drained;
+    volatile uint32_t done;
+    uint32_t start;       // first virtual block of the launch
     uint32_t end;         // first virtual block not executed (absolute)
     uint32_t exhausted;   // end == len
-    uint32_t executed, admitted, max_per_sm, pad;
+    uint32_t executed, admitted, max_per_sm;
     unsigned long long t0, t1;
-    volatile uint32_t done;
-    uint32_t pad2;
 };
 
 struct KlLaunch {
     KlCtl* ctl;
-    KlCtl* partner;                 // stopped when this kernel drains (nullptr: solo phase)
     uint32_t cap;                   // admitted blocks per SM (0 = no cap)
     uint32_t chunk;                 // virtual blocks per fetch
-    uint32_t start;                 // this launch's first virtual block
-    uint32_t partner_start, partner_slice;
     uint32_t n_sms;
+    uint32_t pad;
     KlLaunchRec* rec;
     unsigned long long* counters;   // kl_counters on the device (may be null)
     uint32_t* audit;                // per-virtual-block execution counts (may be null)
@@ -96,6 +115,11 @@ struct KlDecision {
     volatile int32_t done;
     int32_t pad;
 };
+// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream);
+// Stop the current launch (epoch `epoch`) of a kernel at its next slice boundary.
+int kl_dev_stop(KlCtl* ctl, uint32_t epoch, uint32_t slice, void* stream);
+
 // Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy
 // selection (a9) and writes *dec.  `done_counter` must be zero on entry (reset by the kernel).
 int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands,

@@ -1,12 +1,14 @@
 // kl_launcher.cuh -- the persistent slice launcher shared by every kernel body (product path).
 //
 // Slicing: a slice is a contiguous range of a kernel's thread blocks launched with
-// its block index rectified by an offset.  On B200 a phase launches ONE persistent grid per
-// kernel (cap x n_SM blocks); each admitted block pulls virtual block ids from the kernel's
-// slice control word (KlCtl) and runs Body::block(vb).  Occupancy control is a per-SM admission
-// cap read from %smid.  When a kernel drains, its first block to notice stops the partner's
-// launch at the partner's next slice boundary (Alg.1 l.9).  Included by kl_kernels.cu and
-// kl_mm.cu (header-only so no relocatable device code is needed).
+// its block index rectified by an offset.  On B200 a co-schedule launches ONE persistent grid per
+// kernel (cap x n_SM blocks, plus slack); each admitted block pulls virtual block ids from the
+// kernel's slice control word (KlCtl::word) and runs Body::block(vb) -- index rectification as a
+// kernel parameter instead of Fermi SASS rewriting.  Occupancy control is a per-SM
+// admission cap read from %smid.  The first block to find the range exhausted raises the
+// kernel's `drained` event in host-mapped memory (Alg.1 l.9: "K1 and K2 both still have thread
+// blocks" turns false), which is what the host scheduler reacts to; a host-requested stop (k_stop)
+// ends a launch at its next slice boundary.  Header-only: included by kl_kernels.cu and kl_mm.cu.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -25,49 +27,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// ------------------------------------------------------------------------------------------
-// Slice launcher.
-// ------------------------------------------------------------------------------------------
-// Stop the partner's current launch at its first slice boundary at or after its current
-// position (Alg.1 l.9: the co-schedule is kept only while both kernels still have blocks).
-__device__ void stop_at_boundary(KlCtl* p, uint32_t pstart, uint32_t pslice) {
-    unsigned long long old = atomicAdd(&p->word, 0ull);
-    for (;;) {
-        if (old >> 63) return;
-        uint32_t nx = (uint32_t)old;
-        uint32_t rel = nx > pstart ? nx - pstart : 0u;
-        uint32_t sl = pslice ? pslice : 1u;
-        // first slice boundary at or after the current position, but at least one slice into
-        // the launch: a co-schedule runs a slice of each kernel, even when the
-        // partner's blocks had not been dispatched yet when this kernel drained
-        unsigned long long nsl = (unsigned long long)(rel + sl - 1) / sl;
-        if (nsl == 0) nsl = 1;
-        unsigned long long sa = (unsigned long long)pstart + nsl * sl;
-        if (sa < nx) sa = nx;
-        if (sa > 0x7fffffffull) sa = 0x7fffffffull;
-        unsigned long long nw = (old & 0xffffffffull) | (sa << 32) | (1ull << 63);
-        unsigned long long prev = atomicCAS(&p->word, old, nw);
-        if (prev == old) return;
-        old = prev;
-    }
+// Effective limit of the current launch from a word value: min(len, stop_at if stopped).
+__device__ __forceinline__ uint32_t word_limit(unsigned long long w, uint32_t len) {
+    uint32_t lim = len;
+    if (w & KL_W_STOP) lim = min(lim, kl_w_stop_at(w));
+    return lim;
 }
 
 __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     KlCtl* ctl = L.ctl;
     __threadfence();
-    unsigned long long w = atomicAdd(&ctl->word, 0ull);
-    uint32_t lim = len;
-    if (w >> 63) lim = min(lim, (uint32_t)((w >> 32) & 0x7fffffffu));
-    uint32_t executed = atomicExch(&ctl->executed, 0u);
-    uint32_t admitted = atomicExch(&ctl->admitted, 0u);
+    const unsigned long long w = atomicAdd(&ctl->word, 0ull);
+    const uint32_t lim = word_limit(w, len);
+    const uint32_t executed = atomicExch(&ctl->executed, 0u);
+    const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
     uint32_t mx = 0;
     for (uint32_t s = 0; s < L.n_sms && s < KL_MAX_SMS; ++s) {
         mx = max(mx, ctl->sm_hwm[s]);
         ctl->sm_hwm[s] = 0;
     }
-    unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
-    unsigned long long t1 = gtimer();
-    atomicExch(&ctl->word, (unsigned long long)lim);   // next = lim, stop cleared
+    const unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
+    const unsigned long long t1 = gtimer();
+    const uint32_t start = ctl->base;
+    ctl->base = lim;
+    // next launch: next = lim, stop cleared, epoch + 1
+    atomicExch(&ctl->word, kl_w_make(lim, 0u, kl_w_epoch(w) + 1u, false));
     atomicExch(&ctl->exited, 0u);
     const bool exh = (lim == len);
     if (L.counters) {
@@ -81,6 +65,7 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     }
     KlLaunchRec* r = L.rec;
     if (r) {
+        r->start = start;
         r->end = lim;
         r->exhausted = exh ? 1u : 0u;
         r->executed = executed;
@@ -127,14 +112,16 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         uint32_t nexec = 0;
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
-                unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-                uint32_t vb = (uint32_t)old;
-                uint32_t lim = len;
-                if (old >> 63) lim = min(lim, (uint32_t)((old >> 32) & 0x7fffffffu));
-                uint32_t end = vb < lim ? min(vb + L.chunk, lim) : vb;
-                if (vb >= len && lim == len && L.partner) {
-                    if (atomicCAS(&ctl->drained, 0u, 1u) == 0u)
-                        stop_at_boundary(L.partner, L.partner_start, L.partner_slice);
+                const unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                const uint32_t vb = kl_w_next(old);
+                const uint32_t lim = word_limit(old, len);
+                const uint32_t end = vb < lim ? min(vb + L.chunk, lim) : vb;
+                if (vb >= len && lim == len && L.rec) {
+                    // the kernel has no more thread blocks: raise the drained event once
+                    if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
+                        L.rec->drained = 1u;
+                        __threadfence_system();
+                    }
                 }
                 s_vb[it & 1] = vb;
                 s_end[it & 1] = end;
@@ -156,7 +143,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
     }
     if (threadIdx.x == 0) {
         __threadfence();
-        uint32_t e = atomicAdd(&ctl->exited, 1u);
+        const uint32_t e = atomicAdd(&ctl->exited, 1u);
         if (e == gridDim.x - 1) finalize_launch(L, len);
     }
 }
@@ -175,14 +162,15 @@ k_plain(const __grid_constant__ typename Body::Params P, uint32_t offset) {
 template <class Body>
 int info_of(KlKindInfo* o) {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k_persistent<Body>);
-    if (e != cudaSuccess) return (int)e;
+    cudaError_t e;
     if (Body::kDynSmem > 48 * 1024) {
         e = cudaFuncSetAttribute(k_persistent<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
         if (e != cudaSuccess) return (int)e;
         e = cudaFuncSetAttribute(k_plain<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
         if (e != cudaSuccess) return (int)e;
     }
+    e = cudaFuncGetAttributes(&fa, k_persistent<Body>);
+    if (e != cudaSuccess) return (int)e;
     int nb = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_persistent<Body>, Body::kThreads, Body::kDynSmem);
     if (e != cudaSuccess) return (int)e;
@@ -210,6 +198,5 @@ int launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream) {
     k_plain<Body><<<n, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, offset);
     return (int)cudaGetLastError();
 }
-
 
 }  // namespace

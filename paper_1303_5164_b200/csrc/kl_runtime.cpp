@@ -4,12 +4,19 @@
 //   candidate pairs -> PUR/MUR pruning (AND reading R9, halving R10/R24)
 //   -> maximal occupancy splits (a5, R7) -> batched device model (kl_model.cu, cached per
 //   (kind1, kind2, b1, b2)) -> selection a9 (device-fused on a cache miss, host otherwise; the
-//   two are the same rules) -> one co-schedule phase on two lanes (streams) of persistent slice
-//   launchers (kl_kernels.cu), retired when both lanes report through host-mapped records.
+//   two are the same rules) -> reconcile the running co-schedule with the decision.
+// Execution is event driven: each persistent launch (kl_launcher.cuh) raises `drained` in a
+// host-mapped record when its kernel runs out of thread blocks; the host then re-plans while the
+// kernel's last blocks finish, keeps the surviving kernel running when the new decision keeps its
+// occupancy, stops it at a slice boundary (epoch-checked CAS, k_stop) only when the decision
+// changes it, and launches successors on a pool of streams so their blocks take SM slots as the
+// predecessor's tail blocks exit.
 #include <cuda_runtime.h>
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -46,30 +53,41 @@ const kl_profile kDefaultProfiles[KL_NKINDS] = {
     /* SYNTH*/ {0.10, 16.0, 320.0, 0.5, 0.5, 0, 0, 0, 0, 0, 1},
 };
 
+constexpr int kRecRing = 1024;
+constexpr int kPool = 8;
+
+struct Launch;
+
 struct Inst {
     uint64_t id = 0, seq = 0, tag = 0;
     int kind = 0;
     uint32_t grid = 0;
     alignas(128) unsigned char blob[kBlob];
     int slot = -1;
-    uint32_t next = 0;
-    bool done = false;
+    uint32_t next = 0;          // host view: first virtual block not yet retired
+    uint32_t epoch = 0;         // launches issued (matches the control word's epoch mod 128)
+    bool drained = false;       // no more thread blocks (out of R)
+    bool finished = false;      // drained and every launch retired
+    Launch* inflight = nullptr; // at most one launch in flight per kernel
     uint32_t* audit = nullptr;
+    void* ready = nullptr;      // cudaEvent_t to wait on before launching
 };
 
-struct Lane {
-    cudaStream_t s = nullptr;
-    bool own = false;
-    KlLaunchRec* rec = nullptr;
-    Inst* inst = nullptr;
-    uint32_t cap = 0, slice = 0, start = 0;
-    int partner_kind = -1;
+struct Launch {
+    Inst* k = nullptr;
+    int rec = -1, stream = 0;
+    uint32_t cap = 0, slice = 0, epoch = 0;
+    bool stop_requested = false;
+    int32_t decision = 0, partner_kind = -1;
+    double cp = 0.0;
 };
 
 struct Decision {
     bool solo = true;
     int ia = 0, ib = -1;            // indices into R
-    uint32_t b1 = 0, b2 = 0;
+    Inst* k1 = nullptr;
+    Inst* k2 = nullptr;
+    uint32_t b1 = 0, b2 = 0;        // caps (solo: b1 = solo level, launched uncapped)
     double cp = 0.0;
     int n_cand = 0;
 };
@@ -91,8 +109,16 @@ struct kl_ctx {
     KlKindInfo info[KL_NKINDS]{};
     bool info_ok[KL_NKINDS]{};
     int n_sms = 148, max_warps = 64, max_blocks = 32, max_regs = 65536, max_smem = 233472;
-    Lane lane[2];
-    cudaStream_t ctrl = nullptr;
+    cudaStream_t pool[kPool] = {};
+    bool pool_own[kPool] = {};
+    int pool_busy[kPool] = {};
+    cudaStream_t ctrl = nullptr, stopper = nullptr;
+    KlLaunchRec* recs = nullptr;       // mapped ring of launch records
+    std::vector<int> free_recs;
+    std::vector<std::unique_ptr<Launch>> inflight;
+    Decision desired;
+    bool have_desired = false;
+    kl_stats st{};
     cudaEvent_t init_ev = nullptr;
     KlCtl* ctl_pool = nullptr;
     std::vector<int> free_slots;
@@ -116,10 +142,6 @@ struct kl_ctx {
     KlDecision* dec_pinned = nullptr;
     std::unordered_map<uint64_t, kl_prediction> cache;
     int64_t model_batches = 0, model_cands = 0;
-    // phases
-    bool in_flight = false;
-    int64_t phases = 0;
-    double phase_cp = 0.0;
     std::vector<kl_trace_rec> trace;
     int64_t* counters = nullptr;
 
@@ -272,6 +294,7 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
     ctx->model_batches++;
     ctx->model_cands += n;
+    ctx->st.device_launches++;
     for (int i = 0; i < n; ++i) {
         const KlCand& cd = ctx->cand_pinned[i];
         ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)] = ctx->pred_pinned[i];
@@ -366,6 +389,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     if (best < 0) {   // solo: oldest pending kernel at its solo maximum occupancy (R25)
         d->solo = true;
         d->ia = 0;
+        d->k1 = R[0];
         d->b1 = solo_level(ctx, ctx->prof[R[0]->kind]);
         d->cp = 0.0;
         return KL_OK;
@@ -374,148 +398,282 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     d->solo = false;
     d->ia = pair_of_group[cd.pair].first;
     d->ib = pair_of_group[cd.pair].second;
+    d->k1 = R[d->ia];
+    d->k2 = R[d->ib];
     d->b1 = cd.b1;
     d->b2 = cd.b2;
     d->cp = bcp;
     return KL_OK;
 }
 
-uint32_t slice_of(const kl_ctx* c, const kl_profile& p, uint32_t b, int m) {
-    return (uint32_t)std::max(1, m) * b * (uint32_t)c->n_sms;
+kl_status decide(kl_ctx* ctx, Decision* d) {
+    auto t0 = std::chrono::steady_clock::now();
+    kl_status st = find_co_schedule(ctx, d);
+    ctx->st.decide_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (st == KL_OK) ctx->st.decisions++;
+    return st;
+}
+
+uint32_t slice_of(const kl_ctx* c, uint32_t b, int m) {
+    return (uint32_t)std::max(1, m) * std::max(1u, b) * (uint32_t)c->n_sms;
+}
+
+// m of the p% rule for a decision: the common number of waves per slice (a9)
+int waves_of(const kl_ctx* c, const Decision& d) {
+    int m = std::max(1, c->prof[d.k1->kind].m_min);
+    if (d.k2) m = std::max(m, c->prof[d.k2->kind].m_min);
+    return m;
 }
 
 kl_status flush_ctl_init(kl_ctx* ctx) {
     if (ctx->n_init == 0) return KL_OK;
     int rc = kl_dev_ctl_init(ctx->ctl_pool, ctx->init_pinned, ctx->n_init, ctx->ctrl);
     if (rc) return ctx->fail(KL_ECUDA, "ctl init: %s", cudaGetErrorString((cudaError_t)rc));
+    ctx->st.device_launches++;
     KL_CUDA(cudaEventRecord(ctx->init_ev, ctx->ctrl));
-    KL_CUDA(cudaStreamWaitEvent(ctx->lane[0].s, ctx->init_ev, 0));
-    KL_CUDA(cudaStreamWaitEvent(ctx->lane[1].s, ctx->init_ev, 0));
+    for (int i = 0; i < kPool; ++i) KL_CUDA(cudaStreamWaitEvent(ctx->pool[i], ctx->init_ev, 0));
+    KL_CUDA(cudaStreamWaitEvent(ctx->stopper, ctx->init_ev, 0));
     // the mapped init list is read by the kernel: wait before it can be overwritten
     KL_CUDA(cudaEventSynchronize(ctx->init_ev));
     ctx->n_init = 0;
     return KL_OK;
 }
 
-kl_status launch_lane(kl_ctx* ctx, int li, Inst* k, uint32_t cap, uint32_t slice, Inst* partner,
-                      uint32_t partner_slice, double cp) {
-    Lane& ln = ctx->lane[li];
+int pick_stream(kl_ctx* ctx) {
+    int best = 0;
+    for (int i = 1; i < kPool; ++i)
+        if (ctx->pool_busy[i] < ctx->pool_busy[best]) best = i;
+    return best;
+}
+
+kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp) {
+    if (ctx->free_recs.empty()) return ctx->fail(KL_ENOMEM, "launch record ring exhausted");
     const KlKindInfo& inf = ctx->info[k->kind];
-    KlLaunch L{};
-    L.ctl = ctx->ctl_pool + k->slot;
-    L.partner = partner ? ctx->ctl_pool + partner->slot : nullptr;
-    L.cap = cap;
-    L.chunk = (uint32_t)(ctx->cfg.chunk > 0 ? ctx->cfg.chunk : inf.default_chunk);
-    L.start = k->next;
-    L.partner_start = partner ? partner->next : 0;
-    L.partner_slice = partner_slice;
-    L.n_sms = (uint32_t)ctx->n_sms;
-    L.rec = ln.rec;
-    L.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
-    L.audit = k->audit;
-    L.tag = k->tag;
-    const uint32_t per_sm = cap ? cap : (uint32_t)inf.bmax;
+    auto L = std::make_unique<Launch>();
+    L->k = k;
+    L->rec = ctx->free_recs.back();
+    ctx->free_recs.pop_back();
+    L->stream = pick_stream(ctx);
+    L->cap = cap;
+    L->slice = slice;
+    L->epoch = k->epoch++;
+    L->decision = (int32_t)ctx->st.decisions;
+    L->partner_kind = partner_kind;
+    L->cp = cp;
+    KlLaunchRec* rec = ctx->recs + L->rec;
+    std::memset(rec, 0, sizeof(*rec));
+    KlLaunch P{};
+    P.ctl = ctx->ctl_pool + k->slot;
+    P.cap = cap;
+    P.chunk = (uint32_t)(ctx->cfg.chunk > 0 ? ctx->cfg.chunk : inf.default_chunk);
+    P.n_sms = (uint32_t)ctx->n_sms;
+    P.rec = rec;
+    P.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
+    P.audit = k->audit;
+    P.tag = k->tag;
+    // grid: cap blocks per SM plus slack, so SMs whose slots free up late (the predecessor's tail
+    // blocks) still receive their share; surplus blocks fail admission and exit at once
+    const uint32_t per_sm = cap ? cap : (uint32_t)std::max(1, inf.bmax);
     uint32_t grid = per_sm * (uint32_t)ctx->n_sms;
+    if (cap) grid += std::max((uint32_t)ctx->n_sms, grid / 4);
     const uint32_t remaining = k->grid - k->next;
-    if (grid > remaining) grid = std::max(1u, remaining);
-    ln.rec->done = 0;
-    ln.inst = k;
-    ln.cap = cap;
-    ln.slice = slice;
-    ln.start = k->next;
-    ln.partner_kind = partner ? partner->kind : -1;
-    int rc = kl_dev_launch_persistent(k->kind, k->blob, L, grid, ln.s);
+    const uint32_t need = (remaining + P.chunk - 1) / P.chunk;
+    if (grid > need && !cap) grid = std::max(1u, need);
+    cudaStream_t s = ctx->pool[L->stream];
+    if (k->ready) KL_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)k->ready, 0));
+    int rc = kl_dev_launch_persistent(k->kind, k->blob, P, grid, s);
     if (rc) return ctx->fail(KL_ECUDA, "launch kind %d: %s", k->kind, cudaGetErrorString((cudaError_t)rc));
-    (void)cp;
+    ctx->pool_busy[L->stream]++;
+    ctx->st.launches++;
+    ctx->st.device_launches++;
+    k->inflight = L.get();
+    ctx->inflight.push_back(std::move(L));
     return KL_OK;
 }
 
-kl_status retire_phase(kl_ctx* ctx) {
-    if (!ctx->in_flight) return KL_OK;
-    for (int li = 0; li < 2; ++li) {
-        Lane& ln = ctx->lane[li];
-        if (!ln.inst) continue;
-        uint64_t spins = 0;
-        while (!ln.rec->done) {
-            _mm_pause();
-            if ((++spins & 0xFFFF) == 0) {
-                cudaError_t e = cudaStreamQuery(ln.s);
-                if (e != cudaSuccess && e != cudaErrorNotReady)
-                    return ctx->fail(KL_ECUDA, "phase %lld lane %d: %s", (long long)ctx->phases, li, cudaGetErrorString(e));
-                if (e == cudaSuccess && !ln.rec->done)
-                    return ctx->fail(KL_ECUDA, "phase %lld lane %d finished without a record", (long long)ctx->phases, li);
-            }
+kl_status request_stop(kl_ctx* ctx, Launch* L) {
+    if (L->stop_requested) return KL_OK;
+    int rc = kl_dev_stop(ctx->ctl_pool + L->k->slot, L->epoch, L->slice, ctx->stopper);
+    if (rc) return ctx->fail(KL_ECUDA, "stop: %s", cudaGetErrorString((cudaError_t)rc));
+    L->stop_requested = true;
+    ctx->st.stops++;
+    ctx->st.device_launches++;
+    return KL_OK;
+}
+
+// Bring the running co-schedule in line with the desired decision: stop launches the decision
+// no longer wants (or wants at another occupancy), launch wanted kernels that are idle.
+kl_status reconcile(kl_ctx* ctx) {
+    if (!ctx->have_desired) return KL_OK;
+    const Decision& d = ctx->desired;
+    const int m = waves_of(ctx, d);
+    struct Want { Inst* k; uint32_t cap, slice; int partner; };
+    Want w[2];
+    int nw = 0;
+    if (d.solo) {
+        w[nw++] = {d.k1, 0u, slice_of(ctx, d.b1, m), -1};
+    } else {
+        w[nw++] = {d.k1, d.b1, slice_of(ctx, d.b1, m), d.k2->kind};
+        w[nw++] = {d.k2, d.b2, slice_of(ctx, d.b2, m), d.k1->kind};
+    }
+    for (auto& Lp : ctx->inflight) {
+        Launch* L = Lp.get();
+        if (L->stop_requested || L->k->drained) continue;
+        bool keep = false;
+        for (int i = 0; i < nw; ++i)
+            if (w[i].k == L->k && w[i].cap == L->cap) keep = true;
+        if (!keep) {
+            kl_status st = request_stop(ctx, L);
+            if (st) return st;
         }
     }
-    for (int li = 0; li < 2; ++li) {
-        Lane& ln = ctx->lane[li];
-        if (!ln.inst) continue;
-        Inst* k = ln.inst;
-        const KlLaunchRec& r = *ln.rec;
+    for (int i = 0; i < nw; ++i) {
+        Inst* k = w[i].k;
+        if (k->drained || k->inflight) continue;   // running as wanted, or stopping: relaunch later
+        kl_status st = launch_kernel(ctx, k, w[i].cap, w[i].slice, w[i].partner, d.cp);
+        if (st) return st;
+    }
+    return KL_OK;
+}
+
+void mark_drained(kl_ctx* ctx, Inst* k) {
+    if (k->drained) return;
+    k->drained = true;
+    auto& R = ctx->R;
+    R.erase(std::remove(R.begin(), R.end(), k), R.end());
+}
+
+// Poll the launch records.  Returns through *replan whether R changed (a kernel drained) and
+// through *progress whether anything happened at all.
+kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
+    for (size_t i = 0; i < ctx->inflight.size();) {
+        Launch* L = ctx->inflight[i].get();
+        KlLaunchRec* r = ctx->recs + L->rec;
+        if (r->drained && !L->k->drained) {
+            mark_drained(ctx, L->k);
+            *replan = *progress = true;
+        }
+        if (!r->done) {
+            ++i;
+            continue;
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        Inst* k = L->k;
         kl_trace_rec t{};
         t.id = k->id;
         t.kind = k->kind;
-        t.lane = li;
-        t.cap = ln.cap;
-        t.slice = ln.slice;
-        t.start = ln.start;
-        t.end = r.end;
-        t.executed = r.executed;
-        t.admitted = r.admitted;
-        t.max_per_sm = r.max_per_sm;
-        t.exhausted = r.exhausted;
-        t.t0_ns = (int64_t)r.t0;
-        t.t1_ns = (int64_t)r.t1;
-        t.phase = (int32_t)ctx->phases;
-        t.partner_kind = ln.partner_kind;
-        t.cp = ctx->phase_cp;
+        t.lane = L->stream;
+        t.cap = L->cap;
+        t.slice = L->slice;
+        t.start = r->start;
+        t.end = r->end;
+        t.executed = r->executed;
+        t.admitted = r->admitted;
+        t.max_per_sm = r->max_per_sm;
+        t.exhausted = r->exhausted;
+        t.t0_ns = (int64_t)r->t0;
+        t.t1_ns = (int64_t)r->t1;
+        t.phase = L->decision;
+        t.partner_kind = L->partner_kind;
+        t.cp = L->cp;
         ctx->trace.push_back(t);
-        k->next = r.end;
-        if (r.exhausted) {
-            k->done = true;
+        k->next = r->end;
+        k->inflight = nullptr;
+        if (r->exhausted) {
+            if (!k->drained) {
+                mark_drained(ctx, k);
+                *replan = true;
+            }
+            k->finished = true;
             ctx->free_slots.push_back(k->slot);
         }
-        ln.inst = nullptr;
+        ctx->pool_busy[L->stream]--;
+        ctx->free_recs.push_back(L->rec);
+        ctx->inflight.erase(ctx->inflight.begin() + i);
+        *progress = true;
     }
-    auto& R = ctx->R;
-    R.erase(std::remove_if(R.begin(), R.end(), [](Inst* k) { return k->done; }), R.end());
-    ctx->in_flight = false;
-    ctx->phases++;
     return KL_OK;
 }
 
-kl_status launch_phase(kl_ctx* ctx, const Decision& d, kl_coschedule* out) {
+kl_status check_streams(kl_ctx* ctx) {
+    for (int i = 0; i < kPool; ++i) {
+        if (!ctx->pool_busy[i]) continue;
+        cudaError_t e = cudaStreamQuery(ctx->pool[i]);
+        if (e != cudaSuccess && e != cudaErrorNotReady)
+            return ctx->fail(KL_ECUDA, "stream %d: %s", i, cudaGetErrorString(e));
+    }
+    return KL_OK;
+}
+
+void fill_cs(kl_ctx* ctx, const Decision& d, kl_coschedule* out) {
+    if (!out) return;
+    *out = kl_coschedule{};
+    const int m = waves_of(ctx, d);
+    out->id1 = d.k1->id;
+    out->id2 = d.k2 ? d.k2->id : 0;
+    out->kind1 = d.k1->kind;
+    out->kind2 = d.k2 ? d.k2->kind : -1;
+    out->b1 = d.b1;
+    out->b2 = d.b2;
+    out->size1 = slice_of(ctx, d.b1, m);
+    out->size2 = d.k2 ? slice_of(ctx, d.b2, m) : 0;
+    out->cp = d.cp;
+    out->solo = d.solo ? 1 : 0;
+    out->n_candidates = d.n_cand;
+}
+
+// One Alg.1 decision: wait for a scheduling event (unless none was made yet), decide, reconcile.
+// Returns KL_ENOTFOUND when R is empty.
+kl_status schedule_step(kl_ctx* ctx, kl_coschedule* out) {
     kl_status st = flush_ctl_init(ctx);
     if (st) return st;
-    Inst* k1 = ctx->R[d.ia];
-    Inst* k2 = d.solo ? nullptr : ctx->R[d.ib];
-    const kl_profile& p1 = ctx->prof[k1->kind];
-    int m = std::max(1, p1.m_min);
-    if (k2) m = std::max(m, ctx->prof[k2->kind].m_min);
-    const uint32_t s1 = slice_of(ctx, p1, d.b1, m);
-    const uint32_t s2 = k2 ? slice_of(ctx, ctx->prof[k2->kind], d.b2, m) : 0;
-    ctx->phase_cp = d.cp;
-    if (k2) {
-        st = launch_lane(ctx, 0, k1, d.b1, s1, k2, s2, d.cp);
-        if (!st) st = launch_lane(ctx, 1, k2, d.b2, s2, k1, s1, d.cp);
-    } else {
-        st = launch_lane(ctx, 0, k1, 0, s1, nullptr, 0, 0.0);
+    bool replan = !ctx->have_desired, progress = false;
+    uint64_t spins = 0;
+    for (;;) {
+        st = poll(ctx, &replan, &progress);
+        if (st) return st;
+        if (progress && !replan) {          // a stopped launch ended: relaunch it if still wanted
+            st = reconcile(ctx);
+            if (st) return st;
+            progress = false;
+        }
+        if (ctx->R.empty()) {
+            ctx->have_desired = false;
+            return ctx->fail(KL_ENOTFOUND, "nothing pending");
+        }
+        if (replan || ctx->inflight.empty()) break;
+        _mm_pause();
+        if ((++spins & 0x3FFF) == 0) {
+            st = check_streams(ctx);
+            if (st) return st;
+        }
     }
+    Decision d;
+    st = decide(ctx, &d);
     if (st) return st;
-    ctx->in_flight = true;
-    if (out) {
-        *out = kl_coschedule{};
-        out->id1 = k1->id;
-        out->id2 = k2 ? k2->id : 0;
-        out->kind1 = k1->kind;
-        out->kind2 = k2 ? k2->kind : -1;
-        out->b1 = d.b1;
-        out->b2 = d.b2;
-        out->size1 = s1;
-        out->size2 = s2;
-        out->cp = d.cp;
-        out->solo = d.solo ? 1 : 0;
-        out->n_candidates = d.n_cand;
+    ctx->desired = d;
+    ctx->have_desired = true;
+    st = reconcile(ctx);
+    if (st) return st;
+    fill_cs(ctx, d, out);
+    return KL_OK;
+}
+
+kl_status drain_all(kl_ctx* ctx) {
+    uint64_t spins = 0;
+    while (!ctx->inflight.empty()) {
+        bool replan = false, progress = false;
+        kl_status st = poll(ctx, &replan, &progress);
+        if (st) return st;
+        if (progress && !ctx->R.empty()) {
+            st = reconcile(ctx);
+            if (st) return st;
+        }
+        _mm_pause();
+        if ((++spins & 0x3FFF) == 0) {
+            st = check_streams(ctx);
+            if (st) return st;
+        }
     }
     return KL_OK;
 }
@@ -530,7 +688,7 @@ int kl_abi_version(void) { return KL_ABI_VERSION; }
 int kl_struct_sizes(uint32_t* out, int n) {
     const uint32_t s[] = {sizeof(kl_config), sizeof(kl_profile), sizeof(kl_kernel_desc), sizeof(kl_slice_plan),
                           sizeof(kl_candidate), sizeof(kl_prediction), sizeof(kl_coschedule), sizeof(kl_counters),
-                          sizeof(kl_trace_rec), sizeof(kl_args_pc), sizeof(kl_args_sad), sizeof(kl_args_spmv),
+                          sizeof(kl_trace_rec), sizeof(kl_stats), sizeof(kl_args_pc), sizeof(kl_args_sad), sizeof(kl_args_spmv),
                           sizeof(kl_args_st), sizeof(kl_args_mm), sizeof(kl_args_mriq), sizeof(kl_args_bs),
                           sizeof(kl_args_tea), sizeof(kl_args_matadd), sizeof(kl_args_synth)};
     int m = (int)(sizeof(s) / sizeof(s[0]));
@@ -596,17 +754,21 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
                     if (!p.bmax) p.bmax = in.bmax;
                 }
             }
-            for (int li = 0; li < 2; ++li) {
-                void* s = li == 0 ? cfg.stream_a : cfg.stream_b;
+            for (int i = 0; i < kPool; ++i) {
+                void* s = i == 0 ? cfg.stream_a : (i == 1 ? cfg.stream_b : nullptr);
                 if (s) {
-                    ctx->lane[li].s = (cudaStream_t)s;
+                    ctx->pool[i] = (cudaStream_t)s;
                 } else {
-                    KL_CUDA(cudaStreamCreateWithFlags(&ctx->lane[li].s, cudaStreamNonBlocking));
-                    ctx->lane[li].own = true;
+                    KL_CUDA(cudaStreamCreateWithFlags(&ctx->pool[i], cudaStreamNonBlocking));
+                    ctx->pool_own[i] = true;
                 }
-                KL_CUDA(cudaHostAlloc(&ctx->lane[li].rec, sizeof(KlLaunchRec), cudaHostAllocMapped));
-                std::memset(ctx->lane[li].rec, 0, sizeof(KlLaunchRec));
             }
+            int lo = 0, hi = 0;
+            KL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            KL_CUDA(cudaStreamCreateWithPriority(&ctx->stopper, cudaStreamNonBlocking, hi));
+            KL_CUDA(cudaHostAlloc(&ctx->recs, sizeof(KlLaunchRec) * kRecRing, cudaHostAllocMapped));
+            std::memset(ctx->recs, 0, sizeof(KlLaunchRec) * kRecRing);
+            for (int r = kRecRing - 1; r >= 0; --r) ctx->free_recs.push_back(r);
             KL_CUDA(cudaStreamCreateWithFlags(&ctx->ctrl, cudaStreamNonBlocking));
             KL_CUDA(cudaEventCreateWithFlags(&ctx->init_ev, cudaEventDisableTiming));
             KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
@@ -643,14 +805,11 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
 kl_status kl_destroy(kl_ctx* ctx) {
     if (!ctx) return KL_EINVAL;
     if (!ctx->host_only) {
-        if (!ctx->poisoned) {
-            for (auto& l : ctx->lane) if (l.s) cudaStreamSynchronize(l.s);
-            if (ctx->ctrl) cudaStreamSynchronize(ctx->ctrl);
-        }
-        for (auto& l : ctx->lane) {
-            if (l.own && l.s) cudaStreamDestroy(l.s);
-            if (l.rec) cudaFreeHost(l.rec);
-        }
+        if (!ctx->poisoned) cudaDeviceSynchronize();
+        for (int i = 0; i < kPool; ++i)
+            if (ctx->pool_own[i] && ctx->pool[i]) cudaStreamDestroy(ctx->pool[i]);
+        if (ctx->stopper) cudaStreamDestroy(ctx->stopper);
+        if (ctx->recs) cudaFreeHost(ctx->recs);
         for (auto& k : ctx->insts) if (k->audit) cudaFree(k->audit);
         if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
         if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
@@ -678,7 +837,7 @@ kl_status kl_destroy(kl_ctx* ctx) {
 kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     KL_LIVE(ctx);
     if (!d || d->kind < 0 || d->kind >= KL_NKINDS) return ctx->fail(KL_EINVAL, "bad kind");
-    if (d->grid_blocks == 0 || d->grid_blocks >= 0x7fffffffu) return ctx->fail(KL_EINVAL, "grid_blocks out of range");
+    if (d->grid_blocks == 0 || d->grid_blocks >= KL_MAX_GRID) return ctx->fail(KL_EINVAL, "grid_blocks out of range");
     if (!d->args || d->args_bytes != kl_args_size(d->kind))
         return ctx->fail(KL_EINVAL, "args_bytes %u != sizeof(kl_args) %u for kind %d", d->args_bytes, kl_args_size(d->kind), d->kind);
     if (d->profile) {
@@ -695,6 +854,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     k->kind = d->kind;
     k->grid = d->grid_blocks;
     k->tag = d->tag;
+    k->ready = d->ready_event;
     if (!ctx->host_only) {
         if (kl_dev_prepare(d->kind, d->args, d->args_bytes, k->blob, kBlob))
             return ctx->fail(KL_EINVAL, "cannot prepare args of kind %d", d->kind);
@@ -730,7 +890,7 @@ kl_status kl_slice(kl_ctx* ctx, uint64_t id, uint32_t b, uint32_t slice_blocks, 
         static const char* names[] = {"", "warps", "blocks", "registers", "smem", "TMEM"};
         return ctx->fail(KL_EINFEASIBLE, "%u blocks/SM of kind %d exceed %s", b, k->kind, names[code]);
     }
-    uint32_t s = slice_blocks ? slice_blocks : slice_of(ctx, p, b, std::max(1, p.m_min));
+    uint32_t s = slice_blocks ? slice_blocks : slice_of(ctx, b, std::max(1, p.m_min));
     out->slice_blocks = s;
     out->n_slices = (k->grid + s - 1) / s;
     out->blocks_per_sm = b;
@@ -764,66 +924,51 @@ kl_status kl_predict(kl_ctx* ctx, const kl_candidate* c, size_t n, kl_prediction
 
 kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out) {
     KL_LIVE(ctx);
-    if (ctx->in_flight) return ctx->fail(KL_EBUSY, "a phase is in flight");
+    if (!ctx->inflight.empty()) return ctx->fail(KL_EBUSY, "launches are in flight");
     Decision d;
-    kl_status st = find_co_schedule(ctx, &d);
+    kl_status st = decide(ctx, &d);
     if (st) return st;
-    if (out) {
-        *out = kl_coschedule{};
-        Inst* k1 = ctx->R[d.ia];
-        Inst* k2 = d.solo ? nullptr : ctx->R[d.ib];
-        out->id1 = k1->id;
-        out->id2 = k2 ? k2->id : 0;
-        out->kind1 = k1->kind;
-        out->kind2 = k2 ? k2->kind : -1;
-        out->b1 = d.b1;
-        out->b2 = d.b2;
-        int m = std::max(1, ctx->prof[k1->kind].m_min);
-        if (k2) m = std::max(m, ctx->prof[k2->kind].m_min);
-        out->size1 = slice_of(ctx, ctx->prof[k1->kind], d.b1, m);
-        out->size2 = k2 ? slice_of(ctx, ctx->prof[k2->kind], d.b2, m) : 0;
-        out->cp = d.cp;
-        out->solo = d.solo;
-        out->n_candidates = d.n_cand;
-    }
+    fill_cs(ctx, d, out);
     return KL_OK;
 }
 
 kl_status kl_schedule(kl_ctx* ctx, kl_coschedule* out) {
     KL_LIVE(ctx);
     if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
-    kl_status st = retire_phase(ctx);
-    if (st) return st;
-    if (ctx->R.empty()) return ctx->fail(KL_ENOTFOUND, "nothing pending");
-    Decision d;
-    st = find_co_schedule(ctx, &d);
-    if (st) return st;
-    return launch_phase(ctx, d, out);
+    return schedule_step(ctx, out);
 }
 
 kl_status kl_sync(kl_ctx* ctx, kl_counters* out) {
     KL_LIVE(ctx);
     if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
     for (;;) {
-        kl_status st = retire_phase(ctx);
-        if (st) return st;
-        if (ctx->R.empty()) break;
-        Decision d;
-        st = find_co_schedule(ctx, &d);
-        if (st) return st;
-        st = launch_phase(ctx, d, nullptr);
+        kl_status st = schedule_step(ctx, nullptr);
+        if (st == KL_ENOTFOUND) break;
         if (st) return st;
     }
-    KL_CUDA(cudaStreamSynchronize(ctx->lane[0].s));
-    KL_CUDA(cudaStreamSynchronize(ctx->lane[1].s));
+    ctx->err.clear();
+    kl_status st = drain_all(ctx);
+    if (st) return st;
+    for (int i = 0; i < kPool; ++i) KL_CUDA(cudaStreamSynchronize(ctx->pool[i]));
+    KL_CUDA(cudaStreamSynchronize(ctx->stopper));
+    ctx->have_desired = false;
     if (out) {
         *out = kl_counters{};
         if (ctx->counters) {
             KL_CUDA(cudaMemcpyAsync(out, ctx->counters, sizeof(kl_counters), cudaMemcpyDeviceToHost, ctx->ctrl));
             KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
         }
-        out->phases = ctx->phases;
+        out->phases = ctx->st.decisions;
     }
+    return KL_OK;
+}
+
+kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out) {
+    KL_LIVE(ctx);
+    if (!out) return KL_EINVAL;
+    *out = ctx->st;
+    out->model_batches = ctx->model_batches;
+    out->model_candidates = ctx->model_cands;
     return KL_OK;
 }
 
@@ -894,7 +1039,7 @@ kl_status kl_audit(kl_ctx* ctx, uint64_t id, uint32_t* host_out, size_t n) {
     const Inst* k = it->second;
     if (!k->audit) return ctx->fail(KL_EINVAL, "audit disabled (config.audit = 0)");
     if (!host_out || n < k->grid) return ctx->fail(KL_EINVAL, "audit buffer too small");
-    for (auto& l : ctx->lane) KL_CUDA(cudaStreamSynchronize(l.s));
+    for (int i = 0; i < kPool; ++i) KL_CUDA(cudaStreamSynchronize(ctx->pool[i]));
     KL_CUDA(cudaMemcpy(host_out, k->audit, sizeof(uint32_t) * k->grid, cudaMemcpyDeviceToHost));
     return KL_OK;
 }
