@@ -140,8 +140,9 @@ class Clocks:
 def build_queue(rank: int, world: int, instances: int) -> list[str]:
     """Global queue of 32*world kernels (instances x ALL per GPU), sharded round robin so every
     GPU keeps the mix."""
+    from paper_1303_5164_b200.dist import shard
     gq = [e["kind"] for e in G.queue("ALL", len(ALL) * instances * world, order="round_robin")]
-    return gq[rank::world]
+    return shard(gq, rank, world)
 
 
 MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min")
@@ -527,7 +528,10 @@ def main():
                 "phases_per_step": res["phases_per_step"], "parity": res["parity"],
                 "schedule_first_step": res["schedule_first_step"]}
         if not args.no_cpu and world == 1:
-            line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances), args.size)
+            try:
+                line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances), args.size)
+            except Exception as e:      # never lose the GPU line to the CPU leg
+                line["cpu_baseline"] = {"error": repr(e)[:300]}
         print(json.dumps(line))
         if args.json_out:
             with open(args.json_out, "w") as f:

@@ -67,7 +67,7 @@ KIND_SEED = {"PC": 10, "SAD": 11, "SPMV": 12, "ST": 13, "MM": 14, "MRIQ": 15, "B
              "MATADD": 18, "SYNTH": 19}
 
 # Thread configuration (threads per block) per kind, P:1139-1146 (MM: our tcgen05 tile CTA).
-THREADS = {"PC": 256, "SAD": 32, "SPMV": 256, "ST": 128, "MM": 192, "MRIQ": 256, "BS": 128,
+THREADS = {"PC": 256, "SAD": 32, "SPMV": 256, "ST": 128, "MM": 256, "MRIQ": 256, "BS": 128,
            "TEA": 128, "MATADD": 256, "SYNTH": 256}
 
 # Per-block work units that fix the grid decomposition (shared layout facts, not arithmetic).

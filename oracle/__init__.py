@@ -349,8 +349,10 @@ def levels(prof: dict, nsched: int = 4, mode: str = "all") -> list[int]:
 
 
 def solo_b(prof: dict, nsched: int = 4) -> int:
-    """Solo maximum occupancy level b_max (the IPC_i of Eq.1 is the solo IPC at b_max)."""
-    return levels(prof, nsched, "all")[-1]
+    """Solo maximum occupancy level b_max (the IPC_i of Eq.1 is the solo IPC at b_max); 0 if no
+    occupancy gives whole warps per virtual SM."""
+    lv = levels(prof, nsched, "all")
+    return lv[-1] if lv else 0
 
 
 def maximal_splits(sm: dict, p1: dict, p2: dict, nsched=4, mode="all") -> list[tuple[int, int]]:

@@ -1,15 +1,16 @@
 // kl_mm.cu -- MM ("Multiplying two dense matrices", 8192x2048 . 2048x2048) on the
 // 5th-generation tensor cores (product path).
 //
-// One virtual thread block = one 128x128 fp32 output tile.  A persistent block (6 warps) pulls
+// One virtual thread block = one 128x128 fp32 output tile.  A persistent block (8 warps) pulls
 // tiles from the slice launcher and runs, per tile,
 //   warp 0 lane 0 : TMA producer  -- 128x64 bf16 tiles of A and B (128B swizzle) into a ring of
 //                   kStages shared-memory stages, completion on mbarriers (expect_tx);
 //   warp 1 lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16 (M=128,N=128,K=16) x4
 //                   per stage into a 128-column fp32 TMEM accumulator; tcgen05.commit frees the
 //                   stage; the last commit signals the epilogue;
-//   warps 2..5    : epilogue      -- tcgen05.ld 32x32b.x32 (each warp its 32 TMEM lanes) and
-//                   128-byte row stores of C.
+//   warps 4..7    : epilogue      -- tcgen05.ld 32x32b.x32 (each warp its 32 TMEM lanes) and
+//                   128-byte row stores of C;  warps 2-3 idle (8 warps keep b*wpb divisible by
+//                   the 4 schedulers, so the virtual-SM warp count is whole, R14).
 // The stage count is the kernel's occupancy knob (shared memory per block).
 // Numerics: bf16 products are exact in fp32; only the fp32 accumulation order differs from the
 // oracle's fp64 sum (normwise tolerance).
@@ -28,7 +29,7 @@ constexpr int kStages = 4;
 constexpr int kStageBytes = (BM + BN) * BK * 2;          // 32 KiB
 constexpr int kBarOffset = kStages * kStageBytes;
 constexpr int kDynSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;   // 8 warps: whole warps per virtual SM (R14)
 constexpr uint32_t kTmemCols = 128;
 // instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 128, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -176,7 +177,7 @@ struct BodyMM {
                 umma_commit(st.bars + 128);                  // accumulator complete
             }
             __syncwarp();
-        } else {
+        } else if (warp >= 4) {
             mbar_wait(st.bars + 128, st.tphase);
             tc_fence_after();
             const int q = warp & 3;                          // TMEM lane quarter of this warp
