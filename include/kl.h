@@ -215,6 +215,10 @@ kl_status kl_sync(kl_ctx* ctx, kl_counters* out);
  * the sequential and multi-stream baselines and the slicing-overhead calibration. */
 kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* desc, void* stream,
                        uint32_t block_offset, uint32_t n_blocks);
+/* One whole kernel through the persistent slice launcher at `cap` resident blocks per SM
+ * (0 = uncapped), outside the scheduler; blocks until done; *ms = device time of the launch.
+ * Occupancy sweeps for the calibration (solo IPC vs warps, the E4 analog). */
+kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* desc, uint32_t cap, double* ms);
 kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out);
 kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p);   /* clears model cache */
 kl_status kl_reset_model_cache(kl_ctx* ctx);

@@ -156,7 +156,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -194,6 +194,7 @@ def lib() -> C.CDLL:
     L.kl_audit.argtypes = [_vp, C.c_uint64, P(C.c_uint32), C.c_size_t]
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
+    L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
     for s in ABI_SYMBOLS:
         if s not in ("kl_abi_version", "kl_last_error", "kl_struct_sizes"):
             getattr(L, s).restype = C.c_int
@@ -329,6 +330,14 @@ class Context:
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         n = grid_blocks - offset if n_blocks is None else n_blocks
         self._check(self._L.kl_run_plain(self._h, C.byref(d), s, offset, n))
+
+    def run_capped(self, kind, grid_blocks: int, args, cap: int) -> float:
+        """Whole kernel through the persistent launcher at `cap` blocks/SM; returns device ms."""
+        kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
+        d = KernelDesc(kid, grid_blocks, C.cast(C.pointer(args), _vp), C.sizeof(args), None, 0, None)
+        ms = C.c_double()
+        self._check(self._L.kl_run_capped(self._h, C.byref(d), cap, C.byref(ms)))
+        return ms.value
 
     def get_profile(self, kind) -> Profile:
         p = Profile()

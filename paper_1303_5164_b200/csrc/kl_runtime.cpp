@@ -985,6 +985,41 @@ kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* d, void* stream, uint3
     return KL_OK;
 }
 
+kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, double* ms) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    if (!ctx->inflight.empty() || !ctx->R.empty()) return ctx->fail(KL_EBUSY, "scheduler has pending work");
+    uint64_t id = 0;
+    kl_status st = kl_submit(ctx, d, &id);
+    if (st) return st;
+    Inst* k = ctx->by_id[id];
+    ctx->R.clear();                       // not scheduled: launched directly below
+    st = flush_ctl_init(ctx);
+    if (st) return st;
+    cudaEvent_t e0, e1;
+    KL_CUDA(cudaEventCreate(&e0));
+    KL_CUDA(cudaEventCreate(&e1));
+    int si = pick_stream(ctx);
+    KL_CUDA(cudaEventRecord(e0, ctx->pool[si]));
+    ctx->pool_busy[si] += 1000;            // keep launch_kernel on the same stream
+    st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0);
+    ctx->pool_busy[si] -= 1000;
+    if (st) return st;
+    KL_CUDA(cudaEventRecord(e1, ctx->pool[k->inflight->stream]));
+    KL_CUDA(cudaEventSynchronize(e1));
+    bool rp = false, pg = false;
+    while (k->inflight) {
+        st = poll(ctx, &rp, &pg);
+        if (st) return st;
+    }
+    float f = 0.f;
+    KL_CUDA(cudaEventElapsedTime(&f, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms) *ms = f;
+    return KL_OK;
+}
+
 kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out) {
     KL_LIVE(ctx);
     if (kind < 0 || kind >= KL_NKINDS || !out) return KL_EINVAL;
