@@ -145,7 +145,7 @@ def build_queue(rank: int, world: int, instances: int) -> list[str]:
     return shard(gq, rank, world)
 
 
-MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min")
+MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")
 
 
 def load_profiles(path: str):

@@ -123,12 +123,16 @@ typedef struct {
     int32_t tmem;          /* TMEM columns per block */
     int32_t bmax;          /* solo max resident blocks per SM */
     int32_t m_min;         /* p% rule: minimum slice in waves of b*n_sm blocks */
+    double ipc_max;        /* pipe ceiling per virtual SM (R26; 0 = 1, the paper's model) */
+    int32_t pipe;          /* id of the pipe that ceiling belongs to (0 none, 1 MUFU, 2 ALU, 3 FMA) */
+    int32_t pad;
 } kl_profile;
 
 typedef struct {
     double alpha_p, alpha_m;   /* pruning thresholds (defaults 0.4 / 0.1) */
     double p_percent;          /* slicing overhead limit, default 2 */
     double L0, B, a0, b0;      /* latency L(n) = L0 + a0*n/B + b0 (reading R2 of P:875) */
+    double cp_min;             /* co-run only if the best predicted CP exceeds this (R25; 0 = paper) */
     int32_t n_sched;           /* warp schedulers per SM -> virtual SM; 4 on B200 */
     int32_t latency_mode;      /* 0 linear-in-requests (R2), 1 verbatim P:875 */
     int32_t level_mode;        /* 0: every b with b*wpb % n_sched == 0; 1: four levels (config C2) */
@@ -200,7 +204,8 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* desc, uint64_t* out_id);
  * blocks_per_sm resident blocks per SM; slice_blocks = 0 applies the p% rule (m_min waves). */
 kl_status kl_slice(kl_ctx* ctx, uint64_t id, uint32_t blocks_per_sm, uint32_t slice_blocks,
                    kl_slice_plan* out);
-/* Batched model on the device: one prediction per candidate. */
+/* Batched model on the device: one prediction per candidate.  b2 = 0 asks for the
+ * solo prediction of k1 at b1 (ipc1; cp = dT = 0). */
 kl_status kl_predict(kl_ctx* ctx, const kl_candidate* cands, size_t n, kl_prediction* out);
 /* One step of Alg.1: wait for the next scheduling event (a kernel ran out of thread blocks, or
  * the first call), run FindCoSchedule over the pending set and reconcile the running

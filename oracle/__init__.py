@@ -54,7 +54,8 @@ class SmCfg(C.Structure):
 
 
 class KModel(C.Structure):
-    _fields_ = [("rm", C.c_double), ("r", C.c_double), ("ipb", C.c_double), ("wpb", C.c_int)]
+    _fields_ = [("rm", C.c_double), ("r", C.c_double), ("ipb", C.c_double), ("wpb", C.c_int),
+                ("pi", C.c_double), ("pipe", C.c_int)]
 
 
 class Pred(C.Structure):
@@ -86,6 +87,8 @@ def _declare(L):
     L.or_stationary.argtypes = [C.c_int, _D, _D]
     L.or_ipc_homog.restype = C.c_double
     L.or_ipc_homog.argtypes = [C.c_int, _D]
+    L.or_ipc_homog_r.restype = C.c_double
+    L.or_ipc_homog_r.argtypes = [C.c_int, _D, _D]
     L.or_ipc_joint.argtypes = [C.c_int, C.c_int, _D, _D, _D, _D, _D]
     L.or_cp.restype = C.c_double
     L.or_cp.argtypes = [C.c_int, _D, _D]
@@ -222,8 +225,8 @@ def smcfg(L0=800.0, B=1.0, a0=0.0, b0=0.0, W=16, latency_mode=0, pir_mode=0, con
     return SmCfg(L0, B, a0, b0, W, latency_mode, pir_mode, const_q)
 
 
-def kmodel(rm, r=1.0, ipb=1000.0, wpb=4):
-    return KModel(rm, r, ipb, wpb)
+def kmodel(rm, r=1.0, ipb=1000.0, wpb=4, pi=1.0, pipe=0):
+    return KModel(rm, r, ipb, wpb, pi, pipe)
 
 
 def latency(cfg, n, idle=0):
@@ -263,8 +266,10 @@ def stationary(P):
     return pi
 
 
-def ipc_homog(w, pi):
-    return lib().or_ipc_homog(w, _dptr(np.ascontiguousarray(pi)))
+def ipc_homog(w, pi, R=None):
+    if R is None:
+        return lib().or_ipc_homog(w, _dptr(np.ascontiguousarray(pi)))
+    return lib().or_ipc_homog_r(w, _dptr(np.ascontiguousarray(pi)), _dptr(np.ascontiguousarray(R)))
 
 
 def ipc_joint(w1, w2, pi, R):
@@ -369,7 +374,8 @@ def maximal_splits(sm: dict, p1: dict, p2: dict, nsched=4, mode="all") -> list[t
 
 
 def kmodel_of(prof: dict) -> KModel:
-    return KModel(prof["rm"], prof["r"], prof["ipb"], prof["wpb"])
+    return KModel(prof["rm"], prof["r"], prof["ipb"], prof["wpb"], prof.get("ipc_max", 1.0) or 1.0,
+                  int(prof.get("pipe", 0)))
 
 
 def pairs_of(pending: list[dict]) -> list[tuple[int, int]]:
@@ -427,7 +433,7 @@ def _better_split(a, b):
 
 
 def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, nsched=4,
-                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None) -> dict:
+                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0) -> dict:
     """Proc. FindCoSchedule: candidates -> prune -> model CP -> argmax.
 
     Per surviving pair the slice ratio is the argmin of dT (Eq.8) over maximal splits; across
@@ -462,7 +468,7 @@ def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, n
             continue
         if best is None or bestsplit["cp"] > best["cp"] + _band(bestsplit["cp"], best["cp"]):
             best = bestsplit
-    if best is None or best["cp"] <= BAND:
+    if best is None or best["cp"] <= max(BAND, cp_min):
         k = pending[0]
         pr = profs[k["kind"]]
         b = solo_b(pr, nsched)

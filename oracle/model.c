@@ -44,14 +44,35 @@ void or_row(int w, int i, double p_ir, double rm, double* row) {
     }
 }
 
-/* P_{i->r} in a state with `ready` ready warps, `idle` idle warps and n outstanding requests:
- * the literal (W-I)/L with the round duration max(W-I, 1) of P:910-914 (R1),
- * clamped to 1 when the round outlasts the latency. */
-static int p_idle_to_ready(const or_smcfg* c, int ready, int idle, double n, double* out) {
+/* Pipe ceiling of a kernel (R26); 0 means 1 (the paper's issue-only model). */
+static double pipe_of(const or_kmodel* k) { return (k->pi > 0.0 && k->pi < 1.0) ? k->pi : 1.0; }
+
+/* Round duration: every ready warp issues one instruction, so a round
+ * lasts #ready cycles, or 1 if none is ready (R1).  B200 adaptation R26: a kernel whose busiest
+ * pipe sustains only pi instructions per cycle needs ready/pi cycles of that pipe; kernels on the
+ * same pipe share it (their pipe times add), kernels on different pipes overlap.  The round lasts
+ * until the slowest of (issue of all ready warps, every pipe) is done; pi = 1 for every kernel
+ * gives back the paper's max(#ready, 1) exactly. */
+static double round_of(int ready1, const or_kmodel* k1, int ready2, const or_kmodel* k2) {
+    const double p1 = k1 ? pipe_of(k1) : 1.0, p2 = k2 ? pipe_of(k2) : 1.0;
+    double R = (double)(ready1 + ready2);
+    if (k1 && k2 && k1->pipe != 0 && k1->pipe == k2->pipe) {
+        double t = ready1 / p1 + ready2 / p2;
+        if (t > R) R = t;
+    } else {
+        if (ready1 / p1 > R) R = ready1 / p1;
+        if (ready2 / p2 > R) R = ready2 / p2;
+    }
+    return R > 1.0 ? R : 1.0;
+}
+
+/* P_{i->r} in a state with round duration R, `idle` idle warps and n outstanding requests: the
+ * literal (W-I)/L with (W-I) the round duration (R1), clamped to 1 when the round
+ * outlasts the latency. */
+static int p_idle_to_ready(const or_smcfg* c, double R, int idle, double n, double* out) {
     if (c->pir_mode == 1) { *out = c->const_q; return 0; }
     double L = or_latency(c, n, idle);
     if (!(L > (double)c->W)) return -1;            /* guard R22: reducible chain otherwise */
-    double R = (double)(ready > 1 ? ready : 1);
     double p = R / L;
     *out = p < 1.0 ? p : 1.0;
     return 0;
@@ -61,8 +82,8 @@ int or_build_homog(const or_kmodel* k, int w, const or_smcfg* c, double* P, doub
     for (int i = 0; i <= w; ++i) {
         int ready = w - i;
         double p_ir;
-        if (p_idle_to_ready(c, ready, i, (double)i * k->r, &p_ir)) return -1;
-        R[i] = (double)(ready > 1 ? ready : 1);      /* round duration */
+        R[i] = round_of(ready, k, 0, 0);               /* round duration, P:910-914 (+R26) */
+        if (p_idle_to_ready(c, R[i], i, (double)i * k->r, &p_ir)) return -1;
         or_row(w, i, p_ir, k->rm, &P[(size_t)i * (w + 1)]);
     }
     return 0;
@@ -80,13 +101,12 @@ int or_build_joint(const or_kmodel* k1, int w1, const or_kmodel* k2, int w2,
     for (int p = 0; p <= w1; ++p)
         for (int q = 0; q <= w2; ++q) {
             int s = p * (w2 + 1) + q;
-            int ready = (w1 - p) + (w2 - q);
             double p_ir;
-            if (p_idle_to_ready(c, ready, p + q, (double)p * k1->r + (double)q * k2->r, &p_ir)) {
+            R[s] = round_of(w1 - p, k1, w2 - q, k2);
+            if (p_idle_to_ready(c, R[s], p + q, (double)p * k1->r + (double)q * k2->r, &p_ir)) {
                 free(r1); free(r2);
                 return -1;
             }
-            R[s] = (double)(ready > 1 ? ready : 1);
             or_row(w1, p, p_ir, k1->rm, r1);
             or_row(w2, q, p_ir, k2->rm, r2);
             for (int pp = 0; pp <= w1; ++pp)
@@ -140,7 +160,18 @@ int or_stationary(int S, const double* P, double* pi) {
     return rc;
 }
 
-/* Eq.4: IPC = sum_{i<W} g_i (W-i) / (sum_{i<W} g_i (W-i) + g_W). */
+/* Eq.4: IPC = sum_{i<W} g_i (W-i) / (sum_{i<W} g_i (W-i) + g_W), i.e. issued
+ * instructions over elapsed cycles; with the round durations R_i of the chain (R26) the
+ * denominator is sum_i g_i R_i (identical to Eq.4 when every R_i = max(W-i, 1)). */
+double or_ipc_homog_r(int w, const double* pi, const double* R) {
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i <= w; ++i) {
+        if (i < w) num += pi[i] * (double)(w - i);
+        den += pi[i] * R[i];
+    }
+    return num / den;
+}
+
 double or_ipc_homog(int w, const double* pi) {
     double num = 0.0;
     for (int i = 0; i < w; ++i) num += pi[i] * (double)(w - i);
@@ -187,7 +218,7 @@ double or_solo_ipc(const or_kmodel* k, int b, int nsched, const or_smcfg* c, int
     double* pi = (double*)malloc(sizeof(double) * S);
     double ipc = 0.0;
     if (or_build_homog(k, w, c, P, R) || or_stationary(S, P, pi)) *status = 6;
-    else ipc = or_ipc_homog(w, pi);
+    else ipc = or_ipc_homog_r(w, pi, R);
     free(P); free(R); free(pi);
     return ipc;
 }

@@ -60,6 +60,9 @@ typedef struct {        /* per-kernel model descriptor (tb:para; A24 P:1055-1060
     double r;           /* memory requests per memory instruction (outstanding-request weight) */
     double ipb;         /* warp instructions per thread block, I_K (Eq.8) */
     int wpb;            /* warps per block */
+    double pi;          /* pipe ceiling (R26): instructions/cycle the kernel's busiest pipe allows;
+                           1 (or 0) = issue-limited only, the paper's model */
+    int pipe;           /* id of that pipe (0 = none); kernels with the same id share it */
 } or_kmodel;
 
 double or_latency(const or_smcfg* c, double n_outstanding, int idle_warps);
@@ -77,6 +80,7 @@ int or_build_joint(const or_kmodel* k1, int w1, const or_kmodel* k2, int w2,
  * partial pivoting (Eq.3).  Returns 0, or -1 if singular. */
 int or_stationary(int S, const double* P, double* pi);
 double or_ipc_homog(int w, const double* pi);                                   /* Eq.4 */
+double or_ipc_homog_r(int w, const double* pi, const double* R);                  /* Eq.4, R26 */
 void or_ipc_joint(int w1, int w2, const double* pi, const double* R,
                   double* ipc1, double* ipc2, double* c);                         /* Eq.5-7 */
 double or_cp(int n, const double* cipc, const double* ipc);                       /* Eq.1 */

@@ -95,13 +95,14 @@ ARGS = [ArgsPC, ArgsSAD, ArgsSPMV, ArgsST, ArgsMM, ArgsMRIQ, ArgsBS, ArgsTEA, Ar
 class Profile(C.Structure):
     _fields_ = [("rm", C.c_double), ("r", C.c_double), ("ipb", C.c_double), ("pur", C.c_double),
                 ("mur", C.c_double), ("wpb", C.c_int32), ("regs", C.c_int32), ("smem", C.c_int32),
-                ("tmem", C.c_int32), ("bmax", C.c_int32), ("m_min", C.c_int32)]
+                ("tmem", C.c_int32), ("bmax", C.c_int32), ("m_min", C.c_int32), ("ipc_max", C.c_double),
+                ("pipe", C.c_int32), ("pad", C.c_int32)]
 
 
 class Config(C.Structure):
     _fields_ = [("alpha_p", C.c_double), ("alpha_m", C.c_double), ("p_percent", C.c_double),
                 ("L0", C.c_double), ("B", C.c_double), ("a0", C.c_double), ("b0", C.c_double),
-                ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
+                ("cp_min", C.c_double), ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
                 ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),

@@ -95,8 +95,8 @@ int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n_
 
 // ---- model kernels (kl_model.cu) ---------------------------------------------------------
 struct KlModelKind {       // per-kind model inputs, device table
-    double rm, r, ipb;
-    int32_t wpb, bsolo, pad0, pad1;
+    double rm, r, ipb, pi;    // pi: pipe ceiling (R26), 1 = none
+    int32_t wpb, bsolo, pipe, pad1;
 };
 struct KlModelCfg {
     double L0, B, a0, b0;

@@ -31,11 +31,26 @@ __device__ double latency(const KlModelCfg& c, double n, int idle) {
     return c.L0 + c.a0 * n / c.B + c.b0;
 }
 
-// P_ir in a state (R1); returns false if the guard L > W fails (R22).
-__device__ bool p_ir(const KlModelCfg& c, int ready, int idle, double n, double* out) {
+// Round duration (R1) with the B200 pipe ceilings (R26): issue of all
+// ready warps, each kernel's pipe time (ready / pi), pipes shared between kernels on the same
+// pipe id; at least one cycle.
+__device__ double round_dur(int r1, const KlModelKind* k1, int r2, const KlModelKind* k2) {
+    double R = (double)(r1 + r2);
+    const double p1 = k1 ? k1->pi : 1.0, p2 = k2 ? k2->pi : 1.0;
+    if (k1 && k2 && k1->pipe != 0 && k1->pipe == k2->pipe) {
+        R = fmax(R, r1 / p1 + r2 / p2);
+    } else {
+        R = fmax(R, r1 / p1);
+        R = fmax(R, r2 / p2);
+    }
+    return fmax(R, 1.0);
+}
+
+// P_ir in a state of round duration R (R1); returns false if the guard L > W fails (R22).
+__device__ bool p_ir(const KlModelCfg& c, double R, int idle, double n, double* out) {
     double L = latency(c, n, idle);
     if (!(L > (double)c.W)) return false;
-    double p = (double)(ready > 1 ? ready : 1) / L;
+    double p = R / L;
     *out = p < 1.0 ? p : 1.0;
     return true;
 }
@@ -103,25 +118,33 @@ __device__ bool gth(double* P, int S, double* pi, double* red, int* flag) {
     return true;
 }
 
-// Solo IPC (Eq.4) of a kind at w warps on the virtual SM.
+// Solo IPC (Eq.4, denominator = elapsed cycles sum_i g_i R_i) of a kind at w warps on the
+// virtual SM.
 __device__ bool solo_ipc(const KlModelKind& k, int w, const KlModelCfg& c, double* P, double* pi,
                          double* red, double* out) {
     const int S = w + 1;
     __shared__ int s_ok;
+    __shared__ double s_R[kMaxW + 1];
     if (threadIdx.x == 0) s_ok = 1;
     __syncthreads();
     for (int i = threadIdx.x; i < S; i += kThreads) {
         double pr;
-        if (!p_ir(c, w - i, i, (double)i * k.r, &pr)) { s_ok = 0; continue; }
+        const double R = round_dur(w - i, &k, 0, nullptr);
+        s_R[i] = R;
+        if (!p_ir(c, R, i, (double)i * k.r, &pr)) { s_ok = 0; continue; }
         row_of(w, i, pr, k.rm, P + i * S);
     }
     __syncthreads();
     if (!s_ok) return false;
     if (!gth(P, S, pi, red, nullptr)) return false;
-    double num = 0.0;
-    for (int i = threadIdx.x; i < w; i += kThreads) num += pi[i] * (double)(w - i);
+    double num = 0.0, den = 0.0;
+    for (int i = threadIdx.x; i < S; i += kThreads) {
+        if (i < w) num += pi[i] * (double)(w - i);
+        den += pi[i] * s_R[i];
+    }
     num = block_sum(num, red);
-    *out = num / (num + pi[w]);
+    den = block_sum(den, red);
+    *out = num / den;
     __syncthreads();
     return true;
 }
@@ -164,8 +187,9 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     if (t1 % cfg.n_sched || t2 % cfg.n_sched || ts1 % cfg.n_sched || ts2 % cfg.n_sched) status = KL_EINFEASIBLE;
     const int w1 = t1 / cfg.n_sched, w2 = t2 / cfg.n_sched;
     const int ws1 = ts1 / cfg.n_sched, ws2 = ts2 / cfg.n_sched;
-    if (w1 < 1 || w2 < 1 || w1 + w2 > cfg.W || ws1 < 1 || ws1 > cfg.W || ws2 < 1 || ws2 > cfg.W ||
-        (w1 + 1) * (w2 + 1) > kMaxS || cfg.W > kMaxW)
+    const bool solo_query = (cd.b2 == 0);   // prediction of k1 alone at b1 (calibration)
+    if (w1 < 1 || (w2 < 1 && !solo_query) || w1 + w2 > cfg.W || ws1 < 1 || ws1 > cfg.W || ws2 < 1 ||
+        ws2 > cfg.W || (w1 + 1) * (w2 + 1) > kMaxS || cfg.W > kMaxW)
         status = KL_EINFEASIBLE;
     if (status == 0) {
         if (!solo_ipc(k1, ws1, cfg, P, pi, red, &out.solo1) || !solo_ipc(k2, ws2, cfg, P, pi, red, &out.solo2))
@@ -179,10 +203,9 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
         // evaluated with the shared round duration and latency of state (p,q)
         for (int s = threadIdx.x; s < S; s += kThreads) {
             const int p = s / (w2 + 1), q = s - p * (w2 + 1);
-            const int ready = (w1 - p) + (w2 - q);
             double pr, r1[kMaxW + 1], r2[kMaxW + 1];
-            R[s] = (double)(ready > 1 ? ready : 1);
-            if (!p_ir(cfg, ready, p + q, (double)p * k1.r + (double)q * k2.r, &pr)) { s_ok = 0; continue; }
+            R[s] = round_dur(w1 - p, &k1, w2 - q, solo_query ? nullptr : &k2);
+            if (!p_ir(cfg, R[s], p + q, (double)p * k1.r + (double)q * k2.r, &pr)) { s_ok = 0; continue; }
             row_of(w1, p, pr, k1.rm, r1);
             row_of(w2, q, pr, k2.rm, r2);
             for (int pp = 0; pp <= w1; ++pp)
@@ -206,8 +229,10 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
             out.ipc1 = n1 / den;
             out.ipc2 = n2 / den;
             out.c = out.ipc1 + out.ipc2;
-            out.cp = 1.0 - 1.0 / (out.ipc1 / out.solo1 + out.ipc2 / out.solo2);   // Eq.1
-            out.dT = fabs(k1.ipb * (double)cd.b1 / out.ipc1 - k2.ipb * (double)cd.b2 / out.ipc2);  // Eq.8
+            if (!solo_query) {
+                out.cp = 1.0 - 1.0 / (out.ipc1 / out.solo1 + out.ipc2 / out.solo2);   // Eq.1
+                out.dT = fabs(k1.ipb * (double)cd.b1 / out.ipc1 - k2.ipb * (double)cd.b2 / out.ipc2);  // Eq.8
+            }
         }
     }
     out.status = status;
@@ -243,7 +268,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
             double cp = preds[i].cp;
             if (best < 0 || cp > bcp + band(cp, bcp)) { best = i; bcp = cp; }
         }
-        if (best >= 0 && !(bcp > 1e-12)) best = -1;   // R25: no profitable pair -> solo
+        // (R25 "no profitable pair -> solo" is applied by the host with the configured cp_min)
         dec->cand = best;
         dec->cp = best >= 0 ? bcp : 0.0;
         dec->n_pairs = n_pairs;

@@ -41,16 +41,16 @@ constexpr int kMaxCand = 8192;
 // profiles/kl_profile_b200.json, passed through kl_config.profiles).  PUR/MUR default to the
 // paper's C2050 values (tb:benchmarks).
 const kl_profile kDefaultProfiles[KL_NKINDS] = {
-    /* PC   */ {0.25, 32.0, 720.0, 0.0096, 0.1404, 0, 0, 0, 0, 0, 1},
-    /* SAD  */ {0.03, 4.0, 3600.0, 0.1498, 0.1120, 0, 0, 0, 0, 0, 1},
-    /* SPMV */ {0.30, 8.0, 200.0, 0.3464, 0.003, 0, 0, 0, 0, 0, 1},
-    /* ST   */ {0.15, 4.0, 3072.0, 0.3629, 0.1156, 0, 0, 0, 0, 0, 1},
-    /* MM   */ {0.01, 1.0, 12000.0, 0.5804, 0.0161, 0, 0, 0, 0, 0, 1},
-    /* MRIQ */ {0.001, 1.0, 196608.0, 0.8539, 0.0002, 0, 0, 0, 0, 0, 1},
-    /* BS   */ {0.03, 16.0, 4800.0, 0.8642, 0.0604, 0, 0, 0, 0, 0, 1},
-    /* TEA  */ {0.01, 16.0, 15360.0, 0.9978, 0.0196, 0, 0, 0, 0, 0, 1},
-    /* MATADD*/ {0.30, 4.0, 80.0, 0.1, 0.1, 0, 0, 0, 0, 0, 1},
-    /* SYNTH*/ {0.10, 16.0, 320.0, 0.5, 0.5, 0, 0, 0, 0, 0, 1},
+    /* PC   */ {0.25, 32.0, 720.0, 0.0096, 0.1404, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* SAD  */ {0.03, 4.0, 3600.0, 0.1498, 0.1120, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* SPMV */ {0.30, 8.0, 200.0, 0.3464, 0.003, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* ST   */ {0.15, 4.0, 3072.0, 0.3629, 0.1156, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* MM   */ {0.01, 1.0, 12000.0, 0.5804, 0.0161, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* MRIQ */ {0.001, 1.0, 196608.0, 0.8539, 0.0002, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* BS   */ {0.03, 16.0, 4800.0, 0.8642, 0.0604, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* TEA  */ {0.01, 16.0, 15360.0, 0.9978, 0.0196, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* MATADD*/ {0.30, 4.0, 80.0, 0.1, 0.1, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
+    /* SYNTH*/ {0.10, 16.0, 320.0, 0.5, 0.5, 0, 0, 0, 0, 0, 1, 1.0, 0, 0},
 };
 
 constexpr int kRecRing = 1024;
@@ -260,6 +260,8 @@ void fill_model_kinds(kl_ctx* c) {
         m.ipb = p.ipb;
         m.wpb = p.wpb;
         m.bsolo = (int)solo_level(c, p);
+        m.pi = (p.ipc_max > 0.0 && p.ipc_max < 1.0) ? p.ipc_max : 1.0;
+        m.pipe = p.pipe;
         c->mk_pinned[k] = m;
     }
 }
@@ -365,11 +367,38 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     double bcp = 0.0;
     if (n > 0 && missing) {
         if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context cannot run the model");
+        // one batch also covers every other pair of the pending kinds (unpruned, pair = -1), so
+        // the later decisions of this queue are cache hits instead of mid-queue model batches
+        int ne = n;
+        bool have[KL_NKINDS] = {};
+        for (auto* k : R) have[k->kind] = true;
+        for (int a = 0; a < KL_NKINDS; ++a)
+            for (int b = a; b < KL_NKINDS; ++b) {
+                if (!have[a] || !have[b]) continue;
+                for (auto& sp : maximal_splits(ctx, ctx->prof[a], ctx->prof[b])) {
+                    if (ctx->cache.count(cache_key(a, b, sp.first, sp.second))) continue;
+                    bool in_list = false;
+                    for (int i = 0; i < n && !in_list; ++i) {
+                        const KlCand& c = ctx->cand_pinned[i];
+                        in_list = c.k1 == a && c.k2 == b && c.b1 == sp.first && c.b2 == sp.second;
+                    }
+                    if (in_list || ne >= kMaxCand) continue;
+                    KlCand cd{};
+                    cd.k1 = a;
+                    cd.k2 = b;
+                    cd.b1 = sp.first;
+                    cd.b2 = sp.second;
+                    cd.pair = -1;
+                    cd.warps = (int)sp.first * ctx->prof[a].wpb + (int)sp.second * ctx->prof[b].wpb;
+                    ctx->cand_pinned[ne++] = cd;
+                }
+            }
         KlDecision dec{};
-        kl_status st = run_model(ctx, n, np, &dec);
+        kl_status st = run_model(ctx, ne, np, &dec);
         if (st) return st;
         best = dec.cand;
         bcp = dec.cp;
+        if (best >= 0 && !(bcp > std::max(1e-12, ctx->cfg.cp_min))) best = -1;
     } else if (n > 0) {
         // host selection with the same rules as the fused device selection
         for (int p = 0; p < np; ++p) {
@@ -384,7 +413,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             if (bi < 0) continue;
             if (best < 0 || bp.cp > bcp + band(bp.cp, bcp)) { best = bi; bcp = bp.cp; }
         }
-        if (best >= 0 && !(bcp > 1e-12)) best = -1;
+        if (best >= 0 && !(bcp > std::max(1e-12, ctx->cfg.cp_min))) best = -1;
     }
     if (best < 0) {   // solo: oldest pending kernel at its solo maximum occupancy (R25)
         d->solo = true;
@@ -1039,6 +1068,7 @@ kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p) {
     if (!q.tmem) q.tmem = cur.tmem;
     if (!q.bmax) q.bmax = cur.bmax;
     if (!q.m_min) q.m_min = cur.m_min;
+    if (!(q.ipc_max > 0.0)) q.ipc_max = cur.ipc_max > 0.0 ? cur.ipc_max : 1.0;
     ctx->prof[kind] = q;
     ctx->cache.clear();
     return KL_OK;

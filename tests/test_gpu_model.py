@@ -19,7 +19,8 @@ def _rand_profiles(rng):
         profs[k] = dict(rm=float(rng.uniform(0.001, 0.6)), r=float(rng.uniform(1, 32)),
                         ipb=float(rng.uniform(100, 50000)), pur=float(rng.uniform(0, 1)),
                         mur=float(rng.uniform(0, 0.3)), wpb=wpb, regs=int(rng.choice([16, 32, 48, 64])),
-                        smem=int(rng.choice([0, 2048, 16384])), tmem=0, bmax=bmax, m_min=1)
+                        smem=int(rng.choice([0, 2048, 16384])), tmem=0, bmax=bmax, m_min=1,
+                        ipc_max=float(rng.choice([1.0, rng.uniform(0.2, 1.0)])), pipe=int(rng.integers(0, 3)))
     return profs
 
 
@@ -70,12 +71,29 @@ def _decide_both(ctx):
     return d1, d2
 
 
+def test_solo_queries_match_oracle():
+    """b2 = 0 asks the device model for k1 alone at b1 (used by the calibration fit)."""
+    rng = np.random.default_rng(11)
+    profs = _rand_profiles(rng)
+    ctx = _ctx(profs)
+    cfg = O.smcfg(W=16, **CFG)
+    cands = [(k, k, b, 0) for k in K.KINDS for b in O.levels(profs[k])]
+    for (k, _, b, _), g in zip(cands, ctx.predict(cands)):
+        ref, st = O.solo_ipc(O.kmodel_of(profs[k]), b, 4, cfg)
+        assert g.status == st
+        if st == 0:
+            assert abs(g.ipc1 - ref) < 1e-9, (k, b, g.ipc1, ref)
+    ctx.close()
+
+
 def test_decisions_match_oracle():
     rng = np.random.default_rng(7)
     n_cmp = 0
     for rep in range(12):
         profs = _rand_profiles(rng)
-        ctx = _ctx(profs, alpha_p=float(rng.choice([0.0, 0.2, 0.4])), alpha_m=float(rng.choice([0.0, 0.05, 0.1])))
+        cp_min = float(rng.choice([0.0, 0.02]))
+        ctx = _ctx(profs, alpha_p=float(rng.choice([0.0, 0.2, 0.4])), alpha_m=float(rng.choice([0.0, 0.05, 0.1])),
+                   cp_min=cp_min)
         n = int(rng.integers(1, 9))
         kinds = [str(k) for k in rng.choice([k for k in K.KINDS if k != "MM"], n)]
         pend = []
@@ -84,7 +102,7 @@ def test_decisions_match_oracle():
             pend.append({"kind": k, "blocks": 1000, "id": kid})
         d1, d2 = _decide_both(ctx)
         ref = O.find_co_schedule(pend, profs, O.smcfg(W=16, **CFG), ap=ctx.config.alpha_p,
-                                 am=ctx.config.alpha_m)
+                                 am=ctx.config.alpha_m, cp_min=cp_min)
         for d in (d1, d2):
             assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref["solo"])
             assert d.id1 == pend[ref["ia"]]["id"]

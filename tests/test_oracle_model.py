@@ -161,7 +161,7 @@ def test_cp_unit_checks():
     assert O.cp([1.0], [1.0]) == 0.0
 
 
-def _simulate(ws, rms, rs, cfg, rounds, seed):
+def _simulate(ws, rms, rs, cfg, rounds, seed, pis=None):
     """Per-warp Monte Carlo of the round process: each ready warp issues one
     instruction and then stalls with probability Rm; each idle warp returns with probability
     P_ir = min(1, R/L) evaluated in the current state; time advances by the round duration
@@ -177,6 +177,8 @@ def _simulate(ws, rms, rs, cfg, rounds, seed):
             nidle = [int(x.sum()) for x in idle]
             ready = sum(w - n for w, n in zip(ws, nidle))
             R = max(ready, 1)
+            if pis:   # one pipe shared by all simulated kernels (R26)
+                R = max(R, sum((w - n) / p for w, n, p in zip(ws, nidle, pis)))
             n_out = sum(n * r for n, r in zip(nidle, rs))
             L = O.latency(cfg, n_out, sum(nidle))
             pir = min(1.0, R / L)
@@ -249,6 +251,43 @@ def test_predict_consistency():
     assert abs(r.cp - O.cp([r.ipc1, r.ipc2], [s1, s2])) < 1e-15
     assert abs(r.dT - abs(5000 * 4 / r.ipc1 - 20000 * 8 / r.ipc2)) < 1e-9 * r.dT
     assert O.predict(k1, 8, 8, k2, 8, 16, 4, cfg).status == 2      # 16 + 8 warps > W_v
+
+
+@pytest.mark.parametrize("W", [1, 3, 8, 16])
+@pytest.mark.parametrize("pi", [1.0, 0.68, 0.3])
+def test_pipe_ceiling_rm_zero(W, pi):
+    """R26: with no memory stalls every round issues W instructions in W/pi cycles: IPC = pi."""
+    P, R = O.build_homog(O.kmodel(0.0, pi=pi, pipe=1), W, O.smcfg(L0=300.0, W=16))
+    assert abs(O.ipc_homog(W, O.stationary(P), R) - pi) < 1e-12
+
+
+@pytest.mark.parametrize("rm,L,pi", [(0.5, 10.0, 0.5), (1.0, 9.0, 0.25), (0.05, 200.0, 0.7)])
+def test_pipe_ceiling_w1_closed_form(rm, L, pi):
+    """R26 with W=1, constant L: the two-state balance g1 = g0 Rm L is unchanged and the ready
+    round lasts 1/pi cycles, so IPC = 1/(1/pi + Rm L) = pi/(1 + pi Rm L)."""
+    P, R = O.build_homog(O.kmodel(rm, pi=pi, pipe=2), 1, O.smcfg(L0=L, a0=0.0, W=1))
+    assert abs(O.ipc_homog(1, O.stationary(P), R) - pi / (1 + pi * rm * L)) < 1e-12
+
+
+@pytest.mark.parametrize("W", [4, 8, 12])
+def test_pipe_ceiling_lumpability(W):
+    """Identical kernels share their pipe: the split joint chain lumps to the homogeneous one."""
+    k = O.kmodel(0.1, r=4.0, pi=0.6, pipe=1)
+    cfg = O.smcfg(L0=200.0, B=2.0, a0=1.5, W=16)
+    Ph, Rh = O.build_homog(k, W, cfg)
+    ipc_h = O.ipc_homog(W, O.stationary(Ph), Rh)
+    for w1 in range(1, W):
+        P, R = O.build_joint(k, w1, k, W - w1, cfg)
+        assert abs(O.ipc_joint(w1, W - w1, O.stationary(P), R)[2] - ipc_h) < 1e-12
+
+
+def test_pipe_ceiling_monte_carlo():
+    """Round process with pipe-bound rounds (R = max(#ready/pi, 1)) simulated per warp."""
+    cfg = O.smcfg(L0=60.0, a0=0.0, W=8)
+    P, R = O.build_homog(O.kmodel(0.2, pi=0.5, pipe=1), 8, cfg)
+    model = O.ipc_homog(8, O.stationary(P), R)
+    mc, sig = _simulate([8], [0.2], [1.0], cfg, 100000, seed=3, pis=[0.5])
+    assert abs(mc - model) <= 3.5 * sig + 1e-4, (mc, model, sig)
 
 
 def test_reducible_chain_rejected():

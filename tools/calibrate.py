@@ -15,6 +15,15 @@ Per kind (solo, plain launch at max occupancy, paper size):
   IPC = smsp__inst_executed.avg.per_cycle_active                      (virtual-SM IPC)
 The latency constants: L0 from a dependent-load chain (one PC block, many hops, HBM-resident
 array), B = measured HBM bandwidth in 32-B sectors per cycle per virtual SM at the loaded clock.
+
+Effective parameters (readings R20/R26): each kind runs alone through the slice
+launcher at every occupancy level (kl_run_capped); its measured IPC per virtual SM at each level
+is fitted by the device model (kl_predict solo queries):
+  ipc_max = pipe ceiling = the plateau of the measured curve (pipe-bound kinds), pipe = its id;
+  rm      = stall-causing memory instructions per instruction (profiled Rm / memory-level
+            parallelism: a warp stalls once per batch of independent loads);
+  r       = requests per stall (bandwidth contention in L(n)).
+The profiled Rm, r are kept as rm_profiled, r_profiled.
 """
 from __future__ import annotations
 
@@ -30,6 +39,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 KINDS = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA", "SYNTH"]
+# busiest pipe per kind (ncu: MRIQ XU 93 %; TEA / SAD integer ALU; BS MUFU-heavy), 0 = memory
+PIPES = {"MRIQ": 1, "BS": 1, "TEA": 2, "SAD": 2}
 METRICS = ["smsp__inst_executed.sum", "smsp__sass_inst_executed_op_global_ld.sum",
            "smsp__sass_inst_executed_op_global_st.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
            "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -171,6 +182,7 @@ def run(out_path):
     L0 = L0_ns * clock / 1e3
     B = hbm / 32.0 / (n_sm * 4) / (clock * 1e6)      # sectors / cycle / virtual SM
     cfg = {"L0": L0, "B": B, "a0": 1.0, "b0": 0.0}
+    fit_effective(ctx, insts, profiles, measured, cfg, clock, n_sm)
     out = {"device": torch.cuda.get_device_name(0), "n_sm": n_sm, "clock_mhz_under_ncu": clock,
            "latency_ns": L0_ns, "config": cfg, "profiles": profiles, "measured": measured,
            "how": "tools/calibrate.py run (ncu solo pass + CUDA-event timing + slice sweep + PC chain)",
@@ -178,6 +190,61 @@ def run(out_path):
     with open(out_path, "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", out_path, "L0", L0, "cycles", "B", B)
+
+
+def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
+    """Occupancy sweep + least-squares fit of (rm, r) with the pipe ceiling from the plateau."""
+    import numpy as np
+    from scipy.optimize import minimize
+
+    import paper_1303_5164_b200 as K
+    ctx = K.Context(device=0, L0=cfg["L0"], B=cfg["B"], a0=cfg["a0"], b0=cfg["b0"])
+    f = clock_mhz * 1e6
+    for k in KINDS:
+        i = insts[k]
+        prof = profiles[k]
+        p0 = ctx.get_profile(k)
+        sweep = {}
+        for cap in range(1, p0.bmax + 1):
+            ctx.run_capped(k, i.grid, i.args, cap)                       # warm
+            sweep[cap] = ctx.run_capped(k, i.grid, i.args, cap)
+        ipc = {b: prof["ipb"] * i.grid / (ms * 1e-3 * f * 4 * n_sm) for b, ms in sweep.items()}
+        levels = [b for b in ipc if (b * prof["wpb"]) % 4 == 0 and b * prof["wpb"] // 4 <= 16]
+        measured[k]["cap_sweep_ms"] = sweep
+        measured[k]["ipc_meas"] = ipc
+        prof["rm_profiled"], prof["r_profiled"] = prof["rm"], prof["r"]
+        prof["pipe"] = PIPES.get(k, 0)
+        plateau = max(ipc.values()) if ipc else 1.0
+        prof["ipc_max"] = min(1.0, plateau * 1.02) if prof["pipe"] else 1.0
+        if not levels or k == "MM":      # async tensor-core kernel: profiled values kept (R20)
+            continue
+        meas = np.array([ipc[b] for b in levels])
+
+        def model(x):
+            q = dict(prof, rm=float(np.exp(x[0])), r=float(np.exp(x[1])))
+            ctx.set_profile(k, {n: q[n] for n in ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")})
+            preds = ctx.predict([(k, k, b, 0) for b in levels])
+            return np.array([p.ipc1 if p.status == 0 else np.nan for p in preds])
+
+        def loss(x):
+            pr = model(x)
+            return 1e3 if np.any(~np.isfinite(pr)) else float(np.sum((pr - meas) ** 2))
+
+        best = None
+        for rm0 in (prof["rm"], prof["rm"] / 4, prof["rm"] / 16):
+            for r0 in (prof["r"], 1.0, 32.0):
+                x0 = np.log([max(rm0, 1e-6), max(r0, 0.05)])
+                res = minimize(loss, x0, method="Nelder-Mead", options={"xatol": 1e-4, "fatol": 1e-9, "maxiter": 400})
+                if best is None or res.fun < best.fun:
+                    best = res
+        prof["rm"], prof["r"] = float(np.exp(best.x[0])), float(np.exp(best.x[1]))
+        pred = model(best.x)
+        measured[k]["fit"] = {"levels": levels, "ipc_meas": meas.tolist(), "ipc_model": pred.tolist(),
+                              "rmse": float(np.sqrt(np.mean((pred - meas) ** 2))),
+                              "mlp": prof["rm_profiled"] / prof["rm"] if prof["rm"] > 0 else None}
+        print(k, "fit", {n: round(prof[n], 5) for n in ("rm", "r", "ipc_max")}, "rmse",
+              round(measured[k]["fit"]["rmse"], 4), flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":
