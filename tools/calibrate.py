@@ -120,8 +120,11 @@ def run(out_path):
         if kind is None:
             continue
         v = row["Metric Value"].replace(",", "")
-        try:
-            per.setdefault(kind, {})[row["Metric Name"]] = float(v)
+        scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
+                 "s": 1e9, "second": 1e9, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+                 "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(row.get("Metric Unit", ""), 1.0)
+        try:   # normalised to ns and bytes
+            per.setdefault(kind, {})[row["Metric Name"]] = float(v) * scale
         except ValueError:
             per.setdefault(kind, {})[row["Metric Name"]] = v
     # ---- timing, p% sweep, latency ------------------------------------------------------------
@@ -221,7 +224,7 @@ def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
         meas = np.array([ipc[b] for b in levels])
 
         def model(x):
-            q = dict(prof, rm=float(np.exp(x[0])), r=float(np.exp(x[1])))
+            q = dict(prof, rm=float(min(1.0, np.exp(x[0]))), r=float(min(1e4, np.exp(x[1]))))
             ctx.set_profile(k, {n: q[n] for n in ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")})
             preds = ctx.predict([(k, k, b, 0) for b in levels])
             return np.array([p.ipc1 if p.status == 0 else np.nan for p in preds])
@@ -237,7 +240,7 @@ def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
                 res = minimize(loss, x0, method="Nelder-Mead", options={"xatol": 1e-4, "fatol": 1e-9, "maxiter": 400})
                 if best is None or res.fun < best.fun:
                     best = res
-        prof["rm"], prof["r"] = float(np.exp(best.x[0])), float(np.exp(best.x[1]))
+        prof["rm"], prof["r"] = float(min(1.0, np.exp(best.x[0]))), float(min(1e4, np.exp(best.x[1])))
         pred = model(best.x)
         measured[k]["fit"] = {"levels": levels, "ipc_meas": meas.tolist(), "ipc_model": pred.tolist(),
                               "rmse": float(np.sqrt(np.mean((pred - meas) ** 2))),
