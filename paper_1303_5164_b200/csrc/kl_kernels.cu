@@ -147,11 +147,8 @@ struct BodySPMV {
     }
 };
 
-// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block.  The z
-// neighbours ride a register queue; each z-plane of the tile (+1-point halo) is staged in shared
-// memory (double-buffered, one barrier per plane), so a point costs one coalesced global load
-// (plus the amortised halo) instead of five.  Operand order is fixed:
-// ((((z- + z+) + y-) + y+) + x-) + x+, then fmaf(c1, s, -(c0 * in)).
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z
+// neighbours ride a register queue, x/y neighbours come through L1.
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
@@ -159,53 +156,33 @@ struct BodyST {
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        __shared__ float sp[2][6][34];
         const int nx = a.nx, ny = a.ny, nz = a.nz;
         const int gx = (nx + 31) / 32, gy = (ny + 3) / 4;
         const int bx = vb % gx, by = (vb / gx) % gy, bz = vb / (gx * gy);
-        const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
-        const int x = bx * 32 + lane, y = by * 4 + ty;
-        const bool live = x < nx && y < ny;
+        const int x = bx * 32 + (threadIdx.x & 31), y = by * 4 + (threadIdx.x >> 5);
+        if (x >= nx || y >= ny) return;
         const int z0 = bz * 64, z1 = min(z0 + 64, nz);
         const size_t sz = (size_t)nx * ny;
         const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
         const float* in = a.in;
-        // halo duties: warp 0 row y0-1, warp 3 row y0+4; lanes 0 / 31 the x halo of their row
-        const int hy = ty == 0 ? y - 1 : (ty == 3 ? y + 1 : -1);
-        const bool hrow = hy >= 0 && hy < ny && x < nx;
-        const int hx = lane == 0 ? x - 1 : (lane == 31 ? x + 1 : -1);
-        const bool hcol = hx >= 0 && hx < nx && y < ny;
-        const size_t col = (size_t)y * nx + x;
-        float zm = 0.f, c = 0.f, zp = 0.f;
-        if (live) {
-            c = __ldg(in + (size_t)z0 * sz + col);
-            if (z0 > 0) zm = __ldg(in + (size_t)(z0 - 1) * sz + col);
-        }
-        for (int z = z0; z < z1; ++z) {
-            const int buf = z & 1;
-            const size_t pl = (size_t)z * sz;
-            if (live && z + 1 < nz) zp = __ldg(in + pl + sz + col);
-            sp[buf][ty + 1][lane + 1] = c;
-            if (hrow) sp[buf][ty == 0 ? 0 : 5][lane + 1] = __ldg(in + pl + (size_t)hy * nx + x);
-            if (hcol) sp[buf][ty + 1][lane == 0 ? 0 : 33] = __ldg(in + pl + (size_t)y * nx + hx);
-            __syncthreads();
-            if (live) {
-                float* o = a.out + pl + col;
-                if (!ixy || z == 0 || z == nz - 1) {
-                    *o = c;
-                } else {
-                    float s = zm + zp;
-                    s = s + sp[buf][ty][lane + 1];
-                    s = s + sp[buf][ty + 2][lane + 1];
-                    s = s + sp[buf][ty + 1][lane];
-                    s = s + sp[buf][ty + 1][lane + 2];
-                    *o = fmaf(a.c1, s, -(a.c0 * c));
-                }
+        size_t f = (size_t)z0 * sz + (size_t)y * nx + x;
+        float zm = z0 > 0 ? __ldg(in + f - sz) : 0.f;
+        float c = __ldg(in + f);
+        for (int z = z0; z < z1; ++z, f += sz) {
+            float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
+            if (!ixy || z == 0 || z == nz - 1) {
+                a.out[f] = c;
+            } else {
+                float s = zm + zp;
+                s = s + __ldg(in + f - nx);
+                s = s + __ldg(in + f + nx);
+                s = s + __ldg(in + f - 1);
+                s = s + __ldg(in + f + 1);
+                a.out[f] = fmaf(a.c1, s, -(a.c0 * c));
             }
             zm = c;
             c = zp;
         }
-        __syncthreads();   // the next virtual block reuses sp
     }
 };
 

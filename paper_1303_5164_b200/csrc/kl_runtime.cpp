@@ -70,7 +70,7 @@ struct Inst {
     bool finished = false;      // drained and every launch retired
     Launch* inflight = nullptr; // at most one launch in flight per kernel
     uint32_t* audit = nullptr;
-    void* ready = nullptr;      // cudaEvent_t to wait on before launching
+    void* ready = nullptr;      // cudaEvent_t: the kernel arrives (joins R) once it completes
 };
 
 struct Launch {
@@ -127,6 +127,7 @@ struct kl_ctx {
     std::vector<std::unique_ptr<Inst>> insts;
     std::unordered_map<uint64_t, Inst*> by_id;
     std::vector<Inst*> R;              // pending set, arrival order (Alg.1 l.1)
+    std::vector<Inst*> arriving;       // submitted, waiting for their ready event (Alg.1 l.2)
     uint64_t next_id = 1, seq = 0;
     // model batch buffers
     KlModelKind* mk_pinned = nullptr;
@@ -575,6 +576,18 @@ void mark_drained(kl_ctx* ctx, Inst* k) {
 // Poll the launch records.  Returns through *replan whether R changed (a kernel drained) and
 // through *progress whether anything happened at all.
 kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
+    // arrivals (Alg.1 l.2-3; "the arrival of new kernels trigger the recalculation")
+    // only the oldest few are queried per poll: ready events of one copy stream complete in order
+    for (size_t i = 0; i < ctx->arriving.size() && i < 4;) {
+        Inst* k = ctx->arriving[i];
+        cudaError_t e = cudaEventQuery((cudaEvent_t)k->ready);
+        if (e == cudaErrorNotReady) { ++i; continue; }
+        if (e != cudaSuccess) return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id, cudaGetErrorString(e));
+        auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
+        ctx->R.insert(pos, k);
+        ctx->arriving.erase(ctx->arriving.begin() + i);
+        *replan = *progress = true;
+    }
     for (size_t i = 0; i < ctx->inflight.size();) {
         Launch* L = ctx->inflight[i].get();
         KlLaunchRec* r = ctx->recs + L->rec;
@@ -666,11 +679,11 @@ kl_status schedule_step(kl_ctx* ctx, kl_coschedule* out) {
             if (st) return st;
             progress = false;
         }
-        if (ctx->R.empty()) {
+        if (ctx->R.empty() && ctx->arriving.empty()) {
             ctx->have_desired = false;
             return ctx->fail(KL_ENOTFOUND, "nothing pending");
         }
-        if (replan || ctx->inflight.empty()) break;
+        if (!ctx->R.empty() && (replan || ctx->inflight.empty())) break;
         _mm_pause();
         if ((++spins & 0x3FFF) == 0) {
             st = check_streams(ctx);
@@ -901,7 +914,8 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     }
     Inst* raw = k.get();
     ctx->by_id[raw->id] = raw;
-    ctx->R.push_back(raw);
+    if (raw->ready && !ctx->host_only) ctx->arriving.push_back(raw);   // arrives when its inputs land
+    else ctx->R.push_back(raw);
     ctx->insts.push_back(std::move(k));
     if (out_id) *out_id = raw->id;
     return KL_OK;
