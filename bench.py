@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile", default=os.path.join(ROOT, "profiles", "kl_profile_b200.json"))
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--split-rule", type=int, default=None, help="0 argmin dT (paper Eq.8), 1 argmax CP")
+    ap.add_argument("--cp-min", type=float, default=None)
     return ap.parse_args()
 
 
@@ -180,6 +182,10 @@ def run_kernelet(args, rank, world, local_rank):
     lane_a = torch.cuda.Stream(device=dev)
     lane_b = torch.cuda.Stream(device=dev)
     cfg = dict(kcfg)
+    if args.split_rule is not None:
+        cfg["split_rule"] = args.split_rule
+    if args.cp_min is not None:
+        cfg["cp_min"] = args.cp_min
     ctx = K.Context(device=local_rank, profiles=profiles, streams=(lane_a, lane_b), counters=counters, **cfg)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126.5 MiB)
     gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev)
@@ -471,7 +477,9 @@ def main():
     config = {"workload": f"ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels, "
                           f"{args.size} sizes, all pending at t=0)", "global_kernels": len(ALL) * args.instances * world,
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
-              "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step"}
+              "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
+              "split_rule": "argmax CP" if args.split_rule == 1 else "argmin dT (Eq.8)",
+              "cp_min": args.cp_min or 0.0}
 
     if args.impl == "reference":
         if rank != 0:

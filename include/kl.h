@@ -136,6 +136,7 @@ typedef struct {
     int32_t n_sched;           /* warp schedulers per SM -> virtual SM; 4 on B200 */
     int32_t latency_mode;      /* 0 linear-in-requests (R2), 1 verbatim P:875 */
     int32_t level_mode;        /* 0: every b with b*wpb % n_sched == 0; 1: four levels (config C2) */
+    int32_t split_rule;        /* slice ratio per pair: 0 argmin dT (Eq.8, the paper); 1 argmax CP */
     int32_t n_sms;             /* 0 = from the device */
     int32_t chunk;             /* virtual blocks per work fetch; 0 = per-kind default */
     int32_t audit;             /* 1: count executions per virtual block (coverage audit) */

@@ -415,8 +415,15 @@ def prune(pending, pairs, profs, ap, am):
     return pairs, (0.0, 0.0)
 
 
-def _better_split(a, b):
-    """a9: argmin dT; ties: larger C, then more warps, then smaller b1."""
+def _better_split(a, b, rule=0):
+    """a9: argmin dT; ties: larger C, then more warps, then smaller b1.  rule 1 (ablation):
+    highest CP first, then the same order."""
+    if rule == 1:
+        t = _band(a["cp"], b["cp"])
+        if a["cp"] > b["cp"] + t:
+            return True
+        if a["cp"] < b["cp"] - t:
+            return False
     t = _band(a["dT"], b["dT"])
     if a["dT"] < b["dT"] - t:
         return True
@@ -433,7 +440,7 @@ def _better_split(a, b):
 
 
 def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, nsched=4,
-                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0) -> dict:
+                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0, split_rule=0) -> dict:
     """Proc. FindCoSchedule: candidates -> prune -> model CP -> argmax.
 
     Per surviving pair the slice ratio is the argmin of dT (Eq.8) over maximal splits; across
@@ -462,7 +469,7 @@ def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, n
             evaluated.append(cand)
             if pr["status"] != 0:
                 continue
-            if bestsplit is None or _better_split(cand, bestsplit):
+            if bestsplit is None or _better_split(cand, bestsplit, split_rule):
                 bestsplit = cand
         if bestsplit is None:
             continue

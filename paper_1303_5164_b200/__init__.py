@@ -103,6 +103,7 @@ class Config(C.Structure):
     _fields_ = [("alpha_p", C.c_double), ("alpha_m", C.c_double), ("p_percent", C.c_double),
                 ("L0", C.c_double), ("B", C.c_double), ("a0", C.c_double), ("b0", C.c_double),
                 ("cp_min", C.c_double), ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
+                ("split_rule", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
                 ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),

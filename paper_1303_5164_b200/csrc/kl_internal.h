@@ -101,6 +101,7 @@ struct KlModelKind {       // per-kind model inputs, device table
 struct KlModelCfg {
     double L0, B, a0, b0;
     int32_t W, n_sched, latency_mode, n_cand;
+    int32_t split_rule, pad;
 };
 struct KlCand {            // one candidate, and its grouping for the fused selection
     int32_t k1, k2;

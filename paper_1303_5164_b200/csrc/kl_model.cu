@@ -155,7 +155,13 @@ __device__ __forceinline__ double band(double x, double y) {
 }
 
 // a9 split order: argmin dT; ties (1e-12 band): larger C, more warps, smaller b1.
-__device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb) {
+__device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb,
+                             int rule) {
+    if (rule == 1) {   // ablation: highest predicted CP first
+        double t = band(a.cp, b.cp);
+        if (a.cp > b.cp + t) return true;
+        if (a.cp < b.cp - t) return false;
+    }
     double t = band(a.dT, b.dT);
     if (a.dT < b.dT - t) return true;
     if (a.dT > b.dT + t) return false;
@@ -254,7 +260,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
             kl_prediction a = preds[i];
             if (a.status != 0) continue;
             KlCand ca = cands[i];
-            if (best < 0 || better_split(a, ca, bp, bc)) { best = i; bp = a; bc = ca; }
+            if (best < 0 || better_split(a, ca, bp, bc, cfg.split_rule)) { best = i; bp = a; bc = ca; }
         }
         if (pr < 128) s_best_pair[pr] = best;
     }

@@ -241,7 +241,12 @@ bool pruned(const kl_profile& a, const kl_profile& b, double ap, double am) {
     return std::fabs(a.pur - b.pur) < ap && std::fabs(a.mur - b.mur) < am;   // R9: AND, strict
 }
 
-bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb) {
+bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb, int rule) {
+    if (rule == 1) {   // ablation: the split with the highest predicted CP (SURVEY key finding 4)
+        double t = band(a.cp, b.cp);
+        if (a.cp > b.cp + t) return true;
+        if (a.cp < b.cp - t) return false;
+    }
     double t = band(a.dT, b.dT);
     if (a.dT < b.dT - t) return true;
     if (a.dT > b.dT + t) return false;
@@ -277,6 +282,7 @@ KlModelCfg model_cfg(const kl_ctx* c, int n) {
     m.n_sched = c->cfg.n_sched;
     m.latency_mode = c->cfg.latency_mode;
     m.n_cand = n;
+    m.split_rule = c->cfg.split_rule;
     return m;
 }
 
@@ -374,7 +380,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
         bool have[KL_NKINDS] = {};
         for (auto* k : R) have[k->kind] = true;
         for (int a = 0; a < KL_NKINDS; ++a)
-            for (int b = a; b < KL_NKINDS; ++b) {
+            for (int b = 0; b < KL_NKINDS; ++b) {   // both orders: K1 is whichever arrived first
                 if (!have[a] || !have[b]) continue;
                 for (auto& sp : maximal_splits(ctx, ctx->prof[a], ctx->prof[b])) {
                     if (ctx->cache.count(cache_key(a, b, sp.first, sp.second))) continue;
@@ -409,7 +415,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
                 const KlCand& cd = ctx->cand_pinned[i];
                 const kl_prediction& a = ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)];
                 if (a.status != 0) continue;
-                if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi])) { bi = i; bp = a; }
+                if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
             }
             if (bi < 0) continue;
             if (best < 0 || bp.cp > bcp + band(bp.cp, bcp)) { best = bi; bcp = bp.cp; }

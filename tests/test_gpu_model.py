@@ -92,8 +92,9 @@ def test_decisions_match_oracle():
     for rep in range(12):
         profs = _rand_profiles(rng)
         cp_min = float(rng.choice([0.0, 0.02]))
+        rule = int(rep % 2)
         ctx = _ctx(profs, alpha_p=float(rng.choice([0.0, 0.2, 0.4])), alpha_m=float(rng.choice([0.0, 0.05, 0.1])),
-                   cp_min=cp_min)
+                   cp_min=cp_min, split_rule=rule)
         n = int(rng.integers(1, 9))
         kinds = [str(k) for k in rng.choice([k for k in K.KINDS if k != "MM"], n)]
         pend = []
@@ -102,7 +103,7 @@ def test_decisions_match_oracle():
             pend.append({"kind": k, "blocks": 1000, "id": kid})
         d1, d2 = _decide_both(ctx)
         ref = O.find_co_schedule(pend, profs, O.smcfg(W=16, **CFG), ap=ctx.config.alpha_p,
-                                 am=ctx.config.alpha_m, cp_min=cp_min)
+                                 am=ctx.config.alpha_m, cp_min=cp_min, split_rule=rule)
         for d in (d1, d2):
             assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref["solo"])
             assert d.id1 == pend[ref["ia"]]["id"]

@@ -224,7 +224,7 @@ def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
         meas = np.array([ipc[b] for b in levels])
 
         def model(x):
-            q = dict(prof, rm=float(min(1.0, np.exp(x[0]))), r=float(min(1e4, np.exp(x[1]))))
+            q = dict(prof, rm=float(min(1.0, np.exp(x[0]))), r=float(min(64.0, max(0.25, np.exp(x[1])))))
             ctx.set_profile(k, {n: q[n] for n in ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")})
             preds = ctx.predict([(k, k, b, 0) for b in levels])
             return np.array([p.ipc1 if p.status == 0 else np.nan for p in preds])
@@ -240,7 +240,7 @@ def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
                 res = minimize(loss, x0, method="Nelder-Mead", options={"xatol": 1e-4, "fatol": 1e-9, "maxiter": 400})
                 if best is None or res.fun < best.fun:
                     best = res
-        prof["rm"], prof["r"] = float(min(1.0, np.exp(best.x[0]))), float(min(1e4, np.exp(best.x[1])))
+        prof["rm"], prof["r"] = float(min(1.0, np.exp(best.x[0]))), float(min(64.0, max(0.25, np.exp(best.x[1]))))
         pred = model(best.x)
         measured[k]["fit"] = {"levels": levels, "ipc_meas": meas.tolist(), "ipc_model": pred.tolist(),
                               "rmse": float(np.sqrt(np.mean((pred - meas) ** 2))),
