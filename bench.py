@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile", default=os.path.join(ROOT, "profiles", "kl_profile_b200.json"))
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--split-rule", type=int, default=None, help="0 argmin dT (paper Eq.8), 1 argmax CP")
+    ap.add_argument("--split-rule", type=int, default=1,
+                    help="slice ratio per pair: 1 argmax CP over all co-schedules (FindCoSchedule l.3-4, "
+                         "default), 0 argmin dT (Eq.8 balanced ratio)")
     ap.add_argument("--cp-min", type=float, default=None)
     return ap.parse_args()
 
@@ -182,8 +184,7 @@ def run_kernelet(args, rank, world, local_rank):
     lane_a = torch.cuda.Stream(device=dev)
     lane_b = torch.cuda.Stream(device=dev)
     cfg = dict(kcfg)
-    if args.split_rule is not None:
-        cfg["split_rule"] = args.split_rule
+    cfg["split_rule"] = args.split_rule
     if args.cp_min is not None:
         cfg["cp_min"] = args.cp_min
     ctx = K.Context(device=local_rank, profiles=profiles, streams=(lane_a, lane_b), counters=counters, **cfg)
@@ -478,7 +479,7 @@ def main():
                           f"{args.size} sizes, all pending at t=0)", "global_kernels": len(ALL) * args.instances * world,
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
-              "split_rule": "argmax CP" if args.split_rule == 1 else "argmin dT (Eq.8)",
+              "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
               "cp_min": args.cp_min or 0.0}
 
     if args.impl == "reference":

@@ -178,8 +178,8 @@ typedef struct {               /* runtime statistics since kl_create */
     int64_t stops;             /* stop requests (re-plans that changed a running kernel) */
     int64_t model_batches, model_candidates;
     int64_t device_launches;   /* every kernel launched by the library (incl. model, stop, init) */
-    int64_t decide_ns;         /* host time spent in FindCoSchedule */
-    int64_t pad;
+    int64_t decide_ns;         /* host time spent in FindCoSchedule (incl. model batches) */
+    int64_t model_ns;          /* host time spent waiting for model batches */
 } kl_stats;
 typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;

@@ -144,7 +144,7 @@ class Counters(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("decisions", "launches", "stops", "model_batches", "model_candidates",
-                                         "device_launches", "decide_ns", "pad")]
+                                         "device_launches", "decide_ns", "model_ns")]
 
 
 class TraceRec(C.Structure):

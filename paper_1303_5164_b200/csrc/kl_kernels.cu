@@ -147,8 +147,11 @@ struct BodySPMV {
     }
 };
 
-// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z
-// neighbours ride a register queue, x/y neighbours come through L1.
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block, marched in
+// groups of 4 planes: the 4 next planes of the column and the 16 x/y neighbours of a group are
+// independent loads issued together (memory-level parallelism for HBM latency); the z
+// neighbours ride a register window.  Operand order is fixed:
+// ((((z- + z+) + y-) + y+) + x-) + x+, then fmaf(c1, s, -(c0 * in)).
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
@@ -164,24 +167,43 @@ struct BodyST {
         const int z0 = bz * 64, z1 = min(z0 + 64, nz);
         const size_t sz = (size_t)nx * ny;
         const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
-        const float* in = a.in;
-        size_t f = (size_t)z0 * sz + (size_t)y * nx + x;
-        float zm = z0 > 0 ? __ldg(in + f - sz) : 0.f;
-        float c = __ldg(in + f);
-        for (int z = z0; z < z1; ++z, f += sz) {
-            float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
-            if (!ixy || z == 0 || z == nz - 1) {
-                a.out[f] = c;
-            } else {
-                float s = zm + zp;
-                s = s + __ldg(in + f - nx);
-                s = s + __ldg(in + f + nx);
-                s = s + __ldg(in + f - 1);
-                s = s + __ldg(in + f + 1);
-                a.out[f] = fmaf(a.c1, s, -(a.c0 * c));
+        const float* in = a.in + (size_t)y * nx + x;
+        float* out = a.out + (size_t)y * nx + x;
+        float w[6];
+        w[0] = z0 > 0 ? __ldg(in + (size_t)(z0 - 1) * sz) : 0.f;
+        w[1] = __ldg(in + (size_t)z0 * sz);
+        for (int z = z0; z < z1; z += 4) {
+            float ym[4], yp[4], xm[4], xp[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int zz = z + u + 1;
+                w[u + 2] = zz < nz ? __ldg(in + (size_t)zz * sz) : 0.f;
+                const size_t pl = (size_t)(z + u) * sz;
+                const bool act = ixy && z + u < z1;
+                ym[u] = act ? __ldg(in + pl - nx) : 0.f;
+                yp[u] = act ? __ldg(in + pl + nx) : 0.f;
+                xm[u] = act ? __ldg(in + pl - 1) : 0.f;
+                xp[u] = act ? __ldg(in + pl + 1) : 0.f;
             }
-            zm = c;
-            c = zp;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int zc = z + u;
+                if (zc >= z1) break;
+                const float c = w[u + 1];
+                float* o = out + (size_t)zc * sz;
+                if (!ixy || zc == 0 || zc == nz - 1) {
+                    *o = c;
+                } else {
+                    float s = w[u] + w[u + 2];
+                    s = s + ym[u];
+                    s = s + yp[u];
+                    s = s + xm[u];
+                    s = s + xp[u];
+                    *o = fmaf(a.c1, s, -(a.c0 * c));
+                }
+            }
+            w[0] = w[4];
+            w[1] = w[5];
         }
     }
 };

@@ -98,6 +98,18 @@ inline uint64_t cache_key(int k1, int k2, uint32_t b1, uint32_t b2) {
     return (((uint64_t)k1 * 16 + (uint64_t)k2) * 1024 + b1) * 1024 + b2;
 }
 
+// The model is symmetric in the two kernels (the joint chain of (K2,K1) is that of (K1,K2) with
+// the state pair reordered): a prediction for (k2,k1,b2,b1) is the stored (k1,k2,b1,b2) one with
+// the per-kernel fields swapped.
+inline kl_prediction swap_pred(const kl_prediction& p) {
+    kl_prediction q = p;
+    q.ipc1 = p.ipc2;
+    q.ipc2 = p.ipc1;
+    q.solo1 = p.solo2;
+    q.solo2 = p.solo1;
+    return q;
+}
+
 }  // namespace
 
 struct kl_ctx {
@@ -142,6 +154,13 @@ struct kl_ctx {
     KlDecision* dec_dev = nullptr;
     KlDecision* dec_pinned = nullptr;
     std::unordered_map<uint64_t, kl_prediction> cache;
+    bool lookup(int k1, int k2, uint32_t b1, uint32_t b2, kl_prediction* out) const {
+        auto it = cache.find(cache_key(k1, k2, b1, b2));
+        if (it != cache.end()) { if (out) *out = it->second; return true; }
+        it = cache.find(cache_key(k2, k1, b2, b1));
+        if (it != cache.end()) { if (out) *out = swap_pred(it->second); return true; }
+        return false;
+    }
     int64_t model_batches = 0, model_cands = 0;
     std::vector<kl_trace_rec> trace;
     int64_t* counters = nullptr;
@@ -289,6 +308,7 @@ KlModelCfg model_cfg(const kl_ctx* c, int n) {
 // Run the device model over cand_pinned[0..n); n_pairs > 0 fuses the selection.
 kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
+    const auto t_model = std::chrono::steady_clock::now();
     fill_model_kinds(ctx);
     KL_CUDA(cudaMemcpyAsync(ctx->mk_dev, ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaMemcpyHostToDevice, ctx->ctrl));
     KL_CUDA(cudaMemcpyAsync(ctx->cand_dev, ctx->cand_pinned, sizeof(KlCand) * n, cudaMemcpyHostToDevice, ctx->ctrl));
@@ -304,6 +324,7 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     ctx->model_batches++;
     ctx->model_cands += n;
     ctx->st.device_launches++;
+    ctx->st.model_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_model).count();
     for (int i = 0; i < n; ++i) {
         const KlCand& cd = ctx->cand_pinned[i];
         ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)] = ctx->pred_pinned[i];
@@ -363,7 +384,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             cd.pair = np;
             cd.warps = (int)s.first * ctx->prof[k1].wpb + (int)s.second * ctx->prof[k2].wpb;
             ctx->cand_pinned[n++] = cd;
-            if (!ctx->cache.count(cache_key(k1, k2, s.first, s.second))) missing = true;
+            if (!ctx->lookup(k1, k2, s.first, s.second, nullptr)) missing = true;
         }
         pair_of_group.push_back(pq);
         ++np;
@@ -380,14 +401,15 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
         bool have[KL_NKINDS] = {};
         for (auto* k : R) have[k->kind] = true;
         for (int a = 0; a < KL_NKINDS; ++a)
-            for (int b = 0; b < KL_NKINDS; ++b) {   // both orders: K1 is whichever arrived first
+            for (int b = a; b < KL_NKINDS; ++b) {   // one order; the other is derived (swap_pred)
                 if (!have[a] || !have[b]) continue;
                 for (auto& sp : maximal_splits(ctx, ctx->prof[a], ctx->prof[b])) {
-                    if (ctx->cache.count(cache_key(a, b, sp.first, sp.second))) continue;
+                    if (ctx->lookup(a, b, sp.first, sp.second, nullptr)) continue;
                     bool in_list = false;
                     for (int i = 0; i < n && !in_list; ++i) {
                         const KlCand& c = ctx->cand_pinned[i];
-                        in_list = c.k1 == a && c.k2 == b && c.b1 == sp.first && c.b2 == sp.second;
+                        in_list = (c.k1 == a && c.k2 == b && c.b1 == sp.first && c.b2 == sp.second) ||
+                                  (c.k1 == b && c.k2 == a && c.b1 == sp.second && c.b2 == sp.first);
                     }
                     if (in_list || ne >= kMaxCand) continue;
                     KlCand cd{};
@@ -413,7 +435,8 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             kl_prediction bp{};
             for (int i = ctx->off_pinned[p]; i < ctx->off_pinned[p + 1]; ++i) {
                 const KlCand& cd = ctx->cand_pinned[i];
-                const kl_prediction& a = ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)];
+                kl_prediction a{};
+                ctx->lookup(cd.k1, cd.k2, cd.b1, cd.b2, &a);
                 if (a.status != 0) continue;
                 if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
             }
