@@ -40,8 +40,8 @@ METRIC = "kernel-queue throughput (kernels/s) & speedup vs sequential, 1/2/4/8 B
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kernelet", choices=["kernelet", "reference"])
     ap.add_argument("--instances", type=int, default=4, help="instances of each ALL-mix kernel per GPU")
     ap.add_argument("--size", default="paper", choices=["paper", "small"])
@@ -61,8 +61,9 @@ def parse():
 # arithmetic the method must do, per instance at the given size.  Used for the roofline.
 # ---------------------------------------------------------------------------------------------
 def algorithmic_work(kind: str, p: dict) -> dict:
-    if kind == "PC":      # one 32-B DRAM sector per dependent load + 8 B of output per thread
-        return {"bound": "hbm", "bytes": p["n_threads"] * (p["hops"] * 32 + 8)}
+    if kind == "PC":      # one 64-B HBM3e access per random dependent load (nodes are visited
+        # once: no reuse for L2) + 8 B of output per thread; ncu: 64 B DRAM read per hop
+        return {"bound": "hbm", "bytes": p["n_threads"] * (p["hops"] * 64 + 8)}
     if kind == "SAD":     # 4 pixel |diff|-accumulates per vabsdiff4; ALU-bound
         n_mb = (p["width"] // 16) * (p["height"] // 16)
         return {"bound": "alu", "ops": n_mb * 1089 * 256 / 4, "bytes": 2 * p["width"] * p["height"] + n_mb * 1089 * 2}
@@ -94,38 +95,42 @@ def alu_peak(kind: str, sm_mhz: float, n_sm: int = 148) -> tuple[float, str]:
 
 # ---------------------------------------------------------------------------------------------
 class Clocks:
-    """Sample nvidia-smi during the timed region (B200_PROFILING.md clocks line)."""
+    """Sample nvidia-smi during the timed region (B200_PROFILING.md clocks line): one streaming
+    `nvidia-smi -lms 100` process started before and stopped after the timed steps."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.2)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.samples.append(f)
 
     def summary(self) -> dict:
         if not self.samples:

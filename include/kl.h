@@ -225,6 +225,12 @@ kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* desc, void* stream,
  * (0 = uncapped), outside the scheduler; blocks until done; *ms = device time of the launch.
  * Occupancy sweeps for the calibration (solo IPC vs warps, the E4 analog). */
 kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* desc, uint32_t cap, double* ms);
+/* Co-run two whole kernels outside the scheduler at caps (cap1, cap2): both are launched through
+ * the slice launcher, the survivor is stopped at its slice boundary when the first runs out of
+ * blocks, and the two launch records are returned (config C3: measured concurrent progress vs
+ * the model's cIPC; E5/E7 analogs). */
+kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, const kl_kernel_desc* d2,
+                      uint32_t cap2, kl_trace_rec out[2]);
 kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out);
 kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p);   /* clears model cache */
 kl_status kl_reset_model_cache(kl_ctx* ctx);

@@ -158,7 +158,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -197,6 +197,7 @@ def lib() -> C.CDLL:
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
     L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
+    L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
     for s in ABI_SYMBOLS:
         if s not in ("kl_abi_version", "kl_last_error", "kl_struct_sizes"):
             getattr(L, s).restype = C.c_int
@@ -340,6 +341,17 @@ class Context:
         ms = C.c_double()
         self._check(self._L.kl_run_capped(self._h, C.byref(d), cap, C.byref(ms)))
         return ms.value
+
+    def run_pair(self, kind1, grid1, args1, cap1, kind2, grid2, args2, cap2):
+        """Co-run two kernels at the given caps until the first runs out of blocks (the other is
+        stopped at its slice boundary); returns the two launch records."""
+        k1 = KIND_ID[kind1] if isinstance(kind1, str) else int(kind1)
+        k2 = KIND_ID[kind2] if isinstance(kind2, str) else int(kind2)
+        d1 = KernelDesc(k1, grid1, C.cast(C.pointer(args1), _vp), C.sizeof(args1), None, 0, None)
+        d2 = KernelDesc(k2, grid2, C.cast(C.pointer(args2), _vp), C.sizeof(args2), None, 0, None)
+        out = (TraceRec * 2)()
+        self._check(self._L.kl_run_pair(self._h, C.byref(d1), cap1, C.byref(d2), cap2, out))
+        return out[0], out[1]
 
     def get_profile(self, kind) -> Profile:
         p = Profile()

@@ -19,12 +19,10 @@ constexpr int kMaxW = 16;                 // virtual-SM warps (64 warps / 4 sche
 constexpr int kMaxS = (kMaxW / 2 + 1) * (kMaxW / 2 + 1);   // 81 joint states at W_v = 16
 constexpr int kThreads = 128;
 
-__device__ double binom_d(int n, int k) {
-    if (k < 0 || k > n) return 0.0;
-    double r = 1.0;
-    for (int i = 1; i <= k; ++i) r = r * (double)(n - k + i) / (double)i;
-    return r;
-}
+// Binomial coefficients C(n,k), n <= 16 (exact in double).
+__constant__ double c_binom[17][17];
+
+__device__ __forceinline__ double binom_d(int n, int k) { return (k < 0 || k > n) ? 0.0 : c_binom[n][k]; }
 
 __device__ double latency(const KlModelCfg& c, double n, int idle) {
     if (c.latency_mode == 1) return c.L0 + c.B / (c.a0 * (double)(idle > 1 ? idle : 1)) + c.b0;
@@ -55,15 +53,23 @@ __device__ bool p_ir(const KlModelCfg& c, double R, int idle, double n, double* 
     return true;
 }
 
-// One-kernel transition row from i idle of w (Eq.2 summed with binomial weights, R3).
+// One-kernel transition row from i idle of w (Eq.2 summed with binomial weights, R3).  The
+// powers p^a (1-p)^(i-a) are built by repeated multiplication (no pow()), in the same (a, b)
+// accumulation order as the oracle.
 __device__ void row_of(int w, int i, double pir, double rm, double* row) {
+    double pw[kMaxW + 1], qw[kMaxW + 1], rw[kMaxW + 1], sw[kMaxW + 1];
+    pw[0] = qw[0] = rw[0] = sw[0] = 1.0;
+    for (int t = 1; t <= w; ++t) {
+        pw[t] = pw[t - 1] * pir;
+        qw[t] = qw[t - 1] * (1.0 - pir);
+        rw[t] = rw[t - 1] * rm;
+        sw[t] = sw[t - 1] * (1.0 - rm);
+    }
     for (int j = 0; j <= w; ++j) row[j] = 0.0;
+    const int nr = w - i;
     for (int a = 0; a <= i; ++a) {
-        double pa = binom_d(i, a) * pow(pir, (double)a) * pow(1.0 - pir, (double)(i - a));
-        for (int b = 0; b <= w - i; ++b) {
-            double pb = binom_d(w - i, b) * pow(rm, (double)b) * pow(1.0 - rm, (double)(w - i - b));
-            row[i - a + b] += pa * pb;
-        }
+        const double pa = binom_d(i, a) * pw[a] * qw[i - a];
+        for (int b = 0; b <= nr; ++b) row[i - a + b] += pa * (binom_d(nr, b) * rw[b] * sw[nr - b]);
     }
 }
 
@@ -294,6 +300,13 @@ int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* c
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_model_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        double tab[17][17] = {};
+        for (int n = 0; n <= 16; ++n) {
+            tab[n][0] = 1.0;
+            for (int k = 1; k <= n; ++k) tab[n][k] = tab[n - 1][k - 1] + (k <= n - 1 ? tab[n - 1][k] : 0.0);
+        }
+        e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }

@@ -1092,6 +1092,59 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     return KL_OK;
 }
 
+kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, const kl_kernel_desc* d2,
+                      uint32_t cap2, kl_trace_rec out[2]) {
+    KL_LIVE(ctx);
+    if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context");
+    if (!ctx->inflight.empty() || !ctx->R.empty()) return ctx->fail(KL_EBUSY, "scheduler has pending work");
+    uint64_t id1 = 0, id2 = 0;
+    kl_status st = kl_submit(ctx, d1, &id1);
+    if (!st) st = kl_submit(ctx, d2, &id2);
+    if (st) return st;
+    Inst* k1 = ctx->by_id[id1];
+    Inst* k2 = ctx->by_id[id2];
+    ctx->R.clear();                       // not scheduled: launched directly below
+    st = flush_ctl_init(ctx);
+    if (st) return st;
+    const size_t t0 = ctx->trace.size();
+    st = launch_kernel(ctx, k1, cap1, slice_of(ctx, cap1 ? cap1 : 1, 1), k2->kind, 0.0);
+    if (!st) st = launch_kernel(ctx, k2, cap2, slice_of(ctx, cap2 ? cap2 : 1, 1), k1->kind, 0.0);
+    if (st) return st;
+    bool stopped = false;
+    uint64_t spins = 0;
+    while (k1->inflight || k2->inflight) {
+        bool rp = false, pg = false;
+        st = poll(ctx, &rp, &pg);
+        if (st) return st;
+        if (!stopped && (k1->drained || k2->drained)) {   // first one ran out of blocks
+            Inst* other = k1->drained ? k2 : k1;
+            if (other->inflight && !other->drained) {
+                st = request_stop(ctx, other->inflight);
+                if (st) return st;
+            }
+            stopped = true;
+        }
+        _mm_pause();
+        if ((++spins & 0x3FFF) == 0) {
+            st = check_streams(ctx);
+            if (st) return st;
+        }
+    }
+    if (ctx->trace.size() < t0 + 2) return ctx->fail(KL_ECUDA, "pair run lost a record");
+    for (size_t i = t0; i < ctx->trace.size(); ++i) {
+        const kl_trace_rec& t = ctx->trace[i];
+        if (t.id == id1) out[0] = t;
+        if (t.id == id2) out[1] = t;
+    }
+    // the stopped kernel keeps its remainder; it is not part of any queue
+    for (Inst* k : {k1, k2})
+        if (!k->finished) {
+            k->drained = k->finished = true;
+            ctx->free_slots.push_back(k->slot);
+        }
+    return KL_OK;
+}
+
 kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out) {
     KL_LIVE(ctx);
     if (kind < 0 || kind >= KL_NKINDS || !out) return KL_EINVAL;
