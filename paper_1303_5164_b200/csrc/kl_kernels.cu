@@ -147,11 +147,12 @@ struct BodySPMV {
     }
 };
 
-// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block, marched in
-// groups of 4 planes: the 4 next planes of the column and the 16 x/y neighbours of a group are
-// independent loads issued together (memory-level parallelism for HBM latency); the z
-// neighbours ride a register window.  Operand order is fixed:
-// ((((z- + z+) + y-) + y+) + x-) + x+, then fmaf(c1, s, -(c0 * in)).
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block.  Issue-lean
+// (ncu showed the first version issue-bound at 40 instructions per point): boundary columns are
+// a plain copy; an interior column walks z with one base pointer, a 3-plane register window and
+// the four x/y neighbours at fixed offsets, 4 planes per group so their loads are in flight
+// together.  Operand order is fixed: ((((z- + z+) + y-) + y+) + x-) + x+, then
+// fmaf(c1, s, -(c0 * in)).
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
@@ -166,50 +167,70 @@ struct BodyST {
         if (x >= nx || y >= ny) return;
         const int z0 = bz * 64, z1 = min(z0 + 64, nz);
         const size_t sz = (size_t)nx * ny;
-        const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
-        const float* in = a.in + (size_t)y * nx + x;
-        float* out = a.out + (size_t)y * nx + x;
-        float w[6];
-        w[0] = z0 > 0 ? __ldg(in + (size_t)(z0 - 1) * sz) : 0.f;
-        w[1] = __ldg(in + (size_t)z0 * sz);
-        for (int z = z0; z < z1; z += 4) {
-            float ym[4], yp[4], xm[4], xp[4];
+        const float* pin = a.in + (size_t)z0 * sz + (size_t)y * nx + x;
+        float* pout = a.out + (size_t)z0 * sz + (size_t)y * nx + x;
+        if (!(x > 0 && x < nx - 1 && y > 0 && y < ny - 1)) {   // boundary column: out = in
+            for (int z = z0; z < z1; ++z, pin += sz, pout += sz) *pout = __ldg(pin);
+            return;
+        }
+        const float c0 = a.c0, c1 = a.c1;
+        float zm = z0 > 0 ? __ldg(pin - sz) : 0.f;
+        float c = __ldg(pin);
+        int z = z0;
+        for (; z + 4 <= z1; z += 4, pin += 4 * sz, pout += 4 * sz) {
+            float v[4], ym[4], yp[4], xm[4], xp[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int zz = z + u + 1;
-                w[u + 2] = zz < nz ? __ldg(in + (size_t)zz * sz) : 0.f;
-                const size_t pl = (size_t)(z + u) * sz;
-                const bool act = ixy && z + u < z1;
-                ym[u] = act ? __ldg(in + pl - nx) : 0.f;
-                yp[u] = act ? __ldg(in + pl + nx) : 0.f;
-                xm[u] = act ? __ldg(in + pl - 1) : 0.f;
-                xp[u] = act ? __ldg(in + pl + 1) : 0.f;
+                const float* q = pin + u * sz;
+                v[u] = (z + u + 1 < nz) ? __ldg(q + sz) : 0.f;   // plane z+u+1 (z+ of point u)
+                ym[u] = __ldg(q - nx);
+                yp[u] = __ldg(q + nx);
+                xm[u] = __ldg(q - 1);
+                xp[u] = __ldg(q + 1);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int zc = z + u;
-                if (zc >= z1) break;
-                const float c = w[u + 1];
-                float* o = out + (size_t)zc * sz;
-                if (!ixy || zc == 0 || zc == nz - 1) {
-                    *o = c;
+                const float zp = v[u];
+                float r;
+                if (zc == 0 || zc == nz - 1) {
+                    r = c;
                 } else {
-                    float s = w[u] + w[u + 2];
-                    s = s + ym[u];
-                    s = s + yp[u];
-                    s = s + xm[u];
-                    s = s + xp[u];
-                    *o = fmaf(a.c1, s, -(a.c0 * c));
+                    float s2 = zm + zp;
+                    s2 = s2 + ym[u];
+                    s2 = s2 + yp[u];
+                    s2 = s2 + xm[u];
+                    s2 = s2 + xp[u];
+                    r = fmaf(c1, s2, -(c0 * c));
                 }
+                pout[u * sz] = r;
+                zm = c;
+                c = zp;
             }
-            w[0] = w[4];
-            w[1] = w[5];
+        }
+        for (; z < z1; ++z, pin += sz, pout += sz) {            // ragged z tail
+            const float zp = (z + 1 < nz) ? __ldg(pin + sz) : 0.f;
+            float r;
+            if (z == 0 || z == nz - 1) {
+                r = c;
+            } else {
+                float s2 = zm + zp;
+                s2 = s2 + __ldg(pin - nx);
+                s2 = s2 + __ldg(pin + nx);
+                s2 = s2 + __ldg(pin - 1);
+                s2 = s2 + __ldg(pin + 1);
+                r = fmaf(c1, s2, -(c0 * c));
+            }
+            *pout = r;
+            zm = c;
+            c = zp;
         }
     }
 };
 
-// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks;
-// phase reduced to [-1/2, 1/2] turns (on the FMA pipe) before the MUFU sin/cos.  MUFU-bound:
+// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks
+// with 2*pi folded into k at staging time, so the inner loop is 3 FMA for the phase, the two
+// MUFU ops (MUFU.SIN/COS reduce the argument themselves) and 2 FMA accumulates.  MUFU-bound:
 // 2 MUFU ops per (voxel, k) at 16 lanes/clk/SM.
 struct BodyMRIQ {
     using Params = kl_args_mriq;
@@ -218,7 +239,7 @@ struct BodyMRIQ {
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        __shared__ float skx[256], sky[256], skz[256], sph[256];
+        __shared__ float4 sk[256];   // (2 pi kx, 2 pi ky, 2 pi kz, phiMag)
         const int i = (int)vb * 256 + threadIdx.x;
         const bool live = i < a.num_x;
         const float x = live ? __ldg(a.x + i) : 0.f, y = live ? __ldg(a.y + i) : 0.f,
@@ -229,23 +250,19 @@ struct BodyMRIQ {
             const int n = min(256, a.num_k - k0);
             __syncthreads();
             if ((int)threadIdx.x < n) {
-                skx[threadIdx.x] = __ldg(a.kx + k0 + threadIdx.x);
-                sky[threadIdx.x] = __ldg(a.ky + k0 + threadIdx.x);
-                skz[threadIdx.x] = __ldg(a.kz + k0 + threadIdx.x);
-                sph[threadIdx.x] = __ldg(a.phimag + k0 + threadIdx.x);
+                const int k = k0 + threadIdx.x;
+                sk[threadIdx.x] = make_float4(two_pi * __ldg(a.kx + k), two_pi * __ldg(a.ky + k),
+                                              two_pi * __ldg(a.kz + k), __ldg(a.phimag + k));
             }
             __syncthreads();
 #pragma unroll 8
             for (int k = 0; k < n; ++k) {
-                float t = fmaf(skx[k], x, fmaf(sky[k], y, skz[k] * z));
-                // t - rint(t) with the FMA pipe (1.5 * 2^23 trick, exact for |t| < 2^22): FRND
-                // would run on the MUFU pipe the sin/cos already saturate (ncu: XU 93%)
-                const float r = __fsub_rn(__fadd_rn(t, 12582912.0f), 12582912.0f);
-                t = t - r;
-                float s, c;
-                __sincosf(two_pi * t, &s, &c);
-                qr = fmaf(sph[k], c, qr);
-                qi = fmaf(sph[k], s, qi);
+                const float4 q = sk[k];
+                const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
+                float sn, cs;
+                __sincosf(t, &sn, &cs);
+                qr = fmaf(q.w, cs, qr);
+                qi = fmaf(q.w, sn, qi);
             }
         }
         if (live) {
