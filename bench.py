@@ -43,7 +43,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kernelet", choices=["kernelet", "reference"])
-    ap.add_argument("--instances", type=int, default=4, help="instances of each ALL-mix kernel per GPU")
+    ap.add_argument("--instances", type=int, default=4, help="instances of each ALL-mix kernel per GPU (c2)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2: ALL mix x4 per GPU (configs[1], default); c4: 1000 random kernels per GPU; "
+                         "c5: 10,000-kernel multi-user queue over all GPUs")
     ap.add_argument("--size", default="paper", choices=["paper", "small"])
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -146,12 +149,24 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------------------------
-def build_queue(rank: int, world: int, instances: int) -> list[str]:
-    """Global queue of 32*world kernels (instances x ALL per GPU), sharded round robin so every
-    GPU keeps the mix."""
+def global_queue(workload: str, instances: int, world: int) -> list[str]:
+    """c2 (configs[1]): ALL mix, `instances` of each kernel per GPU, round-robin arrivals.
+    c4 (configs[3]): 1000 kernels per GPU drawn uniformly from ALL (seed 42).
+    c5 (configs[4]): 10,000-kernel multi-user queue (16 Poisson users on CI/MI/MIX/ALL), the
+    whole queue shared by all GPUs (strong scaling)."""
+    if workload == "c2":
+        return [e["kind"] for e in G.queue("ALL", len(ALL) * instances * world, order="round_robin")]
+    if workload == "c4":
+        return [e["kind"] for e in G.queue("ALL", 1000 * world, seed=42, order="uniform")]
+    if workload == "c5":
+        return [e["kind"] for e in G.multi_user_queue(10000, 16, seed=7)]
+    raise ValueError(workload)
+
+
+def build_queue(rank: int, world: int, instances: int, workload: str = "c2") -> list[str]:
+    """This GPU's shard of the global queue, mix-preserving round robin."""
     from paper_1303_5164_b200.dist import shard
-    gq = [e["kind"] for e in G.queue("ALL", len(ALL) * instances * world, order="round_robin")]
-    return shard(gq, rank, world)
+    return shard(global_queue(workload, instances, world), rank, world)
 
 
 MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")
@@ -178,12 +193,25 @@ def run_kernelet(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     K.lib()
-    kinds = build_queue(rank, world, args.instances)
+    kinds = build_queue(rank, world, args.instances, args.workload)
     profiles, kcfg = load_profiles(args.profile)
     t_gen = time.time()
     data = {k: G.gen(k, args.size) for k in sorted(set(kinds))}
     inputs = {k: inputs_to_device(data[k], dev) for k in data}
-    insts = [Instance(data[k], dev, inputs=inputs[k]) for k in kinds]
+    # output leases: a pool of POOL output sets per kind, instance j of a kind writes set j % POOL
+    # (inputs are shared read-only); the trace check below proves no two launches that were
+    # resident at the same time wrote the same set
+    from paper_1303_5164_b200.workload import alloc_outputs
+    POOL = 4
+    pools, seen, lease = {}, {}, []
+    insts = []
+    for k in kinds:
+        j = seen.get(k, 0)
+        seen[k] = j + 1
+        if j < POOL:
+            pools.setdefault(k, []).append(alloc_outputs(k, data[k]["params"], dev))
+        insts.append(Instance(data[k], dev, inputs=inputs[k], outputs=pools[k][j % POOL]))
+        lease.append((k, j % POOL))
     t_gen = time.time() - t_gen
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
     lane_a = torch.cuda.Stream(device=dev)
@@ -224,6 +252,7 @@ def run_kernelet(args, rank, world, local_rank):
     n_trace0 = len(ctx.trace())
 
     step_ms, dev_ms, cnts = [], [], []
+    dec0 = ctx.stats().decisions
     with Clocks(local_rank) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -239,7 +268,9 @@ def run_kernelet(args, rank, world, local_rank):
             cnts.append(c)
         barrier()
     trace = ctx.trace()[n_trace0:]
+    st = ctx.stats()
     launches = len(trace) + 2 * args.steps      # lane launches + model batch + ctl init per step
+    lease_conflicts = check_leases(trace, ids, lease)
     t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -254,11 +285,14 @@ def run_kernelet(args, rank, world, local_rank):
         "value": len(insts) * world * args.steps / (total_ms / 1e3),
         "ms_per_step": total_ms / args.steps,
         "device_ms_per_step": statistics.median(dev_ms),
-        "phases_per_step": c_last.phases,
+        "phases_per_step": (ctx.stats().decisions - dec0) / args.steps,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "parity": parity,
         "setup_s": round(t_gen, 1),
+        "lease_conflicts": lease_conflicts,
+        "host_decide_ms_per_step": st.decide_ns / 1e6 / max(1, args.warmup + args.steps),
+        "model_ms_per_step": st.model_ns / 1e6 / max(1, args.warmup + args.steps),
     }
     phase_kinds = [(K.KINDS[tr.kind], tr.cap, K.KINDS[tr.partner_kind] if tr.partner_kind >= 0 else None)
                    for tr in trace[: max(1, len(trace) // args.steps)]]
@@ -270,6 +304,23 @@ def run_kernelet(args, rank, world, local_rank):
         res["per_kernel"] = per_kernel(ctx, insts, data, dev, flush, barrier)
     ctx.close()
     return res
+
+
+def check_leases(trace, ids, lease) -> int:
+    """Launches of different instances that share an output set must never be resident at the
+    same time (per-launch [t0, t1] from the device records)."""
+    owner = {kid: lease[n] for n, kid in enumerate(ids)}
+    spans = {}
+    for t in trace:
+        if t.id in owner and t.admitted:
+            spans.setdefault(owner[t.id], []).append((t.t0_ns, t.t1_ns, t.id))
+    bad = 0
+    for v in spans.values():
+        v.sort()
+        for (a0, a1, ia), (b0, b1, ib) in zip(v, v[1:]):
+            if ia != ib and b0 < a1:
+                bad += 1
+    return bad
 
 
 def sample_parity(insts, data, per_kind: int = 64) -> dict:
@@ -480,8 +531,12 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    config = {"workload": f"ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels, "
-                          f"{args.size} sizes, all pending at t=0)", "global_kernels": len(ALL) * args.instances * world,
+    n_global = len(global_queue(args.workload, args.instances, world))
+    wl_name = {"c2": f"ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels, {args.size} sizes, "
+                     "all pending at t=0)",
+               "c4": f"1000 kernels per GPU uniform over ALL (seed 42), {args.size} sizes",
+               "c5": f"10,000-kernel multi-user queue (16 Poisson users, CI/MI/MIX/ALL), {args.size} sizes"}[args.workload]
+    config = {"workload": wl_name, "global_kernels": n_global,
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
@@ -490,7 +545,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        kinds = build_queue(0, 1, args.instances)
+        kinds = build_queue(0, 1, args.instances, args.workload)
         leg = OracleLeg(kinds, args.size)
         vals = []
         for s in range(args.warmup + args.steps):
@@ -499,7 +554,7 @@ def main():
                 vals.append(r["value"])
         v = statistics.median(vals)
         line = {"metric": METRIC, "value": v, "unit": "kernels/s", "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
                 "vs_baseline": None, "dtype": "f32/f64/u32 (per kernel)", "data": "synthetic", "config": config,
                 "cpu_baseline": {**r, "value": v}, "e2e": {"value": v, "unit": "kernels/s", "h2d_bytes_per_step": 0,
                                                           "d2h_bytes_per_step": 0}}
@@ -535,21 +590,24 @@ def main():
                 a = v["ops"] / (v["ms"] / 1e3)
                 roof_all[k] = {"bound": "alu", "achieved": a / 1e12, "peak": pk_ / 1e12, "unit": f"T{what}",
                                "frac": a / pk_, "ms": v["ms"]}
-        dom = max(pk, key=lambda k: pk[k]["ms"] * sum(1 for x in build_queue(0, 1, args.instances) if x == k)) if pk else None
+        qk = build_queue(0, 1, args.instances, args.workload)
+        dom = max(pk, key=lambda k: pk[k]["ms"] * sum(1 for x in qk if x == k)) if pk else None
         roof = dict(roof_all[dom], kernel=dom, traffic=None) if dom else None
         line = {"metric": METRIC, "value": res["value"], "unit": "kernels/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32/bf16->f32/u32/u8 (per kernel); model f64",
+                "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f32/bf16->f32/u32/u8 (per kernel); model f64",
                 "data": "synthetic", "config": config, "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
                 "e2e": res.get("e2e"), "roofline": roof,
                 "speedup_vs_sequential": res["value"] / world / seq if seq else None,
                 "speedup_vs_multistream": res["value"] / world / ms4 if ms4 else None,
                 "baselines": bl, "roofline_all": roof_all, "device_ms_per_step": res["device_ms_per_step"],
                 "phases_per_step": res["phases_per_step"], "parity": res["parity"],
+                "lease_conflicts": res["lease_conflicts"], "host_decide_ms_per_step": res["host_decide_ms_per_step"],
+                "model_ms_per_step": res["model_ms_per_step"],
                 "schedule_first_step": res["schedule_first_step"]}
         if not args.no_cpu and world == 1:
             try:
-                line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances), args.size)
+                line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances, args.workload), args.size)
             except Exception as e:      # never lose the GPU line to the CPU leg
                 line["cpu_baseline"] = {"error": repr(e)[:300]}
         print(json.dumps(line))

@@ -147,12 +147,58 @@ struct BodySPMV {
     }
 };
 
-// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block.  Issue-lean
-// (ncu showed the first version issue-bound at 40 instructions per point): boundary columns are
-// a plain copy; an interior column walks z with one base pointer, a 3-plane register window and
-// the four x/y neighbours at fixed offsets, 4 planes per group so their loads are in flight
-// together.  Operand order is fixed: ((((z- + z+) + y-) + y+) + x-) + x+, then
-// fmaf(c1, s, -(c0 * in)).
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block.  Operand order
+// is fixed everywhere: ((((z- + z+) + y-) + y+) + x-) + x+, then fmaf(c1, s, -(c0 * in)).
+// Fast path (the paper's 512 x 512 planes, interior bricks): compile-time strides make every
+// neighbour an immediate offset of one pointer; the centre column is streamed 8 planes ahead
+// (software-pipelined register window) so each thread keeps 8 HBM loads in flight while the
+// x/y neighbours of the same planes hit L1.  Any other shape / boundary brick: generic path.
+__device__ __forceinline__ float st_point(float zm, float zp, float ym, float yp, float xm, float xp,
+                                          float c, float c0, float c1) {
+    float s = zm + zp;
+    s = s + ym;
+    s = s + yp;
+    s = s + xm;
+    s = s + xp;
+    return fmaf(c1, s, -(c0 * c));
+}
+
+template <int NX, int NY>
+__device__ __forceinline__ void st_fast(const float* __restrict__ p, float* __restrict__ o, float c0, float c1) {
+    constexpr int SZ = NX * NY;
+    float w[10];                          // planes z-1 .. z+8 of this column
+    w[0] = __ldg(p - SZ);
+    w[1] = __ldg(p);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u + 2] = __ldg(p + (u + 1) * SZ);
+#pragma unroll 1
+    for (int g = 0; g < 8; ++g) {
+        float nw[8];
+        if (g < 7) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nw[u] = __ldg(p + (u + 9) * SZ);   // next group, 8 ahead
+        }
+        float ym[8], yp[8], xm[8], xp[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            ym[u] = __ldg(p + u * SZ - NX);
+            yp[u] = __ldg(p + u * SZ + NX);
+            xm[u] = __ldg(p + u * SZ - 1);
+            xp[u] = __ldg(p + u * SZ + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u * SZ] = st_point(w[u], w[u + 2], ym[u], yp[u], xm[u], xp[u], w[u + 1], c0, c1);
+        w[0] = w[8];
+        w[1] = w[9];
+        if (g < 7) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u + 2] = nw[u];
+        }
+        p += 8 * SZ;
+        o += 8 * SZ;
+    }
+}
+
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
@@ -167,61 +213,24 @@ struct BodyST {
         if (x >= nx || y >= ny) return;
         const int z0 = bz * 64, z1 = min(z0 + 64, nz);
         const size_t sz = (size_t)nx * ny;
-        const float* pin = a.in + (size_t)z0 * sz + (size_t)y * nx + x;
-        float* pout = a.out + (size_t)z0 * sz + (size_t)y * nx + x;
-        if (!(x > 0 && x < nx - 1 && y > 0 && y < ny - 1)) {   // boundary column: out = in
-            for (int z = z0; z < z1; ++z, pin += sz, pout += sz) *pout = __ldg(pin);
+        const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
+        const size_t col = (size_t)y * nx + x;
+        if (nx == 512 && ny == 512 && ixy && z0 > 0 && z0 + 64 + 8 < nz) {
+            st_fast<512, 512>(a.in + (size_t)z0 * sz + col, a.out + (size_t)z0 * sz + col, a.c0, a.c1);
             return;
         }
-        const float c0 = a.c0, c1 = a.c1;
-        float zm = z0 > 0 ? __ldg(pin - sz) : 0.f;
-        float c = __ldg(pin);
-        int z = z0;
-        for (; z + 4 <= z1; z += 4, pin += 4 * sz, pout += 4 * sz) {
-            float v[4], ym[4], yp[4], xm[4], xp[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float* q = pin + u * sz;
-                v[u] = (z + u + 1 < nz) ? __ldg(q + sz) : 0.f;   // plane z+u+1 (z+ of point u)
-                ym[u] = __ldg(q - nx);
-                yp[u] = __ldg(q + nx);
-                xm[u] = __ldg(q - 1);
-                xp[u] = __ldg(q + 1);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int zc = z + u;
-                const float zp = v[u];
-                float r;
-                if (zc == 0 || zc == nz - 1) {
-                    r = c;
-                } else {
-                    float s2 = zm + zp;
-                    s2 = s2 + ym[u];
-                    s2 = s2 + yp[u];
-                    s2 = s2 + xm[u];
-                    s2 = s2 + xp[u];
-                    r = fmaf(c1, s2, -(c0 * c));
-                }
-                pout[u * sz] = r;
-                zm = c;
-                c = zp;
-            }
-        }
-        for (; z < z1; ++z, pin += sz, pout += sz) {            // ragged z tail
-            const float zp = (z + 1 < nz) ? __ldg(pin + sz) : 0.f;
-            float r;
-            if (z == 0 || z == nz - 1) {
-                r = c;
+        const float* in = a.in;
+        size_t f = (size_t)z0 * sz + col;
+        float zm = z0 > 0 ? __ldg(in + f - sz) : 0.f;
+        float c = __ldg(in + f);
+        for (int z = z0; z < z1; ++z, f += sz) {
+            const float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
+            if (!ixy || z == 0 || z == nz - 1) {
+                a.out[f] = c;
             } else {
-                float s2 = zm + zp;
-                s2 = s2 + __ldg(pin - nx);
-                s2 = s2 + __ldg(pin + nx);
-                s2 = s2 + __ldg(pin - 1);
-                s2 = s2 + __ldg(pin + 1);
-                r = fmaf(c1, s2, -(c0 * c));
+                a.out[f] = st_point(zm, zp, __ldg(in + f - nx), __ldg(in + f + nx), __ldg(in + f - 1),
+                                    __ldg(in + f + 1), c, a.c0, a.c1);
             }
-            *pout = r;
             zm = c;
             c = zp;
         }
