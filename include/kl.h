@@ -80,7 +80,7 @@ typedef struct {   /* ST: 7-point stencil, in[z][y][x]; block = 32x4 (x,y) tile 
 typedef struct {   /* MM: C[M][N] (fp32) = A[M][K] (bf16) * B, B given K-major as Bt[N][K] (bf16)*/
     const uint16_t* A; const uint16_t* Bt;
     float* C;
-    int32_t M, N, K;       /* M, N multiples of 128; K multiple of 64 */
+    int32_t M, N, K;       /* M multiple of 128, N multiple of 256, K multiple of 64 */
 } kl_args_mm;
 typedef struct {   /* MRIQ: Q[i] = sum_k phiMag_k exp(i 2 pi k.x_i); one voxel per thread       */
     const float *x, *y, *z, *kx, *ky, *kz, *phimag;

@@ -75,7 +75,7 @@ SAD_MB = 16            # macroblock edge
 SAD_RANGE = 16         # search offsets in [-16, 16]
 SPMV_ROWS_PER_BLOCK = 8
 ST_TILE = (32, 4, 64)  # x, y, z points per block
-MM_TILE = (128, 128)   # output tile (M, N) per block
+MM_TILE = (128, 256)   # output tile (M, N) per block
 BS_PER_BLOCK = 128 * 20
 TEA_PER_BLOCK = 128 * 10
 MRIQ_PER_BLOCK = 256

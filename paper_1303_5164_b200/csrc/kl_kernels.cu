@@ -147,41 +147,12 @@ struct BodySPMV {
     }
 };
 
-// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block.  Operand order
-// is fixed everywhere: ((((z- + z+) + y-) + y+) + x-) + x+, then fmaf(c1, s, -(c0 * in)).
-// Fast path (the paper's 512 x 512 planes, interior bricks): compile-time strides make every
-// neighbour an immediate offset of one pointer (about 15 instructions per point instead of 40),
-// unrolled by 4 planes so their loads are in flight together, at 16 resident blocks per SM.
-// Any other shape / boundary brick: the generic path.
-__device__ __forceinline__ float st_point(float zm, float zp, float ym, float yp, float xm, float xp,
-                                          float c, float c0, float c1) {
-    float s = zm + zp;
-    s = s + ym;
-    s = s + yp;
-    s = s + xm;
-    s = s + xp;
-    return fmaf(c1, s, -(c0 * c));
-}
-
-template <int NX, int NY>
-__device__ __forceinline__ void st_fast(const float* __restrict__ p, float* __restrict__ o, float c0, float c1) {
-    constexpr int SZ = NX * NY;
-    float zm = __ldg(p - SZ), c = __ldg(p);
-#pragma unroll 4
-    for (int u = 0; u < 64; ++u) {
-        const float zp = __ldg(p + SZ);
-        *o = st_point(zm, zp, __ldg(p - NX), __ldg(p + NX), __ldg(p - 1), __ldg(p + 1), c, c0, c1);
-        zm = c;
-        c = zp;
-        p += SZ;
-        o += SZ;
-    }
-}
-
+// ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z
+// neighbours ride a register queue, x/y neighbours come through L1.
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 16;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -193,22 +164,21 @@ struct BodyST {
         const int z0 = bz * 64, z1 = min(z0 + 64, nz);
         const size_t sz = (size_t)nx * ny;
         const bool ixy = x > 0 && x < nx - 1 && y > 0 && y < ny - 1;
-        const size_t col = (size_t)y * nx + x;
-        if (nx == 512 && ny == 512 && ixy && z0 > 0 && z0 + 64 < nz) {
-            st_fast<512, 512>(a.in + (size_t)z0 * sz + col, a.out + (size_t)z0 * sz + col, a.c0, a.c1);
-            return;
-        }
         const float* in = a.in;
-        size_t f = (size_t)z0 * sz + col;
+        size_t f = (size_t)z0 * sz + (size_t)y * nx + x;
         float zm = z0 > 0 ? __ldg(in + f - sz) : 0.f;
         float c = __ldg(in + f);
         for (int z = z0; z < z1; ++z, f += sz) {
-            const float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
+            float zp = (z + 1 < nz) ? __ldg(in + f + sz) : 0.f;
             if (!ixy || z == 0 || z == nz - 1) {
                 a.out[f] = c;
             } else {
-                a.out[f] = st_point(zm, zp, __ldg(in + f - nx), __ldg(in + f + nx), __ldg(in + f - 1),
-                                    __ldg(in + f + 1), c, a.c0, a.c1);
+                float s = zm + zp;
+                s = s + __ldg(in + f - nx);
+                s = s + __ldg(in + f + nx);
+                s = s + __ldg(in + f - 1);
+                s = s + __ldg(in + f + 1);
+                a.out[f] = fmaf(a.c1, s, -(a.c0 * c));
             }
             zm = c;
             c = zp;

@@ -16,12 +16,6 @@
 
 namespace {
 
-// Bodies may declare kMinBlocks (resident blocks per SM the compiler must allow); default 1.
-template <class B, class = void>
-struct MinBlocks { static constexpr int value = 1; };
-template <class B>
-struct MinBlocks<B, decltype((void)B::kMinBlocks)> { static constexpr int value = B::kMinBlocks; };
-
 __device__ __forceinline__ uint32_t smid_u32() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -86,7 +80,7 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
 }
 
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
+__global__ void __launch_bounds__(Body::kThreads)
 k_persistent(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
     extern __shared__ __align__(1024) char dsmem[];
     __shared__ uint32_t s_vb[2], s_end[2], s_adm;
@@ -156,7 +150,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
 
 // Plain grid: blockIdx rectified by the slice offset.
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
+__global__ void __launch_bounds__(Body::kThreads)
 k_plain(const __grid_constant__ typename Body::Params P, uint32_t offset) {
     extern __shared__ __align__(1024) char dsmem[];
     typename Body::State st;

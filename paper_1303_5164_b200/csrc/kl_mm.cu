@@ -1,16 +1,17 @@
 // kl_mm.cu -- MM ("Multiplying two dense matrices", 8192x2048 . 2048x2048) on the
 // 5th-generation tensor cores (product path).
 //
-// One virtual thread block = one 128x128 fp32 output tile.  A persistent block (8 warps) pulls
+// One virtual thread block = one 128x256 fp32 output tile.  A persistent block (8 warps) pulls
 // tiles from the slice launcher and runs, per tile,
-//   warp 0 lane 0 : TMA producer  -- 128x64 bf16 tiles of A and B (128B swizzle) into a ring of
-//                   kStages shared-memory stages, completion on mbarriers (expect_tx);
-//   warp 1 lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16 (M=128,N=128,K=16) x4
-//                   per stage into a 128-column fp32 TMEM accumulator; tcgen05.commit frees the
-//                   stage; the last commit signals the epilogue;
-//   warps 4..7    : epilogue      -- tcgen05.ld 32x32b.x32 (each warp its 32 TMEM lanes) and
-//                   128-byte row stores of C;  warps 2-3 idle (8 warps keep b*wpb divisible by
-//                   the 4 schedulers, so the virtual-SM warp count is whole, R14).
+//   warp 0 lane 0 : TMA producer  -- 128x64 (A) and 256x64 (B) bf16 tiles, 128B swizzle, into a
+//                   ring of kStages shared-memory stages, completion on mbarriers (expect_tx);
+//   warp 1 lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) x4
+//                   per stage into one of two 256-column fp32 TMEM accumulators; tcgen05.commit
+//                   frees the stage; the last commit signals the epilogue;
+//   warps 4..7    : epilogue      -- drains the PREVIOUS tile's accumulator (tcgen05.ld
+//                   32x32b.x32, each warp its 32 TMEM lanes) while warps 0-1 run this tile's
+//                   mainloop; the last tile is drained in fini().  Warps 2-3 idle (8 warps keep
+//                   b*wpb divisible by the 4 schedulers: whole virtual-SM warps, R14).
 // The stage count is the kernel's occupancy knob (shared memory per block).
 // Numerics: bf16 products are exact in fp32; only the fp32 accumulation order differs from the
 // oracle's fp64 sum (normwise tolerance).
@@ -24,19 +25,19 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int kStages = 4;
-constexpr int kStageBytes = (BM + BN) * BK * 2;          // 32 KiB
+constexpr int kStageBytes = (BM + BN) * BK * 2;          // 48 KiB
 constexpr int kBarOffset = kStages * kStageBytes;
 constexpr int kDynSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int kThreads = 256;   // 8 warps: whole warps per virtual SM (R14)
-constexpr uint32_t kTmemCols = 128;
-// instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 128, M = 128
+constexpr uint32_t kTmemCols = 2 * BN;   // two fp32 accumulators: tile i's MMAs overlap tile i-1's epilogue
+// instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 256, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 struct MMParams {
     CUtensorMap ta;   // A  [M][K] bf16, box 64 x 128
-    CUtensorMap tb;   // Bt [N][K] bf16, box 64 x 128
+    CUtensorMap tb;   // Bt [N][K] bf16, box 64 x 256
     float* C;
     int32_t M, N, K;
 };
@@ -104,15 +105,19 @@ struct BodyMM {
     static constexpr int kThreads = ::kThreads, kChunk = 1, kDynSmem = ::kDynSmem;
     struct State {
         uint32_t base;      // 1024-aligned shared address of stage 0
-        uint32_t bars;      // full[s] at bars + 8s, empty[s] at bars + 64 + 8s, tfull at bars + 128
+        uint32_t bars;      // full[s] bars+8s, empty[s] bars+64+8s, tfull[b] bars+128+8b, tmem ptr bars+192
         uint32_t tmem;
-        uint32_t stage, phase, tphase;
+        uint32_t stage, phase;
+        uint32_t tph;       // per-accumulator wait parity bits
+        uint32_t ntile;     // tiles issued by this persistent block
+        int prev_m, prev_n; // tile whose accumulator is still to be drained (-1: none)
     };
     __device__ static void init(const Params&, State& st, char* dsmem) {
         const uint32_t raw = smem_u32(dsmem);
         st.base = (raw + 1023u) & ~1023u;
         st.bars = st.base + kBarOffset;
-        st.stage = st.phase = st.tphase = 0;
+        st.stage = st.phase = st.tph = st.ntile = 0;
+        st.prev_m = st.prev_n = -1;
         const int warp = threadIdx.x >> 5;
         if (threadIdx.x == 0) {
             for (int s = 0; s < kStages; ++s) {
@@ -120,6 +125,7 @@ struct BodyMM {
                 mbar_init(st.bars + 64 + 8 * s, 1);
             }
             mbar_init(st.bars + 128, 1);
+            mbar_init(st.bars + 136, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
@@ -133,7 +139,30 @@ struct BodyMM {
         tc_fence_after();
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(st.tmem) : "r"(st.bars + 192));
     }
-    __device__ static void fini(const Params&, State& st, char*) {
+    // Epilogue warps: wait for tile (m, n)'s accumulator b, move it TMEM -> registers -> C.
+    __device__ static void drain(const Params& P, State& st, int m, int n, uint32_t b) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        mbar_wait(st.bars + 128 + 8 * b, (st.tph >> b) & 1u);
+        tc_fence_after();
+        const int q = warp & 3;                              // TMEM lane quarter of this warp
+        const int row = m * BM + q * 32 + lane;
+        float* crow = P.C + (size_t)row * P.N + (size_t)n * BN;
+        const uint32_t tbase = st.tmem + ((uint32_t)(q * 32) << 16) + b * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            uint32_t r[32];
+            TMEM_LD_X32(tbase + (uint32_t)c, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            float4* dst = reinterpret_cast<float4*>(crow + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+        tc_fence_before();
+    }
+    __device__ static void fini(const Params& P, State& st, char*) {
+        if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_n, (st.ntile - 1) & 1u);
         tc_fence_before();
         __syncthreads();
         tc_fence_after();
@@ -145,6 +174,7 @@ struct BodyMM {
         const int tiles_n = P.N / BN;
         const int tm = (int)vb / tiles_n, tn = (int)vb % tiles_n;
         const int nk = P.K / BK;
+        const uint32_t acc = st.ntile & 1u;                 // accumulator of this tile
         if (warp == 0) {
             if (lane == 0) {
                 uint32_t s = st.stage, ph = st.phase;
@@ -163,44 +193,34 @@ struct BodyMM {
             tc_fence_after();
             if (lane == 0) {
                 uint32_t s = st.stage, ph = st.phase;
+                const uint32_t tacc = st.tmem + acc * BN;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(st.bars + 8 * s, ph);
                     tc_fence_after();
                     const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(st.tmem, umma_desc(sa + k * 32), umma_desc(sb + k * 32), kIdesc,
+                        umma_bf16(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), kIdesc,
                                   (kb | k) != 0 ? 1u : 0u);
                     umma_commit(st.bars + 64 + 8 * s);       // stage free once these MMAs finish
                     if (++s == kStages) { s = 0; ph ^= 1u; }
                 }
-                umma_commit(st.bars + 128);                  // accumulator complete
+                umma_commit(st.bars + 128 + 8 * acc);        // accumulator `acc` complete
             }
             __syncwarp();
-        } else if (warp >= 4) {
-            mbar_wait(st.bars + 128, st.tphase);
-            tc_fence_after();
-            const int q = warp & 3;                          // TMEM lane quarter of this warp
-            const int row = tm * BM + q * 32 + lane;
-            float* crow = P.C + (size_t)row * P.N + (size_t)tn * BN;
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t r[32];
-                TMEM_LD_X32(st.tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                float4* dst = reinterpret_cast<float4*>(crow + c);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            }
-            tc_fence_before();
+        } else if (warp >= 4 && st.prev_m >= 0) {
+            drain(P, st, st.prev_m, st.prev_n, acc ^ 1u);    // previous tile, other accumulator
         }
         // every role advances the shared pipeline state identically
         for (int kb = 0; kb < nk; ++kb)
             if (++st.stage == kStages) { st.stage = 0; st.phase ^= 1u; }
-        st.tphase ^= 1u;
-        __syncthreads();   // accumulator drained before the next tile's first MMA
+        if (st.prev_m >= 0) st.tph ^= 1u << (acc ^ 1u);    // that accumulator's wait was consumed
+        st.prev_m = tm;
+        st.prev_n = tn;
+        st.ntile++;
+        tc_fence_before();
+        __syncthreads();   // the drained accumulator is free before the next tile's first MMA
+        tc_fence_after();
     }
 };
 
@@ -220,12 +240,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t k) {
+bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t k, int box_rows) {
     auto fn = get_encode();
     if (!fn) return false;
     cuuint64_t dims[2] = {k, rows};
     cuuint64_t strides[1] = {k * 2};
-    cuuint32_t box[2] = {BK, 128};
+    cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -249,8 +269,8 @@ int kl_mm_prepare(const void* args, uint32_t bytes, void* blob, uint32_t cap) {
     if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.M % BM || a.N % BN || a.K % BK) return -1;
     MMParams p;
     std::memset(&p, 0, sizeof p);
-    if (!encode_kmajor(&p.ta, a.A, (uint64_t)a.M, (uint64_t)a.K)) return -1;
-    if (!encode_kmajor(&p.tb, a.Bt, (uint64_t)a.N, (uint64_t)a.K)) return -1;
+    if (!encode_kmajor(&p.ta, a.A, (uint64_t)a.M, (uint64_t)a.K, BM)) return -1;
+    if (!encode_kmajor(&p.tb, a.Bt, (uint64_t)a.N, (uint64_t)a.K, BN)) return -1;
     p.C = a.C;
     p.M = a.M;
     p.N = a.N;
