@@ -154,6 +154,14 @@ struct kl_ctx {
     KlDecision* dec_dev = nullptr;
     KlDecision* dec_pinned = nullptr;
     std::unordered_map<uint64_t, kl_prediction> cache;
+    // maximal occupancy splits per ordered kind pair (depend on the profiles only)
+    std::vector<std::pair<uint32_t, uint32_t>> splits[KL_NKINDS][KL_NKINDS];
+    bool splits_ok[KL_NKINDS][KL_NKINDS] = {};
+    void clear_caches() {
+        cache.clear();
+        for (auto& row : splits_ok)
+            for (auto& v : row) v = false;
+    }
     bool lookup(int k1, int k2, uint32_t b1, uint32_t b2, kl_prediction* out) const {
         auto it = cache.find(cache_key(k1, k2, b1, b2));
         if (it != cache.end()) { if (out) *out = it->second; return true; }
@@ -305,6 +313,14 @@ KlModelCfg model_cfg(const kl_ctx* c, int n) {
     return m;
 }
 
+const std::vector<std::pair<uint32_t, uint32_t>>& splits_of(kl_ctx* c, int k1, int k2) {
+    if (!c->splits_ok[k1][k2]) {
+        c->splits[k1][k2] = maximal_splits(c, c->prof[k1], c->prof[k2]);
+        c->splits_ok[k1][k2] = true;
+    }
+    return c->splits[k1][k2];
+}
+
 // Run the device model over cand_pinned[0..n); n_pairs > 0 fuses the selection.
 kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
@@ -371,7 +387,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     std::vector<std::pair<int, int>> pair_of_group;
     for (auto& pq : keep) {
         const int k1 = R[pq.first]->kind, k2 = R[pq.second]->kind;
-        auto ms = maximal_splits(ctx, ctx->prof[k1], ctx->prof[k2]);
+        const auto& ms = splits_of(ctx, k1, k2);
         if (ms.empty()) continue;
         ctx->off_pinned[np] = n;
         for (auto& s : ms) {
@@ -403,7 +419,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
         for (int a = 0; a < KL_NKINDS; ++a)
             for (int b = a; b < KL_NKINDS; ++b) {   // one order; the other is derived (swap_pred)
                 if (!have[a] || !have[b]) continue;
-                for (auto& sp : maximal_splits(ctx, ctx->prof[a], ctx->prof[b])) {
+                for (auto& sp : splits_of(ctx, a, b)) {
                     if (ctx->lookup(a, b, sp.first, sp.second, nullptr)) continue;
                     bool in_list = false;
                     for (int i = 0; i < n && !in_list; ++i) {
@@ -915,7 +931,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
         const kl_profile& p = *d->profile;
         if (!(p.rm >= 0.0 && p.rm <= 1.0)) return ctx->fail(KL_EINVAL, "Rm outside [0,1]");
         ctx->prof[d->kind] = p;
-        ctx->cache.clear();
+        ctx->clear_caches();
     }
     if (!ctx->host_only && !ctx->info_ok[d->kind]) return ctx->fail(KL_EINVAL, "kind %d not available in this build", d->kind);
     if (ctx->free_slots.empty()) return ctx->fail(KL_ENOMEM, "slice control pool exhausted");
@@ -1166,13 +1182,13 @@ kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p) {
     if (!q.m_min) q.m_min = cur.m_min;
     if (!(q.ipc_max > 0.0)) q.ipc_max = cur.ipc_max > 0.0 ? cur.ipc_max : 1.0;
     ctx->prof[kind] = q;
-    ctx->cache.clear();
+    ctx->clear_caches();
     return KL_OK;
 }
 
 kl_status kl_reset_model_cache(kl_ctx* ctx) {
     KL_LIVE(ctx);
-    ctx->cache.clear();
+    ctx->cache.clear();   // predictions only; the split tables depend on the profiles alone
     return KL_OK;
 }
 

@@ -1,0 +1,32 @@
+#!/bin/bash
+# Refresh every measured artefact on the GPU box (run under gpurun from the repo root).
+# Outputs land in gpurun_out/ (copied into profiles/ by hand after review).
+set -u
+mkdir -p gpurun_out
+echo "== gpu tests"; timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+echo "== calibrate"; timeout 900 python tools/calibrate.py run gpurun_out/kl_profile_b200.json > gpurun_out/calib.log 2>&1
+grep -E " fit |wrote" gpurun_out/calib.log | cut -c1-160
+cp gpurun_out/kl_profile_b200.json profiles/kl_profile_b200.json
+echo "== bench c2"; timeout 900 python bench.py --json-out gpurun_out/bench_c2.json > gpurun_out/bench_c2.log 2>&1
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/bench_c2.json"))
+print({k: d.get(k) for k in ("value", "ms_per_step", "device_ms_per_step", "speedup_vs_sequential",
+                             "speedup_vs_multistream", "clocks", "lease_conflicts", "host_decide_ms_per_step",
+                             "model_ms_per_step")})
+print("e2e", d["e2e"]["value"], "roofline", d["roofline"])
+PY
+echo "== bench c2 rule 0"; timeout 600 python bench.py --no-cpu --split-rule 0 --json-out gpurun_out/bench_c2_rule0.json > gpurun_out/bench_c2_rule0.log 2>&1
+python -c "import json;d=json.load(open('gpurun_out/bench_c2_rule0.json'));print(d['value'], d['ms_per_step'], d['speedup_vs_sequential'])"
+echo "== bench c4"; timeout 900 python bench.py --workload c4 --steps 3 --warmup 1 --no-cpu --json-out gpurun_out/bench_c4.json > gpurun_out/bench_c4.log 2>&1
+python -c "import json;d=json.load(open('gpurun_out/bench_c4.json'));print(d['value'], d['ms_per_step'], d['speedup_vs_sequential'], d['lease_conflicts'])"
+echo "== model error"; timeout 900 python tools/model_error.py gpurun_out/model_error.json > gpurun_out/model_error.log 2>&1
+python -c "import json;print(json.load(open('gpurun_out/model_error.json'))['summary'])" | cut -c1-300
+echo "== ncu launch list"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-baselines --no-cpu > gpurun_out/ncu_bench.log 2>&1
+echo "== ncu full"
+for k in MRIQ MM ST PC BS; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_plain -s 1 -c 1 -o gpurun_out/prof_$k python tools/prof_target.py $k plain > gpurun_out/ncu_full_$k.log 2>&1
+done
+python tools/ncu_summary.py gpurun_out/ncu_summary.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
+echo "== done"; ls gpurun_out
