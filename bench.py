@@ -56,6 +56,8 @@ def parse():
                     help="slice ratio per pair: 1 argmax CP over all co-schedules (FindCoSchedule l.3-4, "
                          "default), 0 argmin dT (Eq.8 balanced ratio)")
     ap.add_argument("--cp-min", type=float, default=None)
+    ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
+                                               "(tools/opt_table.py) instead of the Markov model")
     return ap.parse_args()
 
 
@@ -220,12 +222,18 @@ def run_kernelet(args, rank, world, local_rank):
     cfg["split_rule"] = args.split_rule
     if args.cp_min is not None:
         cfg["cp_min"] = args.cp_min
+    if args.opt:
+        cfg["model_frozen"] = 1
     ctx = K.Context(device=local_rank, profiles=profiles, streams=(lane_a, lane_b), counters=counters, **cfg)
+    if args.opt:   # the paper's OPT: the same greedy Alg.1 over pre-executed (measured) CP
+        tab = json.load(open(args.opt))["table"]
+        ctx.cache_put([((t["k1"], t["k2"], t["b1"], t["b2"]), t) for t in tab])
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126.5 MiB)
     gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev)
 
     def one_step():
-        ctx.reset_model_cache()
+        if not args.opt:
+            ctx.reset_model_cache()
         ctx.reset_counters()
         counters[5] = rank
         counters[6] = world
@@ -545,7 +553,7 @@ def main():
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
-              "cp_min": args.cp_min or 0.0}
+              "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model"}
 
     if args.impl == "reference":
         if rank != 0:

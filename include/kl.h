@@ -137,6 +137,7 @@ typedef struct {
     int32_t latency_mode;      /* 0 linear-in-requests (R2), 1 verbatim P:875 */
     int32_t level_mode;        /* 0: every b with b*wpb % n_sched == 0; 1: four levels (config C2) */
     int32_t split_rule;        /* slice ratio per pair: 0 argmin dT (Eq.8, the paper); 1 argmax CP */
+    int32_t model_frozen;      /* 1: decide from installed predictions only (OPT, kl_cache_put) */
     int32_t n_sms;             /* 0 = from the device */
     int32_t chunk;             /* virtual blocks per work fetch; 0 = per-kind default */
     int32_t audit;             /* 1: count executions per virtual block (coverage audit) */
@@ -234,6 +235,10 @@ kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, cons
 kl_status kl_get_profile(kl_ctx* ctx, kl_kind kind, kl_profile* out);
 kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p);   /* clears model cache */
 kl_status kl_reset_model_cache(kl_ctx* ctx);
+/* Install predictions for candidates (e.g. measured by pre-execution: the paper's OPT comparator,
+ * P:1232-1233) into the prediction cache; with config.model_frozen = 1 the device model is never
+ * run and a candidate without an installed prediction counts as infeasible. */
+kl_status kl_cache_put(kl_ctx* ctx, const kl_candidate* cands, const kl_prediction* preds, size_t n);
 kl_status kl_reset_counters(kl_ctx* ctx);        /* zero counters_dev (t_start = INT64_MAX) */
 kl_status kl_trace(kl_ctx* ctx, kl_trace_rec* out, size_t cap, size_t* n_out);
 /* Coverage audit (config.audit = 1): copy kernel `id`'s per-virtual-block execution counts

@@ -103,7 +103,7 @@ class Config(C.Structure):
     _fields_ = [("alpha_p", C.c_double), ("alpha_m", C.c_double), ("p_percent", C.c_double),
                 ("L0", C.c_double), ("B", C.c_double), ("a0", C.c_double), ("b0", C.c_double),
                 ("cp_min", C.c_double), ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
-                ("split_rule", C.c_int32),
+                ("split_rule", C.c_int32), ("model_frozen", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
                 ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
@@ -158,7 +158,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -197,6 +197,7 @@ def lib() -> C.CDLL:
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
     L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
+    L.kl_cache_put.argtypes = [_vp, P(Candidate), P(Prediction), C.c_size_t]
     L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
     for s in ABI_SYMBOLS:
         if s not in ("kl_abi_version", "kl_last_error", "kl_struct_sizes"):
@@ -361,6 +362,17 @@ class Context:
     def set_profile(self, kind, prof) -> None:
         p = profile_from_dict(prof) if isinstance(prof, dict) else prof
         self._check(self._L.kl_set_profile(self._h, KIND_ID[kind] if isinstance(kind, str) else kind, C.byref(p)))
+
+    def cache_put(self, items):
+        """items: [((k1, k2, b1, b2), {ipc1, ipc2, c, solo1, solo2, cp, dT, status})]"""
+        n = len(items)
+        ca = (Candidate * max(n, 1))()
+        pr = (Prediction * max(n, 1))()
+        for i, ((k1, k2, b1, b2), d) in enumerate(items):
+            ca[i] = Candidate(KIND_ID[k1] if isinstance(k1, str) else k1, KIND_ID[k2] if isinstance(k2, str) else k2, b1, b2)
+            for f in ("ipc1", "ipc2", "c", "solo1", "solo2", "cp", "dT", "status"):
+                setattr(pr[i], f, d.get(f, 0))
+        self._check(self._L.kl_cache_put(self._h, ca, pr, n))
 
     def reset_model_cache(self):
         self._check(self._L.kl_reset_model_cache(self._h))

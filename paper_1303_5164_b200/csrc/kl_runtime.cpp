@@ -409,7 +409,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     d->n_cand = n;
     int best = -1;
     double bcp = 0.0;
-    if (n > 0 && missing) {
+    if (n > 0 && missing && !ctx->cfg.model_frozen) {
         if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context cannot run the model");
         // one batch also covers every other pair of the pending kinds (unpruned, pair = -1), so
         // the later decisions of this queue are cache hits instead of mid-queue model batches
@@ -452,7 +452,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             for (int i = ctx->off_pinned[p]; i < ctx->off_pinned[p + 1]; ++i) {
                 const KlCand& cd = ctx->cand_pinned[i];
                 kl_prediction a{};
-                ctx->lookup(cd.k1, cd.k2, cd.b1, cd.b2, &a);
+                if (!ctx->lookup(cd.k1, cd.k2, cd.b1, cd.b2, &a)) a.status = KL_EINFEASIBLE;   // frozen, not installed
                 if (a.status != 0) continue;
                 if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
             }
@@ -1183,6 +1183,16 @@ kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p) {
     if (!(q.ipc_max > 0.0)) q.ipc_max = cur.ipc_max > 0.0 ? cur.ipc_max : 1.0;
     ctx->prof[kind] = q;
     ctx->clear_caches();
+    return KL_OK;
+}
+
+kl_status kl_cache_put(kl_ctx* ctx, const kl_candidate* c, const kl_prediction* p, size_t n) {
+    KL_LIVE(ctx);
+    if (n && (!c || !p)) return KL_EINVAL;
+    for (size_t i = 0; i < n; ++i) {
+        if (c[i].k1 < 0 || c[i].k1 >= KL_NKINDS || c[i].k2 < 0 || c[i].k2 >= KL_NKINDS) return KL_EINVAL;
+        ctx->cache[cache_key(c[i].k1, c[i].k2, c[i].b1, c[i].b2)] = p[i];
+    }
     return KL_OK;
 }
 
