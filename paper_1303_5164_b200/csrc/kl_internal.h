@@ -42,6 +42,9 @@ struct KlCtl {
     uint32_t executed;    // virtual blocks executed in the current launch
     uint32_t base;        // first virtual block of the current launch (slice boundaries)
     unsigned long long t0;  // earliest admitted-block start (globaltimer ns), current launch
+    // host stop request, written by the copy engine (no SM needed): bit 0 valid, bits [1,8) epoch
+    // of the launch to stop, bits [32,64) slice size; the next fetching block performs the stop
+    volatile unsigned long long stop_req;
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
 };
@@ -118,8 +121,10 @@ struct KlDecision {
 };
 // Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
 int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream);
-// Stop the current launch (epoch `epoch`) of a kernel at its next slice boundary.
-int kl_dev_stop(KlCtl* ctl, uint32_t epoch, uint32_t slice, void* stream);
+// Stop request encoding (see KlCtl::stop_req).
+KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
+    return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)slice << 32);
+}
 
 // Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy
 // selection (a9) and writes *dec.  `done_counter` must be zero on entry (reset by the kernel).

@@ -419,6 +419,7 @@ __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n) {
         c->executed = 0;
         c->base = 0;
         c->t0 = ~0ull;
+        c->stop_req = 0ull;
     }
 }
 
@@ -428,27 +429,3 @@ int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream
     return (int)cudaGetLastError();
 }
 
-// Host-requested stop (Alg.1 re-plan): CAS the stop bit with stop_at = the first slice boundary
-// at or after `next`, at least one slice past the launch's first block; ignored if the launch
-// already stopped or the word belongs to another launch (epoch mismatch).
-__global__ void k_stop(KlCtl* ctl, uint32_t epoch, uint32_t slice) {
-    unsigned long long old = atomicAdd(&ctl->word, 0ull);
-    const uint32_t sl = slice ? slice : 1u;
-    for (;;) {
-        if ((old & KL_W_STOP) || kl_w_epoch(old) != (epoch & 0x7fu)) return;
-        const uint32_t nx = kl_w_next(old), base = ctl->base;
-        unsigned long long n_sl = nx > base ? ((unsigned long long)(nx - base) + sl - 1) / sl : 0ull;
-        if (n_sl == 0) n_sl = 1;
-        unsigned long long sa = (unsigned long long)base + n_sl * sl;
-        if (sa > KL_W_MASK28) sa = KL_W_MASK28;
-        const unsigned long long nw = kl_w_make(nx, (uint32_t)sa, kl_w_epoch(old), true);
-        const unsigned long long prev = atomicCAS(&ctl->word, old, nw);
-        if (prev == old) return;
-        old = prev;
-    }
-}
-
-int kl_dev_stop(KlCtl* ctl, uint32_t epoch, uint32_t slice, void* stream) {
-    k_stop<<<1, 1, 0, (cudaStream_t)stream>>>(ctl, epoch, slice);
-    return (int)cudaGetLastError();
-}

@@ -27,6 +27,25 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// Stop the launch of epoch `epoch` at the first slice boundary at or after `next`, at least one
+// slice past its first block; no-op if already stopped or the word belongs to another launch.
+__device__ void stop_word(KlCtl* ctl, uint32_t epoch, uint32_t slice) {
+    unsigned long long old = atomicAdd(&ctl->word, 0ull);
+    const uint32_t sl = slice ? slice : 1u;
+    for (;;) {
+        if ((old & KL_W_STOP) || kl_w_epoch(old) != (epoch & 0x7fu)) return;
+        const uint32_t nx = kl_w_next(old), base = ctl->base;
+        unsigned long long n_sl = nx > base ? ((unsigned long long)(nx - base) + sl - 1) / sl : 0ull;
+        if (n_sl == 0) n_sl = 1;
+        unsigned long long sa = (unsigned long long)base + n_sl * sl;
+        if (sa > KL_W_MASK28) sa = KL_W_MASK28;
+        const unsigned long long nw = kl_w_make(nx, (uint32_t)sa, kl_w_epoch(old), true);
+        const unsigned long long prev = atomicCAS(&ctl->word, old, nw);
+        if (prev == old) return;
+        old = prev;
+    }
+}
+
 // Effective limit of the current launch from a word value: min(len, stop_at if stopped).
 __device__ __forceinline__ uint32_t word_limit(unsigned long long w, uint32_t len) {
     uint32_t lim = len;
@@ -112,7 +131,13 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         uint32_t nexec = 0;
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
-                const unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                const unsigned long long req = ctl->stop_req;
+                unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
+                    // a host re-plan asked this launch to stop: set the boundary (>= this fetch)
+                    stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
+                    old = (atomicAdd(&ctl->word, 0ull) & ~KL_W_MASK28) | (old & KL_W_MASK28);
+                }
                 const uint32_t vb = kl_w_next(old);
                 const uint32_t lim = word_limit(old, len);
                 const uint32_t end = vb < lim ? min(vb + L.chunk, lim) : vb;

@@ -54,6 +54,7 @@ const kl_profile kDefaultProfiles[KL_NKINDS] = {
 };
 
 constexpr int kRecRing = 1024;
+constexpr int kStopRing = 256;
 constexpr int kPool = 8;
 
 struct Launch;
@@ -126,6 +127,8 @@ struct kl_ctx {
     int pool_busy[kPool] = {};
     cudaStream_t ctrl = nullptr, stopper = nullptr;
     KlLaunchRec* recs = nullptr;       // mapped ring of launch records
+    unsigned long long* stop_pinned = nullptr;   // pinned ring of stop-request words
+    uint64_t stop_slot = 0;
     std::vector<int> free_recs;
     std::vector<std::unique_ptr<Launch>> inflight;
     Decision desired;
@@ -566,13 +569,17 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     return KL_OK;
 }
 
+// Stop request (Alg.1 re-plan): the copy engine writes an epoch-tagged request into the kernel's
+// control block (no SM needed -- a stop kernel could not be scheduled while the co-runners fill
+// every SM); the next block that fetches work sets the boundary.
 kl_status request_stop(kl_ctx* ctx, Launch* L) {
     if (L->stop_requested) return KL_OK;
-    int rc = kl_dev_stop(ctx->ctl_pool + L->k->slot, L->epoch, L->slice, ctx->stopper);
-    if (rc) return ctx->fail(KL_ECUDA, "stop: %s", cudaGetErrorString((cudaError_t)rc));
+    unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
+    *slot = kl_stop_req(L->epoch, L->slice);
+    KL_CUDA(cudaMemcpyAsync((void*)&ctx->ctl_pool[L->k->slot].stop_req, slot, sizeof(*slot), cudaMemcpyHostToDevice,
+                            ctx->stopper));
     L->stop_requested = true;
     ctx->st.stops++;
-    ctx->st.device_launches++;
     return KL_OK;
 }
 
@@ -854,6 +861,7 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             KL_CUDA(cudaStreamCreateWithPriority(&ctx->stopper, cudaStreamNonBlocking, hi));
             KL_CUDA(cudaHostAlloc(&ctx->recs, sizeof(KlLaunchRec) * kRecRing, cudaHostAllocMapped));
+            KL_CUDA(cudaHostAlloc(&ctx->stop_pinned, sizeof(unsigned long long) * kStopRing, cudaHostAllocDefault));
             std::memset(ctx->recs, 0, sizeof(KlLaunchRec) * kRecRing);
             for (int r = kRecRing - 1; r >= 0; --r) ctx->free_recs.push_back(r);
             KL_CUDA(cudaStreamCreateWithFlags(&ctx->ctrl, cudaStreamNonBlocking));
@@ -897,6 +905,7 @@ kl_status kl_destroy(kl_ctx* ctx) {
             if (ctx->pool_own[i] && ctx->pool[i]) cudaStreamDestroy(ctx->pool[i]);
         if (ctx->stopper) cudaStreamDestroy(ctx->stopper);
         if (ctx->recs) cudaFreeHost(ctx->recs);
+        if (ctx->stop_pinned) cudaFreeHost(ctx->stop_pinned);
         for (auto& k : ctx->insts) if (k->audit) cudaFree(k->audit);
         if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
         if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
