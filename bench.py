@@ -237,7 +237,7 @@ def run_kernelet(args, rank, world, local_rank):
         ctx.reset_counters()
         counters[5] = rank
         counters[6] = world
-        ids = [ctx.submit(i.kind, i.grid, i.args, tag=n + 1) for n, i in enumerate(insts)]
+        ids = ctx.submit_many([(i.kind, i.grid, i.args, n + 1, None) for n, i in enumerate(insts)])
         c = ctx.sync()
         if world > 1:
             with torch.cuda.stream(lane_a):
@@ -451,8 +451,7 @@ def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b) -> dict
                 ready[k] = ev
         ctx.reset_model_cache()
         ctx.reset_counters()
-        for n, i in enumerate(insts):
-            ctx.submit(i.kind, i.grid, i.args, tag=n + 1, ready_event=ready[i.kind])
+        ctx.submit_many([(i.kind, i.grid, i.args, n + 1, ready[i.kind]) for n, i in enumerate(insts)])
         c = ctx.sync()
         res = ctx.counters.cpu()        # D2H read of the step's result
         e1.record(lane)

@@ -202,6 +202,8 @@ const char* kl_last_error(const kl_ctx* ctx);
 
 /* Alg.1 lines 2-3: add kernel K to the pending set R; returns its id (>= 1). */
 kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* desc, uint64_t* out_id);
+/* kl_submit for n descriptors in order (one ABI crossing for a whole queue). */
+kl_status kl_submit_batch(kl_ctx* ctx, const kl_kernel_desc* descs, size_t n, uint64_t* out_ids);
 /* Slicing plan: slices of slice_blocks contiguous blocks at
  * blocks_per_sm resident blocks per SM; slice_blocks = 0 applies the p% rule (m_min waves). */
 kl_status kl_slice(kl_ctx* ctx, uint64_t id, uint32_t blocks_per_sm, uint32_t slice_blocks,
@@ -239,7 +241,8 @@ kl_status kl_reset_model_cache(kl_ctx* ctx);
  * P:1232-1233) into the prediction cache; with config.model_frozen = 1 the device model is never
  * run and a candidate without an installed prediction counts as infeasible. */
 kl_status kl_cache_put(kl_ctx* ctx, const kl_candidate* cands, const kl_prediction* preds, size_t n);
-kl_status kl_reset_counters(kl_ctx* ctx);        /* zero counters_dev (t_start = INT64_MAX) */
+kl_status kl_reset_counters(kl_ctx* ctx);  /* zero counters_dev (t_start = INT64_MAX), stream-ordered
+                                              before the next launched kernel (no host sync) */
 kl_status kl_trace(kl_ctx* ctx, kl_trace_rec* out, size_t cap, size_t* n_out);
 /* Coverage audit (config.audit = 1): copy kernel `id`'s per-virtual-block execution counts
  * (uint32[grid_blocks], device-maintained) into host_out[0..n). */

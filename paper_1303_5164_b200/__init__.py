@@ -158,7 +158,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -197,6 +197,7 @@ def lib() -> C.CDLL:
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
     L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
+    L.kl_submit_batch.argtypes = [_vp, P(KernelDesc), C.c_size_t, P(C.c_uint64)]
     L.kl_cache_put.argtypes = [_vp, P(Candidate), P(Prediction), C.c_size_t]
     L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
     for s in ABI_SYMBOLS:
@@ -293,6 +294,21 @@ class Context:
         self._check(self._L.kl_submit(self._h, C.byref(d), C.byref(out)))
         self._keep[out.value] = args
         return out.value
+
+    def submit_many(self, items) -> list[int]:
+        """items: [(kind, grid_blocks, args, tag, ready_event or None)] -> ids (one ABI call)."""
+        n = len(items)
+        arr = (KernelDesc * max(n, 1))()
+        for i, (kind, grid, args, tag, ev) in enumerate(items):
+            kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
+            e = getattr(ev, "cuda_event", ev) if ev is not None else None
+            arr[i] = KernelDesc(kid, grid, C.cast(C.pointer(args), _vp), C.sizeof(args), None, tag, e)
+        ids = (C.c_uint64 * max(n, 1))()
+        self._check(self._L.kl_submit_batch(self._h, arr, n, ids))
+        out = list(ids)[:n]
+        for kid, it in zip(out, items):
+            self._keep[kid] = it[2]
+        return out
 
     def slice(self, kid: int, blocks_per_sm: int, slice_blocks: int = 0) -> SlicePlan:
         p = SlicePlan()

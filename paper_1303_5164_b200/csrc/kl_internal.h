@@ -120,7 +120,7 @@ struct KlDecision {
     int32_t pad;
 };
 // Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
-int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream);
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters, void* stream);
 // Stop request encoding (see KlCtl::stop_req).
 KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)slice << 32);

@@ -407,9 +407,12 @@ int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n,
     KL_DISPATCH(kind, launch_plain, blob, offset, n, stream);
 }
 
-// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
-__global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs; optionally
+// reset the completion counters (kl_counters layout; t_start = INT64_MAX).
+__global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (counters && t < 5) counters[t] = (t == 2) ? 0x7fffffffffffffffull : 0ull;
+    for (int i = t; i < n; i += gridDim.x * blockDim.x) {
         KlCtl* c = pool + slots_lens[2 * i];
         c->word = kl_w_make(0u, 0u, 0u, false);
         c->len = slots_lens[2 * i + 1];
@@ -423,9 +426,10 @@ __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n) {
     }
 }
 
-int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream) {
-    if (n <= 0) return 0;
-    k_ctl_init<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(pool, slots_lens, n);
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters, void* stream) {
+    if (n <= 0 && !counters) return 0;
+    const int blocks = n > 0 ? (n + 255) / 256 : 1;
+    k_ctl_init<<<blocks, 256, 0, (cudaStream_t)stream>>>(pool, slots_lens, n, counters);
     return (int)cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@
 #include "kl_internal.h"
 
 uint32_t kl_args_size(int kind);
-int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, void* stream);
+int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters, void* stream);
 
 namespace {
 
@@ -135,9 +135,14 @@ struct kl_ctx {
     bool have_desired = false;
     kl_stats st{};
     cudaEvent_t init_ev = nullptr;
+    cudaEvent_t init_done[2] = {};     // last use of each init buffer
+    bool init_used[2] = {};
+    int init_buf = 0;
+    bool reset_pending = false;        // counters reset folded into the next init launch
     KlCtl* ctl_pool = nullptr;
     std::vector<int> free_slots;
-    uint32_t* init_pinned = nullptr;   // mapped (slot, len) pairs awaiting k_ctl_init
+    uint32_t* init_pinned = nullptr;   // mapped (slot, len) pairs awaiting k_ctl_init (2 buffers)
+    uint32_t* init_base = nullptr;
     int n_init = 0;
     std::vector<std::unique_ptr<Inst>> insts;
     std::unordered_map<uint64_t, Inst*> by_id;
@@ -504,16 +509,23 @@ int waves_of(const kl_ctx* c, const Decision& d) {
 }
 
 kl_status flush_ctl_init(kl_ctx* ctx) {
-    if (ctx->n_init == 0) return KL_OK;
-    int rc = kl_dev_ctl_init(ctx->ctl_pool, ctx->init_pinned, ctx->n_init, ctx->ctrl);
+    if (ctx->n_init == 0 && !ctx->reset_pending) return KL_OK;
+    int rc = kl_dev_ctl_init(ctx->ctl_pool, ctx->init_pinned, ctx->n_init,
+                             ctx->reset_pending ? reinterpret_cast<unsigned long long*>(ctx->counters) : nullptr, ctx->ctrl);
     if (rc) return ctx->fail(KL_ECUDA, "ctl init: %s", cudaGetErrorString((cudaError_t)rc));
     ctx->st.device_launches++;
     KL_CUDA(cudaEventRecord(ctx->init_ev, ctx->ctrl));
     for (int i = 0; i < kPool; ++i) KL_CUDA(cudaStreamWaitEvent(ctx->pool[i], ctx->init_ev, 0));
     KL_CUDA(cudaStreamWaitEvent(ctx->stopper, ctx->init_ev, 0));
-    // the mapped init list is read by the kernel: wait before it can be overwritten
-    KL_CUDA(cudaEventSynchronize(ctx->init_ev));
+    // the kernel reads the mapped list: switch to the other buffer (waited on before reuse)
+    const int b = ctx->init_buf;
+    KL_CUDA(cudaEventRecord(ctx->init_done[b], ctx->ctrl));
+    ctx->init_used[b] = true;
+    ctx->init_buf = b ^ 1;
+    ctx->init_pinned = ctx->init_base + (size_t)ctx->init_buf * 2 * kCtlPool;
+    if (ctx->init_used[ctx->init_buf]) KL_CUDA(cudaEventSynchronize(ctx->init_done[ctx->init_buf]));
     ctx->n_init = 0;
+    ctx->reset_pending = false;
     return KL_OK;
 }
 
@@ -868,7 +880,9 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaEventCreateWithFlags(&ctx->init_ev, cudaEventDisableTiming));
             KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
             KL_CUDA(cudaMemset(ctx->ctl_pool, 0, sizeof(KlCtl) * kCtlPool));
-            KL_CUDA(cudaHostAlloc(&ctx->init_pinned, sizeof(uint32_t) * 2 * kCtlPool, cudaHostAllocMapped));
+            KL_CUDA(cudaHostAlloc(&ctx->init_base, sizeof(uint32_t) * 4 * kCtlPool, cudaHostAllocMapped));
+            ctx->init_pinned = ctx->init_base;
+            for (auto& e : ctx->init_done) KL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocDefault));
             KL_CUDA(cudaMalloc(&ctx->mk_dev, sizeof(KlModelKind) * KL_NKINDS));
             KL_CUDA(cudaHostAlloc(&ctx->cand_pinned, sizeof(KlCand) * kMaxCand, cudaHostAllocDefault));
@@ -910,7 +924,8 @@ kl_status kl_destroy(kl_ctx* ctx) {
         if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
         if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
         cudaFree(ctx->ctl_pool);
-        cudaFreeHost(ctx->init_pinned);
+        cudaFreeHost(ctx->init_base);
+        for (auto& e : ctx->init_done) if (e) cudaEventDestroy(e);
         cudaFreeHost(ctx->mk_pinned);
         cudaFree(ctx->mk_dev);
         cudaFreeHost(ctx->cand_pinned);
@@ -972,6 +987,16 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     else ctx->R.push_back(raw);
     ctx->insts.push_back(std::move(k));
     if (out_id) *out_id = raw->id;
+    return KL_OK;
+}
+
+kl_status kl_submit_batch(kl_ctx* ctx, const kl_kernel_desc* d, size_t n, uint64_t* ids) {
+    KL_LIVE(ctx);
+    if (n && !d) return KL_EINVAL;
+    for (size_t i = 0; i < n; ++i) {
+        kl_status st = kl_submit(ctx, d + i, ids ? ids + i : nullptr);
+        if (st) return st;
+    }
     return KL_OK;
 }
 
@@ -1214,9 +1239,7 @@ kl_status kl_reset_model_cache(kl_ctx* ctx) {
 kl_status kl_reset_counters(kl_ctx* ctx) {
     KL_LIVE(ctx);
     if (ctx->host_only || !ctx->counters) return KL_OK;
-    static const int64_t init[8] = {0, 0, INT64_MAX, 0, 0, 0, 0, 0};
-    KL_CUDA(cudaMemcpyAsync(ctx->counters, init, 5 * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->ctrl));
-    KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
+    ctx->reset_pending = true;   // done by the next init launch, stream-ordered before any kernel
     return KL_OK;
 }
 

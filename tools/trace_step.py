@@ -20,7 +20,7 @@ data = {k: G.gen(k, "paper") for k in sorted(set(kinds))}
 inputs = {k: inputs_to_device(data[k], "cuda") for k in data}
 insts = [Instance(data[k], "cuda", inputs=inputs[k]) for k in kinds]
 out = {"sweep": {}, "trace": []}
-for k in sorted(set(kinds)):
+for k in ([] if "--no-sweep" in sys.argv else sorted(set(kinds))):
     i = next(x for x in insts if x.kind == k)
     p = ctx.get_profile(k)
     row = {}
