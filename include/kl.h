@@ -141,6 +141,9 @@ typedef struct {
     int32_t n_sms;             /* 0 = from the device */
     int32_t chunk;             /* virtual blocks per work fetch; 0 = per-kind default */
     int32_t audit;             /* 1: count executions per virtual block (coverage audit) */
+    int32_t retune;            /* 1 (default): a re-plan that keeps a running kernel at another
+                                  occupancy re-tunes it in place; 0: stop and relaunch */
+    int32_t pad0;
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
@@ -181,6 +184,8 @@ typedef struct {               /* runtime statistics since kl_create */
     int64_t device_launches;   /* every kernel launched by the library (incl. model, stop, init) */
     int64_t decide_ns;         /* host time spent in FindCoSchedule (incl. model batches) */
     int64_t model_ns;          /* host time spent waiting for model batches */
+    int64_t retunes;           /* in-place occupancy changes of a running kernel (no stop) */
+    int64_t topups;            /* top-up grids launched by re-tunes that raised the occupancy */
 } kl_stats;
 typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;
@@ -190,6 +195,8 @@ typedef struct {               /* one launch of a kernel (trace / residency evid
     int32_t phase;             /* index of the FindCoSchedule decision that launched it */
     int32_t partner_kind;      /* kind co-scheduled by that decision, -1 = solo */
     double cp;                 /* predicted CP of that decision */
+    uint32_t cap_max;          /* largest cap in force during the launch (re-tunes) */
+    uint32_t grids;            /* device grids that served it (1 + top-ups) */
 } kl_trace_rec;
 
 /* ---- calls -------------------------------------------------------------------------------- */

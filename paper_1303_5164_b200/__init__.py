@@ -105,7 +105,7 @@ class Config(C.Structure):
                 ("cp_min", C.c_double), ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
                 ("split_rule", C.c_int32), ("model_frozen", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
-                ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
+                ("retune", C.c_int32), ("pad0", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
                 ("profiles", C.POINTER(Profile)), ("stream_a", _vp), ("stream_b", _vp),
                 ("counters_dev", _vp)]
@@ -144,7 +144,7 @@ class Counters(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("decisions", "launches", "stops", "model_batches", "model_candidates",
-                                         "device_launches", "decide_ns", "model_ns")]
+                                         "device_launches", "decide_ns", "model_ns", "retunes", "topups")]
 
 
 class TraceRec(C.Structure):
@@ -152,7 +152,7 @@ class TraceRec(C.Structure):
                 ("slice", C.c_uint32), ("start", C.c_uint32), ("end", C.c_uint32), ("executed", C.c_uint32),
                 ("admitted", C.c_uint32), ("max_per_sm", C.c_uint32), ("exhausted", C.c_uint32),
                 ("t0_ns", C.c_int64), ("t1_ns", C.c_int64), ("phase", C.c_int32),
-                ("partner_kind", C.c_int32), ("cp", C.c_double)]
+                ("partner_kind", C.c_int32), ("cp", C.c_double), ("cap_max", C.c_uint32), ("grids", C.c_uint32)]
 
 
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",

@@ -33,10 +33,23 @@ KL_HD unsigned long long kl_w_make(uint32_t next, uint32_t stop_at, uint32_t epo
            (((unsigned long long)epoch & 0x7full) << 56) | (stop ? KL_W_STOP : 0ull);
 }
 
+// Membership word of the current epoch (one epoch = one host-level launch, possibly served by
+// several device grids: the first grid plus top-ups when a re-plan raises the occupancy):
+//   bits [0,32) live blocks of the epoch, bits [32,39) epoch, bit 39 closed.
+// A block joins only while the epoch matches and the epoch is open; the block that brings the
+// count to zero closes the epoch and finalizes it.  Late blocks (slack, top-ups that arrive after
+// the close) fail to join and exit without touching anything.
+KL_HD unsigned long long kl_j_make(uint32_t epoch, bool closed) {
+    return ((unsigned long long)(epoch & 0x7fu) << 32) | (closed ? (1ull << 39) : 0ull);
+}
+KL_HD uint32_t kl_j_count(unsigned long long j) { return (uint32_t)(j & 0xffffffffull); }
+KL_HD uint32_t kl_j_epoch(unsigned long long j) { return (uint32_t)((j >> 32) & 0x7full); }
+KL_HD bool kl_j_closed(unsigned long long j) { return (j >> 39) & 1ull; }
+
 struct KlCtl {
     unsigned long long word;
+    unsigned long long join;   // membership word (kl_j_*)
     uint32_t len;
-    uint32_t exited;      // blocks of the current launch that finished (admitted or not)
     uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
     uint32_t admitted;    // admitted blocks of the current launch
     uint32_t executed;    // virtual blocks executed in the current launch
@@ -45,6 +58,10 @@ struct KlCtl {
     // host stop request, written by the copy engine (no SM needed): bit 0 valid, bits [1,8) epoch
     // of the launch to stop, bits [32,64) slice size; the next fetching block performs the stop
     volatile unsigned long long stop_req;
+    // host occupancy re-tune, written by the copy engine: bit 0 valid, bits [1,8) epoch, bits
+    // [32,64) blocks per SM (0 = uncapped).  Blocks above the cap on their SM leave at their next
+    // fetch; raising the cap is served by a top-up grid of the same epoch.
+    volatile unsigned long long tune;
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
 };
@@ -66,7 +83,7 @@ struct KlLaunch {
     uint32_t cap;                   // admitted blocks per SM (0 = no cap)
     uint32_t chunk;                 // virtual blocks per fetch
     uint32_t n_sms;
-    uint32_t pad;
+    uint32_t epoch;                 // epoch this grid serves (mod 128)
     KlLaunchRec* rec;
     unsigned long long* counters;   // kl_counters on the device (may be null)
     uint32_t* audit;                // per-virtual-block execution counts (may be null)
@@ -124,6 +141,11 @@ int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned lon
 // Stop request encoding (see KlCtl::stop_req).
 KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)slice << 32);
+}
+
+// Occupancy re-tune encoding (see KlCtl::tune).
+KL_HD unsigned long long kl_tune_req(uint32_t epoch, uint32_t cap) {
+    return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)cap << 32);
 }
 
 // Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy

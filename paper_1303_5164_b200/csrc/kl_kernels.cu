@@ -132,7 +132,7 @@ struct BodySAD {
 struct BodySPMV {
     using Params = kl_args_spmv;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 8, kDynSmem = 0;
+    static constexpr int kThreads = 256, kChunk = 8, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -416,7 +416,8 @@ __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsig
         KlCtl* c = pool + slots_lens[2 * i];
         c->word = kl_w_make(0u, 0u, 0u, false);
         c->len = slots_lens[2 * i + 1];
-        c->exited = 0;
+        c->join = kl_j_make(0u, false);
+        c->tune = 0ull;
         c->drained = 0;
         c->admitted = 0;
         c->executed = 0;

@@ -5,13 +5,17 @@
 // kernel (cap x n_SM blocks, plus slack); each admitted block pulls virtual block ids from the
 // kernel's slice control word (KlCtl::word) and runs Body::block(vb) -- index rectification as a
 // kernel parameter instead of Fermi SASS rewriting.  Occupancy control is a per-SM
-// admission cap read from %smid.  The first block to find the range exhausted raises the
-// kernel's `drained` event in host-mapped memory (Alg.1 l.9: "K1 and K2 both still have thread
-// blocks" turns false), which is what the host scheduler reacts to; a host-requested stop (k_stop)
-// ends a launch at its next slice boundary.  Header-only: included by kl_kernels.cu and kl_mm.cu.
+// admission cap read from %smid; a host re-tune (KlCtl::tune) lowers it in place (surplus blocks
+// leave at their next fetch) or raises it (a top-up grid joins the same epoch), so a re-plan that
+// only changes a running kernel's slice ratio costs no drain and no relaunch.  The first block to
+// find the range exhausted raises the kernel's `drained` event in host-mapped memory (Alg.1 l.9:
+// "K1 and K2 both still have thread blocks" turns false), which is what the host scheduler reacts
+// to; a host-requested stop (KlCtl::stop_req) ends the epoch at the next fetch boundary.
+// Header-only: included by kl_kernels.cu and kl_mm.cu.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include "kl_internal.h"
 
 namespace {
@@ -57,7 +61,9 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     KlCtl* ctl = L.ctl;
     __threadfence();
     const unsigned long long w = atomicAdd(&ctl->word, 0ull);
-    const uint32_t lim = word_limit(w, len);
+    // every id below min(next, limit) was handed out and executed by a block that has left;
+    // over-fetched ids (>= limit) are discarded
+    const uint32_t lim = min(word_limit(w, len), kl_w_next(w));
     const uint32_t executed = atomicExch(&ctl->executed, 0u);
     const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
     uint32_t mx = 0;
@@ -69,9 +75,11 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     const unsigned long long t1 = gtimer();
     const uint32_t start = ctl->base;
     ctl->base = lim;
-    // next launch: next = lim, stop cleared, epoch + 1
-    atomicExch(&ctl->word, kl_w_make(lim, 0u, kl_w_epoch(w) + 1u, false));
-    atomicExch(&ctl->exited, 0u);
+    // next epoch: next = lim, stop cleared; membership reopened for the new epoch
+    const uint32_t ne = kl_w_epoch(w) + 1u;
+    atomicExch(&ctl->word, kl_w_make(lim, 0u, ne, false));
+    __threadfence();
+    atomicExch(&ctl->join, kl_j_make(ne, false));
     const bool exh = (lim == len);
     if (L.counters) {
         atomicAdd(&L.counters[1], (unsigned long long)executed);
@@ -98,29 +106,66 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     }
 }
 
+// Join the grid's epoch (false: the epoch is closed or another epoch is current -> exit).
+__device__ bool join_epoch(KlCtl* ctl, uint32_t epoch) {
+    unsigned long long j = atomicAdd(&ctl->join, 0ull);
+    for (;;) {
+        if (kl_j_closed(j) || kl_j_epoch(j) != (epoch & 0x7fu)) return false;
+        const unsigned long long prev = atomicCAS(&ctl->join, j, j + 1ull);
+        if (prev == j) return true;
+        j = prev;
+    }
+}
+
+// Leave the epoch; the block that brings the count to zero closes and finalizes it.
+__device__ void leave_epoch(const KlLaunch& L, uint32_t len) {
+    KlCtl* ctl = L.ctl;
+    __threadfence();
+    unsigned long long j = atomicAdd(&ctl->join, ~0ull) - 1ull;   // count - 1
+    if (kl_j_count(j) != 0) return;
+    const unsigned long long closed = j | (1ull << 39);
+    if (atomicCAS(&ctl->join, j, closed) == j) finalize_launch(L, len);
+}
+
+// Occupancy cap in force for this grid's epoch: the host re-tune if it names the epoch, else the
+// grid's own cap (0 = uncapped).
+__device__ __forceinline__ uint32_t cap_now(const KlLaunch& L, const KlCtl* ctl) {
+    const unsigned long long t = ctl->tune;
+    if ((t & 1ull) && ((t >> 1) & 0x7full) == (L.epoch & 0x7fu)) return (uint32_t)(t >> 32);
+    return L.cap;
+}
+
+// Optional Body::kMinBlocks: resident blocks per SM the register allocation must allow (keeps
+// the persistent variant at the plain kernel's occupancy despite the fetch logic).
+template <class B, class = void>
+struct min_blocks { static constexpr int value = 0; };   // 0 = unspecified
+template <class B>
+struct min_blocks<B, std::void_t<decltype(B::kMinBlocks)>> { static constexpr int value = B::kMinBlocks; };
+
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads)
+__global__ void __launch_bounds__(Body::kThreads, min_blocks<Body>::value)
 k_persistent(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
     extern __shared__ __align__(1024) char dsmem[];
     __shared__ uint32_t s_vb[2], s_end[2], s_adm;
     KlCtl* ctl = L.ctl;
     const uint32_t len = ctl->len;
     uint32_t sm = 0;
+    bool joined = false;
     if (threadIdx.x == 0) {
-        uint32_t adm = 1;
-        sm = smid_u32();
-        if (L.cap) {
-            uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
-            if (c >= L.cap) {
+        uint32_t adm = 0;
+        joined = join_epoch(ctl, L.epoch);
+        if (joined) {
+            sm = smid_u32();
+            const uint32_t cap = cap_now(L, ctl);
+            const uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
+            if (cap && c >= cap) {
                 atomicSub(&ctl->sm_count[sm], 1u);
-                adm = 0;
             } else {
+                adm = 1;
                 atomicMax(&ctl->sm_hwm[sm], c + 1);
+                atomicAdd(&ctl->admitted, 1u);
+                atomicMin(&ctl->t0, gtimer());
             }
-        }
-        if (adm) {
-            atomicAdd(&ctl->admitted, 1u);
-            atomicMin(&ctl->t0, gtimer());
         }
         s_adm = adm;
     }
@@ -129,23 +174,38 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         typename Body::State st;
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
+        bool counted = true;   // this block still holds an sm_count slot
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
-                const unsigned long long req = ctl->stop_req;
-                unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-                if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
-                    // a host re-plan asked this launch to stop: set the boundary (>= this fetch)
-                    stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
-                    old = (atomicAdd(&ctl->word, 0ull) & ~KL_W_MASK28) | (old & KL_W_MASK28);
+                uint32_t vb = 0, end = 0;
+                // occupancy lowered by a re-tune: surplus blocks on this SM leave (no fetch)
+                const uint32_t cap = cap_now(L, ctl);
+                bool leave = false;
+                if (cap) {
+                    uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                    while (c > cap) {
+                        const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                        if (prev == c) { leave = true; counted = false; break; }
+                        c = prev;
+                    }
                 }
-                const uint32_t vb = kl_w_next(old);
-                const uint32_t lim = word_limit(old, len);
-                const uint32_t end = vb < lim ? min(vb + L.chunk, lim) : vb;
-                if (vb >= len && lim == len && L.rec) {
-                    // the kernel has no more thread blocks: raise the drained event once
-                    if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
-                        L.rec->drained = 1u;
-                        __threadfence_system();
+                if (!leave) {
+                    const unsigned long long req = ctl->stop_req;
+                    unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                    if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
+                        // a host re-plan asked this epoch to stop: set the boundary (>= this fetch)
+                        stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
+                        old = (atomicAdd(&ctl->word, 0ull) & ~KL_W_MASK28) | (old & KL_W_MASK28);
+                    }
+                    vb = kl_w_next(old);
+                    const uint32_t lim = word_limit(old, len);
+                    end = vb < lim ? min(vb + L.chunk, lim) : vb;
+                    if (vb >= len && lim == len && L.rec) {
+                        // the kernel has no more thread blocks: raise the drained event once
+                        if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
+                            L.rec->drained = 1u;
+                            __threadfence_system();
+                        }
                     }
                 }
                 s_vb[it & 1] = vb;
@@ -163,14 +223,10 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         Body::fini(P, st, dsmem);
         if (threadIdx.x == 0) {
             atomicAdd(&ctl->executed, nexec);
-            if (L.cap) atomicSub(&ctl->sm_count[sm], 1u);
+            if (counted) atomicSub(&ctl->sm_count[sm], 1u);
         }
     }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t e = atomicAdd(&ctl->exited, 1u);
-        if (e == gridDim.x - 1) finalize_launch(L, len);
-    }
+    if (threadIdx.x == 0 && joined) leave_epoch(L, len);
 }
 
 // Plain grid: blockIdx rectified by the slice offset.

@@ -77,8 +77,11 @@ struct Inst {
 struct Launch {
     Inst* k = nullptr;
     int rec = -1, stream = 0;
+    std::vector<int> topup_streams;   // streams of top-up grids of this epoch
     uint32_t cap = 0, slice = 0, epoch = 0;
+    uint32_t cap_max = 0;             // 0 = uncapped at some point
     bool stop_requested = false;
+    KlLaunch params{};
     int32_t decision = 0, partner_kind = -1;
     double cp = 0.0;
 };
@@ -135,6 +138,7 @@ struct kl_ctx {
     bool have_desired = false;
     kl_stats st{};
     cudaEvent_t init_ev = nullptr;
+    cudaEvent_t tune_ev = nullptr;     // re-tune write -> top-up grid ordering
     cudaEvent_t init_done[2] = {};     // last use of each init buffer
     bool init_used[2] = {};
     int init_buf = 0;
@@ -545,6 +549,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     ctx->free_recs.pop_back();
     L->stream = pick_stream(ctx);
     L->cap = cap;
+    L->cap_max = cap;
     L->slice = slice;
     L->epoch = k->epoch++;
     L->decision = (int32_t)ctx->st.decisions;
@@ -557,6 +562,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     P.cap = cap;
     P.chunk = (uint32_t)(ctx->cfg.chunk > 0 ? ctx->cfg.chunk : inf.default_chunk);
     P.n_sms = (uint32_t)ctx->n_sms;
+    P.epoch = L->epoch & 0x7fu;
     P.rec = rec;
     P.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
     P.audit = k->audit;
@@ -576,8 +582,45 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     ctx->pool_busy[L->stream]++;
     ctx->st.launches++;
     ctx->st.device_launches++;
+    L->params = P;
     k->inflight = L.get();
     ctx->inflight.push_back(std::move(L));
+    return KL_OK;
+}
+
+// Re-plan that keeps a running kernel but changes its occupancy (slice ratio): the copy engine
+// writes the new cap into the control block; surplus blocks leave at their next fetch, and a raise
+// is served by a top-up grid joining the same epoch.  No drain, no relaunch.
+kl_status retune(kl_ctx* ctx, Launch* L, uint32_t cap, int partner_kind, double cp) {
+    const KlKindInfo& inf = ctx->info[L->k->kind];
+    const uint32_t bmax = (uint32_t)std::max(1, inf.bmax);
+    const uint32_t old_eff = L->cap ? L->cap : bmax, new_eff = cap ? cap : bmax;
+    unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
+    *slot = kl_tune_req(L->epoch, cap);
+    KL_CUDA(cudaMemcpyAsync((void*)&ctx->ctl_pool[L->k->slot].tune, slot, sizeof(*slot), cudaMemcpyHostToDevice,
+                            ctx->stopper));
+    ctx->st.retunes++;
+    L->cap = cap;
+    if (L->cap_max && (cap == 0 || cap > L->cap_max)) L->cap_max = cap;
+    L->partner_kind = partner_kind;
+    L->cp = cp;
+    L->decision = (int32_t)ctx->st.decisions;
+    if (new_eff > old_eff) {
+        KL_CUDA(cudaEventRecord(ctx->tune_ev, ctx->stopper));
+        const int si = pick_stream(ctx);
+        cudaStream_t s = ctx->pool[si];
+        KL_CUDA(cudaStreamWaitEvent(s, ctx->tune_ev, 0));
+        KlLaunch P = L->params;
+        P.cap = cap;
+        uint32_t grid = (new_eff - old_eff) * (uint32_t)ctx->n_sms;
+        grid += std::max((uint32_t)ctx->n_sms, grid / 4);
+        int rc = kl_dev_launch_persistent(L->k->kind, L->k->blob, P, grid, s);
+        if (rc) return ctx->fail(KL_ECUDA, "top-up kind %d: %s", L->k->kind, cudaGetErrorString((cudaError_t)rc));
+        ctx->pool_busy[si]++;
+        L->topup_streams.push_back(si);
+        ctx->st.topups++;
+        ctx->st.device_launches++;
+    }
     return KL_OK;
 }
 
@@ -587,7 +630,10 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
 kl_status request_stop(kl_ctx* ctx, Launch* L) {
     if (L->stop_requested) return KL_OK;
     unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
-    *slot = kl_stop_req(L->epoch, L->slice);
+    // stop at the next fetch (at least one chunk into the epoch): persistent blocks have no
+    // per-slice launch cost, so waiting for the p% slice boundary would only delay the re-plan
+    const uint32_t chunk = L->params.chunk ? L->params.chunk : 1u;
+    *slot = kl_stop_req(L->epoch, chunk);
     KL_CUDA(cudaMemcpyAsync((void*)&ctx->ctl_pool[L->k->slot].stop_req, slot, sizeof(*slot), cudaMemcpyHostToDevice,
                             ctx->stopper));
     L->stop_requested = true;
@@ -613,11 +659,14 @@ kl_status reconcile(kl_ctx* ctx) {
     for (auto& Lp : ctx->inflight) {
         Launch* L = Lp.get();
         if (L->stop_requested || L->k->drained) continue;
-        bool keep = false;
+        int want = -1;
         for (int i = 0; i < nw; ++i)
-            if (w[i].k == L->k && w[i].cap == L->cap) keep = true;
-        if (!keep) {
+            if (w[i].k == L->k) want = i;
+        if (want < 0) {
             kl_status st = request_stop(ctx, L);
+            if (st) return st;
+        } else if (w[want].cap != L->cap) {
+            kl_status st = ctx->cfg.retune ? retune(ctx, L, w[want].cap, w[want].partner, d.cp) : request_stop(ctx, L);
             if (st) return st;
         }
     }
@@ -682,6 +731,8 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
         t.phase = L->decision;
         t.partner_kind = L->partner_kind;
         t.cp = L->cp;
+        t.cap_max = L->cap_max;
+        t.grids = 1u + (uint32_t)L->topup_streams.size();
         ctx->trace.push_back(t);
         k->next = r->end;
         k->inflight = nullptr;
@@ -694,6 +745,7 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
             ctx->free_slots.push_back(k->slot);
         }
         ctx->pool_busy[L->stream]--;
+        for (int s : L->topup_streams) ctx->pool_busy[s]--;
         ctx->free_recs.push_back(L->rec);
         ctx->inflight.erase(ctx->inflight.begin() + i);
         *progress = true;
@@ -814,6 +866,7 @@ kl_status kl_config_default(kl_config* c) {
     c->a0 = 1.0;
     c->b0 = 0.0;
     c->n_sched = 4;            // B200: 4 SMSPs per SM -> W_v = 16
+    c->retune = 1;
     return KL_OK;
 }
 
@@ -878,6 +931,7 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             for (int r = kRecRing - 1; r >= 0; --r) ctx->free_recs.push_back(r);
             KL_CUDA(cudaStreamCreateWithFlags(&ctx->ctrl, cudaStreamNonBlocking));
             KL_CUDA(cudaEventCreateWithFlags(&ctx->init_ev, cudaEventDisableTiming));
+            KL_CUDA(cudaEventCreateWithFlags(&ctx->tune_ev, cudaEventDisableTiming));
             KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
             KL_CUDA(cudaMemset(ctx->ctl_pool, 0, sizeof(KlCtl) * kCtlPool));
             KL_CUDA(cudaHostAlloc(&ctx->init_base, sizeof(uint32_t) * 4 * kCtlPool, cudaHostAllocMapped));
@@ -923,6 +977,7 @@ kl_status kl_destroy(kl_ctx* ctx) {
         for (auto& k : ctx->insts) if (k->audit) cudaFree(k->audit);
         if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
         if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
+        if (ctx->tune_ev) cudaEventDestroy(ctx->tune_ev);
         cudaFree(ctx->ctl_pool);
         cudaFreeHost(ctx->init_base);
         for (auto& e : ctx->init_done) if (e) cudaEventDestroy(e);
