@@ -35,20 +35,33 @@ KL_HD unsigned long long kl_w_make(uint32_t next, uint32_t stop_at, uint32_t epo
 
 // Membership word of the current epoch (one epoch = one host-level launch, possibly served by
 // several device grids: the first grid plus top-ups when a re-plan raises the occupancy):
-//   bits [0,32) live blocks of the epoch, bits [32,39) epoch, bit 39 closed.
-// A block joins only while the epoch matches and the epoch is open; the block that brings the
-// count to zero closes the epoch and finalizes it.  Late blocks (slack, top-ups that arrive after
-// the close) fail to join and exit without touching anything.
-KL_HD unsigned long long kl_j_make(uint32_t epoch, bool closed) {
-    return ((unsigned long long)(epoch & 0x7fu) << 32) | (closed ? (1ull << 39) : 0ull);
+//   bits [0,32) live blocks, bits [32,63) ticket, bit 63 closed.
+// ticket = (slot generation << 7) | (epoch mod 128), so blocks of a finished kernel whose slot
+// was recycled, or of an older epoch, never match.  A block joins with one atomicAdd (after a
+// plain read filters late blocks); the block whose leave brings the count to zero closes the
+// epoch -- but only once its range is finished (exhausted or stopped) -- and finalizes it from
+// the control block's own record (KlCtl::fin), so even a late block undoing a stray join can.
+#define KL_J_CLOSED (1ull << 63)
+KL_HD uint32_t kl_ticket(uint32_t gen, uint32_t epoch) { return ((gen & 0xffffffu) << 7) | (epoch & 0x7fu); }
+KL_HD unsigned long long kl_j_make(uint32_t ticket, bool closed) {
+    return ((unsigned long long)(ticket & 0x7fffffffu) << 32) | (closed ? KL_J_CLOSED : 0ull);
 }
 KL_HD uint32_t kl_j_count(unsigned long long j) { return (uint32_t)(j & 0xffffffffull); }
-KL_HD uint32_t kl_j_epoch(unsigned long long j) { return (uint32_t)((j >> 32) & 0x7full); }
-KL_HD bool kl_j_closed(unsigned long long j) { return (j >> 39) & 1ull; }
+KL_HD uint32_t kl_j_ticket(unsigned long long j) { return (uint32_t)((j >> 32) & 0x7fffffffull); }
+KL_HD bool kl_j_closed(unsigned long long j) { return (j & KL_J_CLOSED) != 0ull; }
+
+struct KlLaunchRec;
+struct KlFin {             // what the finalizing block needs, written by every joined block
+    KlLaunchRec* rec;
+    unsigned long long* counters;
+    unsigned long long tag;
+    uint32_t n_sms, pad;
+};
 
 struct KlCtl {
     unsigned long long word;
     unsigned long long join;   // membership word (kl_j_*)
+    KlFin fin;
     uint32_t len;
     uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
     uint32_t admitted;    // admitted blocks of the current launch
@@ -83,7 +96,7 @@ struct KlLaunch {
     uint32_t cap;                   // admitted blocks per SM (0 = no cap)
     uint32_t chunk;                 // virtual blocks per fetch
     uint32_t n_sms;
-    uint32_t epoch;                 // epoch this grid serves (mod 128)
+    uint32_t ticket;                // kl_ticket(slot generation, epoch) this grid serves
     KlLaunchRec* rec;
     unsigned long long* counters;   // kl_counters on the device (may be null)
     uint32_t* audit;                // per-virtual-block execution counts (may be null)
@@ -136,7 +149,7 @@ struct KlDecision {
     volatile int32_t done;
     int32_t pad;
 };
-// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs.
+// Initialise slice control blocks from a (host-mapped) list of (slot, len, generation) triples.
 int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters, void* stream);
 // Stop request encoding (see KlCtl::stop_req).
 KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {

@@ -27,7 +27,7 @@ struct Empty {};
 struct BodyPC {
     using Params = kl_args_pc;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -152,7 +152,7 @@ struct BodySPMV {
 struct BodyST {
     using Params = kl_args_st;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 16;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -193,7 +193,7 @@ struct BodyST {
 struct BodyMRIQ {
     using Params = kl_args_mriq;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -252,7 +252,7 @@ __device__ __forceinline__ void bs_one(float S, float X, float T, float R, float
 struct BodyBS {
     using Params = kl_args_bs;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 9;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -290,7 +290,7 @@ __device__ __forceinline__ void tea_enc(uint32_t& v0, uint32_t& v1, uint32_t k0,
 struct BodyTEA {
     using Params = kl_args_tea;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 16;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -313,7 +313,7 @@ struct BodyTEA {
 struct BodyMATADD {
     using Params = kl_args_matadd;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -327,7 +327,7 @@ struct BodyMATADD {
 struct BodySYNTH {
     using Params = kl_args_synth;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
@@ -407,16 +407,24 @@ int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n,
     KL_DISPATCH(kind, launch_plain, blob, offset, n, stream);
 }
 
-// Initialise slice control blocks from a (host-mapped) list of (slot, len) pairs; optionally
+// Initialise slice control blocks from a (host-mapped) list of (slot, len, gen) triples; optionally
 // reset the completion counters (kl_counters layout; t_start = INT64_MAX).
 __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (counters && t < 5) counters[t] = (t == 2) ? 0x7fffffffffffffffull : 0ull;
     for (int i = t; i < n; i += gridDim.x * blockDim.x) {
-        KlCtl* c = pool + slots_lens[2 * i];
+        KlCtl* c = pool + slots_lens[3 * i];
         c->word = kl_w_make(0u, 0u, 0u, false);
-        c->len = slots_lens[2 * i + 1];
-        c->join = kl_j_make(0u, false);
+        c->len = slots_lens[3 * i + 1];
+        // count-preserving: a late block of the slot's previous kernel may have a stray join
+        // pending its undo
+        unsigned long long cur = atomicAdd(&c->join, 0ull);
+        for (;;) {
+            const unsigned long long nw = (cur & 0xffffffffull) | kl_j_make(kl_ticket(slots_lens[3 * i + 2], 0u), false);
+            const unsigned long long prev = atomicCAS(&c->join, cur, nw);
+            if (prev == cur) break;
+            cur = prev;
+        }
         c->tune = 0ull;
         c->drained = 0;
         c->admitted = 0;

@@ -57,9 +57,14 @@ __device__ __forceinline__ uint32_t word_limit(unsigned long long w, uint32_t le
     return lim;
 }
 
-__device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
-    KlCtl* ctl = L.ctl;
+__device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
     __threadfence();
+    volatile KlFin* vf = &ctl->fin;
+    KlFin F;
+    F.rec = vf->rec;
+    F.counters = vf->counters;
+    F.tag = vf->tag;
+    F.n_sms = vf->n_sms;
     const unsigned long long w = atomicAdd(&ctl->word, 0ull);
     // every id below min(next, limit) was handed out and executed by a block that has left;
     // over-fetched ids (>= limit) are discarded
@@ -67,7 +72,7 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     const uint32_t executed = atomicExch(&ctl->executed, 0u);
     const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
     uint32_t mx = 0;
-    for (uint32_t s = 0; s < L.n_sms && s < KL_MAX_SMS; ++s) {
+    for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
         mx = max(mx, ctl->sm_hwm[s]);
         ctl->sm_hwm[s] = 0;
     }
@@ -75,22 +80,34 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     const unsigned long long t1 = gtimer();
     const uint32_t start = ctl->base;
     ctl->base = lim;
-    // next epoch: next = lim, stop cleared; membership reopened for the new epoch
+    const bool exh = (lim == len);
+    // next epoch: next = lim, stop cleared; membership reopened only if blocks remain (an
+    // exhausted kernel's word stays closed, so no late block can ever open a phantom epoch)
+    const uint32_t tk = kl_j_ticket(j);
     const uint32_t ne = kl_w_epoch(w) + 1u;
     atomicExch(&ctl->word, kl_w_make(lim, 0u, ne, false));
     __threadfence();
-    atomicExch(&ctl->join, kl_j_make(ne, false));
-    const bool exh = (lim == len);
-    if (L.counters) {
-        atomicAdd(&L.counters[1], (unsigned long long)executed);
-        if (exh) {
-            atomicAdd(&L.counters[0], 1ull);
-            atomicAdd(&L.counters[4], L.tag);
+    if (!exh) {
+        // reopen for the next epoch; the count is preserved (a late block's stray join may still
+        // be pending its undo)
+        unsigned long long cur = atomicAdd(&ctl->join, 0ull);
+        for (;;) {
+            const unsigned long long nw = (cur & 0xffffffffull) | kl_j_make((tk & ~0x7fu) | (ne & 0x7fu), false);
+            const unsigned long long prev = atomicCAS(&ctl->join, cur, nw);
+            if (prev == cur) break;
+            cur = prev;
         }
-        if (admitted) atomicMin(reinterpret_cast<long long*>(&L.counters[2]), (long long)t0);
-        atomicMax(reinterpret_cast<long long*>(&L.counters[3]), (long long)t1);
     }
-    KlLaunchRec* r = L.rec;
+    if (F.counters) {
+        atomicAdd(&F.counters[1], (unsigned long long)executed);
+        if (exh) {
+            atomicAdd(&F.counters[0], 1ull);
+            atomicAdd(&F.counters[4], F.tag);
+        }
+        if (admitted) atomicMin(reinterpret_cast<long long*>(&F.counters[2]), (long long)t0);
+        atomicMax(reinterpret_cast<long long*>(&F.counters[3]), (long long)t1);
+    }
+    KlLaunchRec* r = F.rec;
     if (r) {
         r->start = start;
         r->end = lim;
@@ -106,32 +123,43 @@ __device__ void finalize_launch(const KlLaunch& L, uint32_t len) {
     }
 }
 
-// Join the grid's epoch (false: the epoch is closed or another epoch is current -> exit).
-__device__ bool join_epoch(KlCtl* ctl, uint32_t epoch) {
-    unsigned long long j = atomicAdd(&ctl->join, 0ull);
-    for (;;) {
-        if (kl_j_closed(j) || kl_j_epoch(j) != (epoch & 0x7fu)) return false;
-        const unsigned long long prev = atomicCAS(&ctl->join, j, j + 1ull);
-        if (prev == j) return true;
-        j = prev;
-    }
+// Leave the epoch; the block that brings the count to zero closes and finalizes it once its range
+// is finished (exhausted, or stopped and drained to the boundary).
+__device__ void leave_epoch(KlCtl* ctl) {
+    __threadfence();
+    const unsigned long long j = atomicAdd(&ctl->join, ~0ull) - 1ull;   // count - 1
+    if (kl_j_count(j) != 0 || kl_j_closed(j)) return;
+    const uint32_t len = ctl->len;
+    const unsigned long long w = atomicAdd(&ctl->word, 0ull);
+    if (kl_w_next(w) < word_limit(w, len)) return;   // not finished: live blocks will come
+    if (atomicCAS(&ctl->join, j, j | KL_J_CLOSED) == j) finalize_epoch(ctl, len, j);
 }
 
-// Leave the epoch; the block that brings the count to zero closes and finalizes it.
-__device__ void leave_epoch(const KlLaunch& L, uint32_t len) {
+// Join the grid's epoch (false: closed, another epoch, or a recycled slot -> exit untouched).
+__device__ bool join_epoch(const KlLaunch& L) {
     KlCtl* ctl = L.ctl;
+    const unsigned long long j0 = *(volatile unsigned long long*)&ctl->join;
+    if (kl_j_closed(j0) || kl_j_ticket(j0) != L.ticket) return false;   // late block: no atomics
+    const unsigned long long j = atomicAdd(&ctl->join, 1ull);
+    if (kl_j_closed(j) || kl_j_ticket(j) != L.ticket) {
+        // raced with a close/reopen: undo the stray count (and close if it was the last)
+        leave_epoch(ctl);
+        return false;
+    }
+    KlFin* f = &ctl->fin;
+    if (f->rec != L.rec) f->rec = L.rec;
+    if (f->counters != L.counters) f->counters = L.counters;
+    if (f->tag != L.tag) f->tag = L.tag;
+    if (f->n_sms != L.n_sms) f->n_sms = L.n_sms;
     __threadfence();
-    unsigned long long j = atomicAdd(&ctl->join, ~0ull) - 1ull;   // count - 1
-    if (kl_j_count(j) != 0) return;
-    const unsigned long long closed = j | (1ull << 39);
-    if (atomicCAS(&ctl->join, j, closed) == j) finalize_launch(L, len);
+    return true;
 }
 
 // Occupancy cap in force for this grid's epoch: the host re-tune if it names the epoch, else the
 // grid's own cap (0 = uncapped).
 __device__ __forceinline__ uint32_t cap_now(const KlLaunch& L, const KlCtl* ctl) {
     const unsigned long long t = ctl->tune;
-    if ((t & 1ull) && ((t >> 1) & 0x7full) == (L.epoch & 0x7fu)) return (uint32_t)(t >> 32);
+    if ((t & 1ull) && ((t >> 1) & 0x7full) == (L.ticket & 0x7fu)) return (uint32_t)(t >> 32);
     return L.cap;
 }
 
@@ -153,7 +181,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
     bool joined = false;
     if (threadIdx.x == 0) {
         uint32_t adm = 0;
-        joined = join_epoch(ctl, L.epoch);
+        joined = join_epoch(L);
         if (joined) {
             sm = smid_u32();
             const uint32_t cap = cap_now(L, ctl);
@@ -226,7 +254,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
             if (counted) atomicSub(&ctl->sm_count[sm], 1u);
         }
     }
-    if (threadIdx.x == 0 && joined) leave_epoch(L, len);
+    if (threadIdx.x == 0 && joined) leave_epoch(ctl);
 }
 
 // Plain grid: blockIdx rectified by the slice offset.

@@ -67,6 +67,7 @@ struct Inst {
     int slot = -1;
     uint32_t next = 0;          // host view: first virtual block not yet retired
     uint32_t epoch = 0;         // launches issued (matches the control word's epoch mod 128)
+    uint32_t gen = 0;           // generation of its control-block slot (membership ticket)
     bool drained = false;       // no more thread blocks (out of R)
     bool finished = false;      // drained and every launch retired
     Launch* inflight = nullptr; // at most one launch in flight per kernel
@@ -148,6 +149,7 @@ struct kl_ctx {
     uint32_t* init_pinned = nullptr;   // mapped (slot, len) pairs awaiting k_ctl_init (2 buffers)
     uint32_t* init_base = nullptr;
     int n_init = 0;
+    uint32_t slot_gen[kCtlPool] = {};
     std::vector<std::unique_ptr<Inst>> insts;
     std::unordered_map<uint64_t, Inst*> by_id;
     std::vector<Inst*> R;              // pending set, arrival order (Alg.1 l.1)
@@ -515,18 +517,20 @@ int waves_of(const kl_ctx* c, const Decision& d) {
 kl_status flush_ctl_init(kl_ctx* ctx) {
     if (ctx->n_init == 0 && !ctx->reset_pending) return KL_OK;
     int rc = kl_dev_ctl_init(ctx->ctl_pool, ctx->init_pinned, ctx->n_init,
-                             ctx->reset_pending ? reinterpret_cast<unsigned long long*>(ctx->counters) : nullptr, ctx->ctrl);
+                             ctx->reset_pending ? reinterpret_cast<unsigned long long*>(ctx->counters) : nullptr,
+                             ctx->stopper);
     if (rc) return ctx->fail(KL_ECUDA, "ctl init: %s", cudaGetErrorString((cudaError_t)rc));
     ctx->st.device_launches++;
-    KL_CUDA(cudaEventRecord(ctx->init_ev, ctx->ctrl));
+    // on the stopper stream: ordered after every stop / re-tune copy aimed at the slots' previous
+    // kernels; the launch streams wait for it
+    KL_CUDA(cudaEventRecord(ctx->init_ev, ctx->stopper));
     for (int i = 0; i < kPool; ++i) KL_CUDA(cudaStreamWaitEvent(ctx->pool[i], ctx->init_ev, 0));
-    KL_CUDA(cudaStreamWaitEvent(ctx->stopper, ctx->init_ev, 0));
     // the kernel reads the mapped list: switch to the other buffer (waited on before reuse)
     const int b = ctx->init_buf;
-    KL_CUDA(cudaEventRecord(ctx->init_done[b], ctx->ctrl));
+    KL_CUDA(cudaEventRecord(ctx->init_done[b], ctx->stopper));
     ctx->init_used[b] = true;
     ctx->init_buf = b ^ 1;
-    ctx->init_pinned = ctx->init_base + (size_t)ctx->init_buf * 2 * kCtlPool;
+    ctx->init_pinned = ctx->init_base + (size_t)ctx->init_buf * 3 * kCtlPool;
     if (ctx->init_used[ctx->init_buf]) KL_CUDA(cudaEventSynchronize(ctx->init_done[ctx->init_buf]));
     ctx->n_init = 0;
     ctx->reset_pending = false;
@@ -562,7 +566,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     P.cap = cap;
     P.chunk = (uint32_t)(ctx->cfg.chunk > 0 ? ctx->cfg.chunk : inf.default_chunk);
     P.n_sms = (uint32_t)ctx->n_sms;
-    P.epoch = L->epoch & 0x7fu;
+    P.ticket = kl_ticket(k->gen, L->epoch);
     P.rec = rec;
     P.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
     P.audit = k->audit;
@@ -934,7 +938,7 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaEventCreateWithFlags(&ctx->tune_ev, cudaEventDisableTiming));
             KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
             KL_CUDA(cudaMemset(ctx->ctl_pool, 0, sizeof(KlCtl) * kCtlPool));
-            KL_CUDA(cudaHostAlloc(&ctx->init_base, sizeof(uint32_t) * 4 * kCtlPool, cudaHostAllocMapped));
+            KL_CUDA(cudaHostAlloc(&ctx->init_base, sizeof(uint32_t) * 6 * kCtlPool, cudaHostAllocMapped));
             ctx->init_pinned = ctx->init_base;
             for (auto& e : ctx->init_done) KL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocDefault));
@@ -1026,8 +1030,10 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
             return ctx->fail(KL_EINVAL, "cannot prepare args of kind %d", d->kind);
         k->slot = ctx->free_slots.back();
         ctx->free_slots.pop_back();
-        ctx->init_pinned[2 * ctx->n_init] = (uint32_t)k->slot;
-        ctx->init_pinned[2 * ctx->n_init + 1] = d->grid_blocks;
+        k->gen = ++ctx->slot_gen[k->slot];
+        ctx->init_pinned[3 * ctx->n_init] = (uint32_t)k->slot;
+        ctx->init_pinned[3 * ctx->n_init + 1] = d->grid_blocks;
+        ctx->init_pinned[3 * ctx->n_init + 2] = k->gen;
         ctx->n_init++;
         if (ctx->cfg.audit) {
             KL_CUDA(cudaMalloc(&k->audit, sizeof(uint32_t) * d->grid_blocks));
