@@ -56,6 +56,7 @@ def parse():
                     help="slice ratio per pair: 1 argmax CP over all co-schedules (FindCoSchedule l.3-4, "
                          "default), 0 argmin dT (Eq.8 balanced ratio)")
     ap.add_argument("--cp-min", type=float, default=None)
+    ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
     return ap.parse_args()
@@ -261,6 +262,7 @@ def run_kernelet(args, rank, world, local_rank):
 
     step_ms, dev_ms, cnts = [], [], []
     dec0 = ctx.stats().decisions
+    dl0 = ctx.stats().device_launches
     with Clocks(local_rank) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -277,7 +279,17 @@ def run_kernelet(args, rank, world, local_rank):
         barrier()
     trace = ctx.trace()[n_trace0:]
     st = ctx.stats()
-    launches = len(trace) + 2 * args.steps      # lane launches + model batch + ctl init per step
+    launches = st.device_launches - dl0         # slice grids, top-ups, model batches, ctl inits
+    if args.trace_out and rank == 0:
+        last = trace[-max(1, len(trace) // args.steps):]
+        z = min(t.t0_ns for t in last if t.admitted)
+        with open(args.trace_out, "w") as f:
+            for t in sorted(last, key=lambda t: t.t0_ns):
+                f.write(json.dumps({"kind": K.KINDS[t.kind], "cap": t.cap, "cap_max": t.cap_max, "grids": t.grids,
+                                    "start": t.start, "end": t.end, "exh": t.exhausted, "adm": t.admitted,
+                                    "t0_us": round((t.t0_ns - z) / 1e3, 1), "t1_us": round((t.t1_ns - z) / 1e3, 1),
+                                    "partner": K.KINDS[t.partner_kind] if t.partner_kind >= 0 else None,
+                                    "cp": round(t.cp, 3), "dec": t.phase}) + "\n")
     lease_conflicts = check_leases(trace, ids, lease)
     t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -299,6 +311,8 @@ def run_kernelet(args, rank, world, local_rank):
         "parity": parity,
         "setup_s": round(t_gen, 1),
         "lease_conflicts": lease_conflicts,
+        "retunes_per_step": st.retunes / max(1, args.warmup + args.steps),
+        "stops_per_step": st.stops / max(1, args.warmup + args.steps),
         "host_decide_ms_per_step": st.decide_ns / 1e6 / max(1, args.warmup + args.steps),
         "model_ms_per_step": st.model_ns / 1e6 / max(1, args.warmup + args.steps),
     }
