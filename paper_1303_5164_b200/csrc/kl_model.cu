@@ -1,9 +1,9 @@
 // kl_model.cu -- batched Markov warp-state model + fused greedy selection (product path).
 //
-// One CTA per candidate (kind1, b1, kind2, b2).  Per candidate it builds the two solo chains and
-// the joint chain of PAPER.md §4.4 in shared memory (fp64), solves each steady state with GTH
-// (Grassmann-Taksar-Heyman state reduction: subtraction-free, so no pivoting is needed), and
-// reduces Eq.4-8 and Eq.1.  The CTA that finishes last runs FindCoSchedule's selection (a9):
+// One CTA (8 warps) per candidate (kind1, b1, kind2, b2).  Per candidate it builds the two solo
+// chains and the joint chain of PAPER.md §4.4 in shared memory (fp64, one warp per state row),
+// solves each steady state with GTH (Grassmann-Taksar-Heyman state reduction: subtraction-free,
+// so no pivoting is needed; one barrier per eliminated state), and reduces Eq.4-8 and Eq.1.  The CTA that finishes last runs FindCoSchedule's selection (a9):
 // per pair argmin dT over its maximal splits, then argmax CP over pairs.
 //
 // Readings: R1 P_ir = min(1, max(#ready,1)/L); R2 L(n) = L0 + a0 n/B + b0 with n
@@ -17,12 +17,11 @@ namespace {
 
 constexpr int kMaxW = 16;                 // virtual-SM warps (64 warps / 4 schedulers)
 constexpr int kMaxS = (kMaxW / 2 + 1) * (kMaxW / 2 + 1);   // 81 joint states at W_v = 16
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;
 
 // Binomial coefficients C(n,k), n <= 16 (exact in double).
 __constant__ double c_binom[17][17];
 
-__device__ __forceinline__ double binom_d(int n, int k) { return (k < 0 || k > n) ? 0.0 : c_binom[n][k]; }
 
 __device__ double latency(const KlModelCfg& c, double n, int idle) {
     if (c.latency_mode == 1) return c.L0 + c.B / (c.a0 * (double)(idle > 1 ? idle : 1)) + c.b0;
@@ -53,29 +52,43 @@ __device__ bool p_ir(const KlModelCfg& c, double R, int idle, double n, double* 
     return true;
 }
 
-// One-kernel transition row from i idle of w (Eq.2 summed with binomial weights, R3).  The
-// powers p^a (1-p)^(i-a) are built by repeated multiplication (no pow()), in the same (a, b)
-// accumulation order as the oracle.
-__device__ void row_of(int w, int i, double pir, double rm, double* row) {
-    double pw[kMaxW + 1], qw[kMaxW + 1], rw[kMaxW + 1], sw[kMaxW + 1];
-    pw[0] = qw[0] = rw[0] = sw[0] = 1.0;
-    for (int t = 1; t <= w; ++t) {
-        pw[t] = pw[t - 1] * pir;
-        qw[t] = qw[t - 1] * (1.0 - pir);
-        rw[t] = rw[t - 1] * rm;
-        sw[t] = sw[t - 1] * (1.0 - rm);
+// One-kernel transition row from i idle of w (Eq.2 summed with binomial weights, R3), one warp:
+// lane a holds Binomial(i, pir) mass at a returns, lane b Binomial(w - i, rm) mass at b stalls;
+// lane j returns T(i -> j) = sum_a pA[a] pB[j - i + a] (0 for j > w).  Powers by repeated
+// multiplication (no pow()); binomial coefficients from the exact table in shared memory.
+__device__ double warp_row(int w, int i, double pir, double rm, const double (*binom)[kMaxW + 1]) {
+    const int lane = threadIdx.x & 31, nr = w - i;
+    double pa = 0.0, pb = 0.0;
+    if (lane <= i) {
+        double x = 1.0;
+        for (int t = 0; t < lane; ++t) x *= pir;
+        for (int t = 0; t < i - lane; ++t) x *= (1.0 - pir);
+        pa = binom[i][lane] * x;
     }
-    for (int j = 0; j <= w; ++j) row[j] = 0.0;
-    const int nr = w - i;
+    if (lane <= nr) {
+        double x = 1.0;
+        for (int t = 0; t < lane; ++t) x *= rm;
+        for (int t = 0; t < nr - lane; ++t) x *= (1.0 - rm);
+        pb = binom[nr][lane] * x;
+    }
+    double row = 0.0;
     for (int a = 0; a <= i; ++a) {
-        const double pa = binom_d(i, a) * pw[a] * qw[i - a];
-        for (int b = 0; b <= nr; ++b) row[i - a + b] += pa * (binom_d(nr, b) * rw[b] * sw[nr - b]);
+        const double va = __shfl_sync(0xffffffffu, pa, a);
+        const int bb = lane - i + a;
+        const double vb = __shfl_sync(0xffffffffu, pb, bb & 31);
+        if (bb >= 0 && bb <= nr) row += va * vb;
     }
+    return lane <= w ? row : 0.0;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
 __device__ double block_sum(double v, double* red) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    v = warp_sum(v);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
     if (l == 0) red[w] = v;
@@ -85,74 +98,112 @@ __device__ double block_sum(double v, double* red) {
     return s;
 }
 
-// GTH steady state of the S x S row-stochastic matrix P (destroyed).  Returns false when a
-// pivot sum is zero (reducible chain).
-__device__ bool gth(double* P, int S, double* pi, double* red, int* flag) {
-    for (int k = S - 1; k >= 1; --k) {
-        double part = 0.0;
-        for (int j = threadIdx.x; j < k; j += kThreads) part += P[k * S + j];
-        double s = block_sum(part, red);
-        if (!(s > 0.0)) return false;
-        for (int i = threadIdx.x; i < k; i += kThreads) P[i * S + k] /= s;
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < k * k; idx += kThreads) {
-            int i = idx / k, j = idx - i * k;
-            P[i * S + j] += P[i * S + k] * P[k * S + j];
-        }
-        __syncthreads();
-    }
-    // back substitution by warp 0: pi_j = sum_{i<j} pi_i P[i][j]
-    if (threadIdx.x < 32) {
-        if (threadIdx.x == 0) pi[0] = 1.0;
-        __syncwarp();
-        for (int j = 1; j < S; ++j) {
-            double part = 0.0;
-            for (int i = threadIdx.x; i < j; i += 32) part += pi[i] * P[i * S + j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            if (threadIdx.x == 0) pi[j] = part;
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    double part = 0.0;
-    for (int i = threadIdx.x; i < S; i += kThreads) part += pi[i];
-    double tot = block_sum(part, red);
-    for (int i = threadIdx.x; i < S; i += kThreads) pi[i] /= tot;
-    __syncthreads();
-    (void)flag;
-    return true;
-}
+// Steady state and IPCs of the chain of kernel A at wa warps (and kernel B at wb warps; wb = 0,
+// kb = null: solo chain).  States (p, q) = idle warps of A and B, S = (wa+1)(wb+1); the row of
+// (p, q) is the outer product of the two one-kernel rows under the state's shared round R and
+// latency (R4/R5).  The stationary distribution is GTH state reduction (subtraction-
+// free) with one barrier per eliminated state: rows are owned by warps, and the owner of row
+// k-1 produces the next pivot sum while updating it.  Returns KL_OK / KL_EINFEASIBLE (guard
+// L > W, R22) / KL_ENUMERIC (zero pivot: reducible chain).
+struct ChainOut { double ipc_a, ipc_b; };
 
-// Solo IPC (Eq.4, denominator = elapsed cycles sum_i g_i R_i) of a kind at w warps on the
-// virtual SM.
-__device__ bool solo_ipc(const KlModelKind& k, int w, const KlModelCfg& c, double* P, double* pi,
-                         double* red, double* out) {
-    const int S = w + 1;
-    __shared__ int s_ok;
-    __shared__ double s_R[kMaxW + 1];
-    if (threadIdx.x == 0) s_ok = 1;
+__device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, int wb, const KlModelCfg& c,
+                         double* P, double* pi, double* Rs, double* red, const double (*binom)[kMaxW + 1],
+                         ChainOut* out) {
+    const int nb = wb + 1, S = (wa + 1) * nb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = kThreads / 32;
+    __shared__ int s_bad;
+    __shared__ double s_piv[2];
+    if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < S; i += kThreads) {
-        double pr;
-        const double R = round_dur(w - i, &k, 0, nullptr);
-        s_R[i] = R;
-        if (!p_ir(c, R, i, (double)i * k.r, &pr)) { s_ok = 0; continue; }
-        row_of(w, i, pr, k.rm, P + i * S);
+    // ---- chain build: one warp per state row
+    for (int s = warp; s < S; s += NW) {
+        const int p = s / nb, q = s - p * nb;
+        const double R = round_dur(wa - p, ka, wb - q, kb);
+        const double n = (double)p * ka->r + (kb ? (double)q * kb->r : 0.0);
+        double pr = 0.0;
+        if (!p_ir(c, R, p + q, n, &pr)) {
+            if (lane == 0) s_bad = KL_EINFEASIBLE;
+            continue;
+        }
+        if (lane == 0) Rs[s] = R;
+        const double r1 = warp_row(wa, p, pr, ka->rm, binom);
+        const double r2 = kb ? warp_row(wb, q, pr, kb->rm, binom) : (lane == 0 ? 1.0 : 0.0);
+        double* row = P + s * S;
+        for (int pp = 0; pp <= wa; ++pp) {
+            const double v1 = __shfl_sync(0xffffffffu, r1, pp);
+            if (lane <= wb) row[pp * nb + lane] = v1 * r2;
+        }
     }
     __syncthreads();
-    if (!s_ok) return false;
-    if (!gth(P, S, pi, red, nullptr)) return false;
-    double num = 0.0, den = 0.0;
-    for (int i = threadIdx.x; i < S; i += kThreads) {
-        if (i < w) num += pi[i] * (double)(w - i);
-        den += pi[i] * s_R[i];
+    if (s_bad) return s_bad;
+    // ---- GTH: for k = S-1 .. 1: s = sum_{j<k} P[k][j]; P[i][k] /= s; P[i][j] += P[i][k] P[k][j]
+    if (warp == (S - 1) % NW) {
+        double part = 0.0;
+        for (int j = lane; j < S - 1; j += 32) part += P[(S - 1) * S + j];
+        part = warp_sum(part);
+        if (lane == 0) s_piv[(S - 1) & 1] = part;
     }
-    num = block_sum(num, red);
+    __syncthreads();
+    for (int k = S - 1; k >= 1; --k) {
+        const double sk = s_piv[k & 1];
+        if (!(sk > 0.0)) return KL_ENUMERIC;   // uniform across the block
+        const double inv = 1.0 / sk;
+        const double* rk = P + k * S;
+        for (int i = warp; i < k; i += NW) {
+            double* ri = P + i * S;
+            const double a = ri[k] * inv;
+            double part = 0.0;
+            for (int j = lane; j < k; j += 32) {
+                const double v = fma(a, rk[j], ri[j]);
+                ri[j] = v;
+                if (j < k - 1) part += v;
+            }
+            __syncwarp();
+            if (lane == 0) ri[k] = a;
+            if (i == k - 1) {
+                part = warp_sum(part);
+                if (lane == 0) s_piv[(k - 1) & 1] = part;
+            }
+        }
+        __syncthreads();
+    }
+    // back substitution by warp 0: pi_0 = 1, pi_j = sum_{i<j} pi_i P[i][j] (column accumulators
+    // m = lane + 32 t held in registers)
+    if (warp == 0) {
+        double acc[3] = {0.0, 0.0, 0.0};
+        double tot = 0.0;
+        for (int j = 0; j < S; ++j) {
+            const int t = j >> 5, src = j & 31;
+            const double mine = t == 0 ? acc[0] : (t == 1 ? acc[1] : acc[2]);
+            const double pj = j == 0 ? 1.0 : __shfl_sync(0xffffffffu, mine, src);
+            tot += pj;
+            if (lane == 0) pi[j] = pj;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int m = lane + 32 * u;
+                if (m > j && m < S) acc[u] = fma(pj, P[j * S + m], acc[u]);
+            }
+        }
+        if (lane == 0) red[8] = tot;
+    }
+    __syncthreads();
+    const double tot = red[8];
+    double den = 0.0, na = 0.0, nbs = 0.0;
+    for (int s = threadIdx.x; s < S; s += kThreads) {
+        const int p = s / nb, q = s - p * nb;
+        const double g = pi[s] / tot;
+        den += g * Rs[s];
+        if (p < wa) na += g * (double)(wa - p);
+        if (q < wb) nbs += g * (double)(wb - q);
+    }
     den = block_sum(den, red);
-    *out = num / den;
+    na = block_sum(na, red);
+    nbs = block_sum(nbs, red);
+    out->ipc_a = na / den;
+    out->ipc_b = nbs / den;
     __syncthreads();
-    return true;
+    return KL_OK;
 }
 
 __device__ __forceinline__ double band(double x, double y) {
@@ -185,10 +236,14 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     extern __shared__ __align__(16) double smem_d[];
     double* P = smem_d;                    // kMaxS * kMaxS
     double* pi = P + kMaxS * kMaxS;        // kMaxS
-    double* R = pi + kMaxS;                // kMaxS
-    double* red = R + kMaxS;               // 8
-    __shared__ int s_ok, s_last;
+    double* Rs = pi + kMaxS;               // kMaxS
+    double* red = Rs + kMaxS;              // 16
+    __shared__ double s_binom[kMaxW + 1][kMaxW + 1];
+    __shared__ int s_last;
     __shared__ int s_best_pair[128];
+    for (int x = threadIdx.x; x < (kMaxW + 1) * (kMaxW + 1); x += kThreads)
+        s_binom[x / (kMaxW + 1)][x % (kMaxW + 1)] = c_binom[x / (kMaxW + 1)][x % (kMaxW + 1)];
+    __syncthreads();
 
     const KlCand cd = cands[blockIdx.x];
     const KlModelKind k1 = kinds[cd.k1], k2 = kinds[cd.k2];
@@ -203,43 +258,22 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     if (w1 < 1 || (w2 < 1 && !solo_query) || w1 + w2 > cfg.W || ws1 < 1 || ws1 > cfg.W || ws2 < 1 ||
         ws2 > cfg.W || (w1 + 1) * (w2 + 1) > kMaxS || cfg.W > kMaxW)
         status = KL_EINFEASIBLE;
-    if (status == 0) {
-        if (!solo_ipc(k1, ws1, cfg, P, pi, red, &out.solo1) || !solo_ipc(k2, ws2, cfg, P, pi, red, &out.solo2))
-            status = KL_ENUMERIC;
-    }
-    if (status == 0) {
-        const int S = (w1 + 1) * (w2 + 1);
-        if (threadIdx.x == 0) s_ok = 1;
-        __syncthreads();
-        // joint chain: row (p,q) = outer product of the two one-kernel rows, both
-        // evaluated with the shared round duration and latency of state (p,q)
-        for (int s = threadIdx.x; s < S; s += kThreads) {
-            const int p = s / (w2 + 1), q = s - p * (w2 + 1);
-            double pr, r1[kMaxW + 1], r2[kMaxW + 1];
-            R[s] = round_dur(w1 - p, &k1, w2 - q, solo_query ? nullptr : &k2);
-            if (!p_ir(cfg, R[s], p + q, (double)p * k1.r + (double)q * k2.r, &pr)) { s_ok = 0; continue; }
-            row_of(w1, p, pr, k1.rm, r1);
-            row_of(w2, q, pr, k2.rm, r2);
-            for (int pp = 0; pp <= w1; ++pp)
-                for (int qq = 0; qq <= w2; ++qq) P[s * S + pp * (w2 + 1) + qq] = r1[pp] * r2[qq];
+    ChainOut co;
+    if (status == 0) {   // Eq.4 solo IPCs at b^max
+        status = chain_ipc(&k1, ws1, nullptr, 0, cfg, P, pi, Rs, red, s_binom, &co);
+        out.solo1 = co.ipc_a;
+        if (status == 0) {
+            status = chain_ipc(&k2, ws2, nullptr, 0, cfg, P, pi, Rs, red, s_binom, &co);
+            out.solo2 = co.ipc_a;
         }
-        __syncthreads();
-        if (!s_ok || !gth(P, S, pi, red, nullptr)) {
-            status = KL_ENUMERIC;
-        } else {
-            // Eq.5-7 with R_(i,j) = joint round duration (R4)
-            double den = 0.0, n1 = 0.0, n2 = 0.0;
-            for (int s = threadIdx.x; s < S; s += kThreads) {
-                const int p = s / (w2 + 1), q = s - p * (w2 + 1);
-                den += pi[s] * R[s];
-                if (p < w1) n1 += pi[s] * (double)(w1 - p);
-                if (q < w2) n2 += pi[s] * (double)(w2 - q);
-            }
-            den = block_sum(den, red);
-            n1 = block_sum(n1, red);
-            n2 = block_sum(n2, red);
-            out.ipc1 = n1 / den;
-            out.ipc2 = n2 / den;
+        if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
+    }
+    if (status == 0) {   // joint chain, Eq.5-7 with R_(i,j) = joint round duration (R4)
+        status = chain_ipc(&k1, w1, solo_query ? nullptr : &k2, solo_query ? 0 : w2, cfg, P, pi, Rs, red, s_binom, &co);
+        if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
+        if (status == 0) {
+            out.ipc1 = co.ipc_a;
+            out.ipc2 = co.ipc_b;
             out.c = out.ipc1 + out.ipc2;
             if (!solo_query) {
                 out.cp = 1.0 - 1.0 / (out.ipc1 / out.solo1 + out.ipc2 / out.solo2);   // Eq.1
@@ -296,7 +330,7 @@ int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* c
                        kl_prediction* preds, int n_pairs, const int32_t* pair_off,
                        uint32_t* done_counter, KlDecision* dec, void* stream) {
     if (cfg.n_cand <= 0) return 0;
-    const size_t smem = sizeof(double) * (kMaxS * kMaxS + 3 * kMaxS + 8);
+    const size_t smem = sizeof(double) * (kMaxS * kMaxS + 2 * kMaxS + 16);
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_model_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
