@@ -102,8 +102,8 @@ __device__ double block_sum(double v, double* red) {
 // kb = null: solo chain).  States (p, q) = idle warps of A and B, S = (wa+1)(wb+1); the row of
 // (p, q) is the outer product of the two one-kernel rows under the state's shared round R and
 // latency (R4/R5).  The stationary distribution is GTH state reduction (subtraction-
-// free) with one barrier per eliminated state: rows are owned by warps, and the owner of row
-// k-1 produces the next pivot sum while updating it.  Returns KL_OK / KL_EINFEASIBLE (guard
+// free) with one barrier per eliminated state on a 16 x 16 thread tile; the threads owning row
+// k-1 produce the next pivot sum while updating it.  Returns KL_OK / KL_EINFEASIBLE (guard
 // L > W, R22) / KL_ENUMERIC (zero pivot: reducible chain).
 struct ChainOut { double ipc_a, ipc_b; };
 
@@ -114,6 +114,7 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = kThreads / 32;
     __shared__ int s_bad;
     __shared__ double s_piv[2];
+    __shared__ double inv_s[kMaxS];
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
     // ---- chain build: one warp per state row
@@ -137,8 +138,12 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     }
     __syncthreads();
     if (s_bad) return s_bad;
-    // ---- GTH: for k = S-1 .. 1: s = sum_{j<k} P[k][j]; P[i][k] /= s; P[i][j] += P[i][k] P[k][j]
-    if (warp == (S - 1) % NW) {
+    // ---- GTH: for k = S-1 .. 1: s_k = sum_{j<k} P[k][j]; P[i][j] += (P[i][k]/s_k) P[k][j], i,j < k.
+    // 16 x 16 thread tile (rows i = ty + 16m, columns j = tx + 16n); column k is left unscaled
+    // (back substitution applies 1/s_k), and the half-warp owning row k-1 reduces the next pivot
+    // sum from its freshly updated values: one barrier per eliminated state.
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    if (warp == 0) {
         double part = 0.0;
         for (int j = lane; j < S - 1; j += 32) part += P[(S - 1) * S + j];
         part = warp_sum(part);
@@ -149,34 +154,45 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
         const double sk = s_piv[k & 1];
         if (!(sk > 0.0)) return KL_ENUMERIC;   // uniform across the block
         const double inv = 1.0 / sk;
+        if (threadIdx.x == 0) inv_s[k] = inv;
         const double* rk = P + k * S;
-        for (int i = warp; i < k; i += NW) {
+        double pk[kMaxS / 16 + 1];
+#pragma unroll
+        for (int n = 0; n < kMaxS / 16 + 1; ++n) {
+            const int j = tx + 16 * n;
+            pk[n] = j < k ? rk[j] : 0.0;
+        }
+        double part = 0.0;
+        for (int i = ty; i < k; i += 16) {
             double* ri = P + i * S;
             const double a = ri[k] * inv;
-            double part = 0.0;
-            for (int j = lane; j < k; j += 32) {
-                const double v = fma(a, rk[j], ri[j]);
-                ri[j] = v;
-                if (j < k - 1) part += v;
+            const bool piv = (i == k - 1);
+#pragma unroll
+            for (int n = 0; n < kMaxS / 16 + 1; ++n) {
+                const int j = tx + 16 * n;
+                if (j < k) {
+                    const double v = fma(a, pk[n], ri[j]);
+                    ri[j] = v;
+                    if (piv && j < k - 1) part += v;
+                }
             }
-            __syncwarp();
-            if (lane == 0) ri[k] = a;
-            if (i == k - 1) {
-                part = warp_sum(part);
-                if (lane == 0) s_piv[(k - 1) & 1] = part;
-            }
+        }
+        if (warp == (((k - 1) & 15) >> 1)) {   // warp-uniform: holds row k-1 in one half
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (tx == 0 && ty == ((k - 1) & 15)) s_piv[(k - 1) & 1] = part;
         }
         __syncthreads();
     }
-    // back substitution by warp 0: pi_0 = 1, pi_j = sum_{i<j} pi_i P[i][j] (column accumulators
-    // m = lane + 32 t held in registers)
+    // back substitution by warp 0: pi_0 = 1, pi_j = (1/s_j) sum_{i<j} pi_i P[i][j] (column
+    // accumulators m = lane + 32 t held in registers)
     if (warp == 0) {
         double acc[3] = {0.0, 0.0, 0.0};
         double tot = 0.0;
         for (int j = 0; j < S; ++j) {
             const int t = j >> 5, src = j & 31;
             const double mine = t == 0 ? acc[0] : (t == 1 ? acc[1] : acc[2]);
-            const double pj = j == 0 ? 1.0 : __shfl_sync(0xffffffffu, mine, src);
+            const double pj = j == 0 ? 1.0 : __shfl_sync(0xffffffffu, mine, src) * inv_s[j];
             tot += pj;
             if (lane == 0) pi[j] = pj;
 #pragma unroll
