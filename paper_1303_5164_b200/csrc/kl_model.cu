@@ -113,7 +113,7 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     const int nb = wb + 1, S = (wa + 1) * nb;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, NW = kThreads / 32;
     __shared__ int s_bad;
-    __shared__ double s_piv[2];
+    __shared__ double s_piv[2], s_inv[2];
     __shared__ double inv_s[kMaxS];
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
@@ -147,13 +147,16 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
         double part = 0.0;
         for (int j = lane; j < S - 1; j += 32) part += P[(S - 1) * S + j];
         part = warp_sum(part);
-        if (lane == 0) s_piv[(S - 1) & 1] = part;
+        if (lane == 0) {
+            s_piv[(S - 1) & 1] = part;
+            s_inv[(S - 1) & 1] = 1.0 / part;
+        }
     }
     __syncthreads();
     for (int k = S - 1; k >= 1; --k) {
         const double sk = s_piv[k & 1];
         if (!(sk > 0.0)) return KL_ENUMERIC;   // uniform across the block
-        const double inv = 1.0 / sk;
+        const double inv = s_inv[k & 1];
         if (threadIdx.x == 0) inv_s[k] = inv;
         const double* rk = P + k * S;
         double pk[kMaxS / 16 + 1];
@@ -162,25 +165,31 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
             const int j = tx + 16 * n;
             pk[n] = j < k ? rk[j] : 0.0;
         }
-        double part = 0.0;
         for (int i = ty; i < k; i += 16) {
             double* ri = P + i * S;
             const double a = ri[k] * inv;
-            const bool piv = (i == k - 1);
 #pragma unroll
             for (int n = 0; n < kMaxS / 16 + 1; ++n) {
                 const int j = tx + 16 * n;
-                if (j < k) {
-                    const double v = fma(a, pk[n], ri[j]);
-                    ri[j] = v;
-                    if (piv && j < k - 1) part += v;
-                }
+                if (j < k) ri[j] = fma(a, pk[n], ri[j]);
             }
         }
         if (warp == (((k - 1) & 15) >> 1)) {   // warp-uniform: holds row k-1 in one half
+            double part = 0.0;
+            if (ty == ((k - 1) & 15)) {         // re-read this thread's own updates of row k-1
+                const double* rp = P + (k - 1) * S;
+#pragma unroll
+                for (int n = 0; n < kMaxS / 16 + 1; ++n) {
+                    const int j = tx + 16 * n;
+                    if (j < k - 1) part += rp[j];
+                }
+            }
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            if (tx == 0 && ty == ((k - 1) & 15)) s_piv[(k - 1) & 1] = part;
+            if (tx == 0 && ty == ((k - 1) & 15)) {
+                s_piv[(k - 1) & 1] = part;
+                s_inv[(k - 1) & 1] = 1.0 / part;
+            }
         }
         __syncthreads();
     }
