@@ -4,9 +4,11 @@
 set -u
 mkdir -p gpurun_out
 echo "== gpu tests"; timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
-echo "== calibrate"; timeout 900 python tools/calibrate.py run gpurun_out/kl_profile_b200.json > gpurun_out/calib.log 2>&1
-grep -E " fit |wrote" gpurun_out/calib.log | cut -c1-160
-cp gpurun_out/kl_profile_b200.json profiles/kl_profile_b200.json
+if [ "${CALIB:-0}" = "1" ]; then
+  echo "== calibrate"; timeout 900 python tools/calibrate.py run gpurun_out/kl_profile_b200.json > gpurun_out/calib.log 2>&1
+  grep -E " fit |wrote" gpurun_out/calib.log | cut -c1-160
+  cp gpurun_out/kl_profile_b200.json profiles/kl_profile_b200.json
+fi
 echo "== bench c2"; timeout 900 python bench.py --json-out gpurun_out/bench_c2.json > gpurun_out/bench_c2.log 2>&1
 python - <<'PY'
 import json
@@ -24,9 +26,11 @@ echo "== model error"; timeout 900 python tools/model_error.py gpurun_out/model_
 python -c "import json;print(json.load(open('gpurun_out/model_error.json'))['summary'])" | cut -c1-300
 echo "== ncu launch list"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-baselines --no-cpu > gpurun_out/ncu_bench.log 2>&1
-echo "== ncu full"
-for k in MRIQ MM ST PC BS; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_plain -s 1 -c 1 -o gpurun_out/prof_$k python tools/prof_target.py $k plain > gpurun_out/ncu_full_$k.log 2>&1
+echo "== ncu full (the persistent slice-launcher variant the bench runs, second launch)"
+for k in MRIQ MM ST PC BS TEA SAD SPMV; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_persistent -s 1 -c 1 -o gpurun_out/prof_$k python tools/prof_target.py $k sched > gpurun_out/ncu_full_$k.log 2>&1
 done
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_model_batch -c 1 -o gpurun_out/prof_MODEL python tools/model_bench.py 1 > gpurun_out/ncu_full_MODEL.log 2>&1
+python tools/model_bench.py 20 > gpurun_out/model_bench.json
 python tools/ncu_summary.py gpurun_out/ncu_summary.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
 echo "== done"; ls gpurun_out
