@@ -22,7 +22,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRC = [os.path.join(_HERE, f) for f in ("kernels.c", "model.c")]
+_SRC = [os.path.join(_HERE, f) for f in ("kernels.c", "model.c", "model3.c")]
 
 
 def build(force: bool = False) -> str:
@@ -56,6 +56,12 @@ class SmCfg(C.Structure):
 class KModel(C.Structure):
     _fields_ = [("rm", C.c_double), ("r", C.c_double), ("ipb", C.c_double), ("wpb", C.c_int),
                 ("pi", C.c_double), ("pipe", C.c_int)]
+
+
+class KModel3(C.Structure):
+    """f1 three-state kind descriptor (oracle/model3.c, reading R27)."""
+    _fields_ = [("rm", C.c_double), ("r", C.c_double), ("uc", C.c_double), ("ru", C.c_double),
+                ("ipb", C.c_double), ("wpb", C.c_int), ("pi", C.c_double), ("pipe", C.c_int)]
 
 
 class Pred(C.Structure):
@@ -97,6 +103,14 @@ def _declare(L):
     L.or_solo_ipc.restype = C.c_double
     L.or_solo_ipc.argtypes = [C.POINTER(KModel), C.c_int, C.c_int, C.POINTER(SmCfg),
                               C.POINTER(C.c_int)]
+    L.or3_nstates.argtypes = [C.c_int]
+    L.or3_row.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _D]
+    L.or3_build.argtypes = [C.POINTER(KModel3), C.c_int, C.POINTER(KModel3), C.c_int, C.POINTER(SmCfg), _D, _D]
+    L.or3_ipc.argtypes = [C.c_int, C.c_int, C.c_int, _D, _D, _D, _D]
+    L.or3_solo_ipc.restype = C.c_double
+    L.or3_solo_ipc.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.POINTER(SmCfg), C.POINTER(C.c_int)]
+    L.or3_predict.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.POINTER(KModel3), C.c_int, C.c_int,
+                              C.c_int, C.POINTER(SmCfg), C.POINTER(Pred)]
     L.or_fits.argtypes = [C.POINTER(SmRes), C.POINTER(KRes), C.c_int, C.POINTER(KRes), C.c_int]
     L.or_max_blocks.argtypes = [C.POINTER(SmRes), C.POINTER(KRes)]
     L.or_pruned.argtypes = [C.c_double] * 6
@@ -290,6 +304,58 @@ def predict(k1, b1, b1max, k2, b2, b2max, nsched, cfg) -> Pred:
     lib().or_predict(C.byref(k1), b1, b1max, C.byref(k2), b2, b2max, nsched, C.byref(cfg),
                      C.byref(out))
     return out
+
+
+# ---- f1: three-state model (oracle/model3.c, reading R27) ---------------------
+def kmodel3(rm, r=1.0, uc=0.0, ru=None, ipb=1000.0, wpb=4, pi=1.0, pipe=0):
+    return KModel3(rm, r, uc, r if ru is None else ru, ipb, wpb, pi, pipe)
+
+
+def nstates3(w):
+    return lib().or3_nstates(w)
+
+
+def row3(k, w, c, u, pc, pu):
+    r = np.zeros(nstates3(w))
+    lib().or3_row(C.byref(k), w, c, u, pc, pu, _dptr(r))
+    return r
+
+
+def build3(k1, w1, cfg, k2=None, w2=0):
+    S = nstates3(w1) * (nstates3(w2) if k2 is not None else 1)
+    P = np.zeros((S, S))
+    R = np.zeros(S)
+    rc = lib().or3_build(C.byref(k1), w1, C.byref(k2) if k2 is not None else None, w2 if k2 is not None else 0,
+                         C.byref(cfg), _dptr(P), _dptr(R))
+    if rc:
+        raise ValueError("latency guard L > W failed (R22)")
+    return P, R
+
+
+def ipc3(w1, pi, R, w2=None):
+    a, b = C.c_double(), C.c_double()
+    lib().or3_ipc(w1, w2 or 0, 1 if w2 is not None else 0, _dptr(np.ascontiguousarray(pi)),
+                  _dptr(np.ascontiguousarray(R)), C.byref(a), C.byref(b))
+    return (a.value, b.value) if w2 is not None else a.value
+
+
+def states3(w):
+    """(c, u) of every state index of one kernel (model3.c idx3 order)."""
+    return [(c, u) for c in range(w + 1) for u in range(w - c + 1)]
+
+
+def predict3(k1, b1, b1max, k2, b2, b2max, nsched, cfg) -> Pred:
+    out = Pred()
+    lib().or3_predict(C.byref(k1), b1, b1max, C.byref(k2), b2, b2max, nsched, C.byref(cfg), C.byref(out))
+    return out
+
+
+def solo_ipc3(k, b, nsched, cfg):
+    st = C.c_int()
+    v = lib().or3_solo_ipc(C.byref(k), b, nsched, C.byref(cfg), C.byref(st))
+    if st.value:
+        raise ValueError(f"solo three-state model failed ({st.value})")
+    return v
 
 
 def solo_ipc(k, b, nsched, cfg):

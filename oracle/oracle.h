@@ -93,6 +93,26 @@ void or_predict(const or_kmodel* k1, int b1, int b1max, const or_kmodel* k2, int
 double or_solo_ipc(const or_kmodel* k, int b, int nsched, const or_smcfg* c, int* status);
 
 /* ---------------- O3: occupancy and pruning ---------------------------- */
+/* ---------------- f1: three-state (coalesced / uncoalesced) model, P:1000-1019 (model3.c) ------ */
+typedef struct {
+    double rm;          /* memory instruction ratio */
+    double r;           /* requests per coalesced memory instruction */
+    double uc;          /* fraction of memory instructions that are uncoalesced */
+    double ru;          /* requests per uncoalesced memory instruction */
+    double ipb;         /* warp instructions per block (Eq.8) */
+    int wpb;            /* warps per block */
+    double pi;          /* pipe ceiling (R26) */
+    int pipe;
+} or_kmodel3;
+int or3_nstates(int w);
+void or3_row(const or_kmodel3* k, int w, int c, int u, double pc, double pu, double* row);
+int or3_build(const or_kmodel3* k1, int w1, const or_kmodel3* k2, int w2, const or_smcfg* cfg, double* P,
+              double* R);
+void or3_ipc(int w1, int w2, int joint, const double* pi, const double* R, double* ipc1, double* ipc2);
+double or3_solo_ipc(const or_kmodel3* k, int b, int nsched, const or_smcfg* cfg, int* status);
+void or3_predict(const or_kmodel3* k1, int b1, int b1max, const or_kmodel3* k2, int b2, int b2max, int nsched,
+                 const or_smcfg* cfg, or_pred* out);
+
 typedef struct { int max_warps, max_blocks, max_regs, max_smem, max_tmem_cols, reg_unit; } or_smres;
 typedef struct { int wpb, regs, smem, tmem; } or_kres;
 /* Resident blocks of k1 (b1) and k2 (b2) fit one SM?  Returns 0 or a code naming the binding
