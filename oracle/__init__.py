@@ -61,7 +61,7 @@ class KModel(C.Structure):
 class KModel3(C.Structure):
     """f1 three-state kind descriptor (oracle/model3.c, reading R27)."""
     _fields_ = [("rm", C.c_double), ("r", C.c_double), ("uc", C.c_double), ("ru", C.c_double),
-                ("ipb", C.c_double), ("wpb", C.c_int), ("pi", C.c_double), ("pipe", C.c_int)]
+                ("ipb", C.c_double), ("wpb", C.c_int), ("pi", C.c_double), ("pipe", C.c_int), ("g", C.c_int)]
 
 
 class Pred(C.Structure):
@@ -107,6 +107,7 @@ def _declare(L):
     L.or3_row.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _D]
     L.or3_build.argtypes = [C.POINTER(KModel3), C.c_int, C.POINTER(KModel3), C.c_int, C.POINTER(SmCfg), _D, _D]
     L.or3_ipc.argtypes = [C.c_int, C.c_int, C.c_int, _D, _D, _D, _D]
+    L.or3_ipc_g.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D]
     L.or3_solo_ipc.restype = C.c_double
     L.or3_solo_ipc.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.POINTER(SmCfg), C.POINTER(C.c_int)]
     L.or3_predict.argtypes = [C.POINTER(KModel3), C.c_int, C.c_int, C.POINTER(KModel3), C.c_int, C.c_int,
@@ -307,8 +308,8 @@ def predict(k1, b1, b1max, k2, b2, b2max, nsched, cfg) -> Pred:
 
 
 # ---- f1: three-state model (oracle/model3.c, reading R27) ---------------------
-def kmodel3(rm, r=1.0, uc=0.0, ru=None, ipb=1000.0, wpb=4, pi=1.0, pipe=0):
-    return KModel3(rm, r, uc, r if ru is None else ru, ipb, wpb, pi, pipe)
+def kmodel3(rm, r=1.0, uc=0.0, ru=None, ipb=1000.0, wpb=4, pi=1.0, pipe=0, g=1):
+    return KModel3(rm, r, uc, r if ru is None else ru, ipb, wpb, pi, pipe, g)
 
 
 def nstates3(w):
@@ -332,10 +333,10 @@ def build3(k1, w1, cfg, k2=None, w2=0):
     return P, R
 
 
-def ipc3(w1, pi, R, w2=None):
+def ipc3(w1, pi, R, w2=None, g1=1, g2=1):
     a, b = C.c_double(), C.c_double()
-    lib().or3_ipc(w1, w2 or 0, 1 if w2 is not None else 0, _dptr(np.ascontiguousarray(pi)),
-                  _dptr(np.ascontiguousarray(R)), C.byref(a), C.byref(b))
+    lib().or3_ipc_g(w1, g1, w2 or 0, g2, 1 if w2 is not None else 0, _dptr(np.ascontiguousarray(pi)),
+                    _dptr(np.ascontiguousarray(R)), C.byref(a), C.byref(b))
     return (a.value, b.value) if w2 is not None else a.value
 
 

@@ -20,6 +20,12 @@
  *     round and latency (R5); IPC as Eq.4-7 with R_(i,j) the round duration.
  * With uc = 0 (or ru = r) the chain reduces exactly to the two-state chain (pinned).
  *
+ * Block granularity ("consider the thread block as a scheduling unit", reading R13):
+ * a kernel may be modelled in units of g warps that move together (g = the block's warps per
+ * virtual SM); w then counts units, a ready unit issues g instructions per round (the round and
+ * the pipe ceilings see g x ready warps), an idle unit keeps g x r (g x ru) requests outstanding,
+ * and IPC counts g instructions per ready unit.  g = 1 is the warp model.
+ *
  * One kernel's state (c, u): c coalesced-idle, u uncoalesced-idle warps, c + u <= w; index
  * idx(c, u) = sum_{c'<c} (w - c' + 1) + u.  Joint state (s1, s2) -> s1 * n2 + s2.
  */
@@ -90,6 +96,7 @@ static int lat3(const or_smcfg* cfg, const or_kmodel3* k, double R, int idle, do
 int or3_build(const or_kmodel3* k1, int w1, const or_kmodel3* k2, int w2, const or_smcfg* cfg, double* P,
               double* R) {
     const int n1 = or3_nstates(w1), n2 = k2 ? or3_nstates(w2) : 1, S = n1 * n2;
+    const int g1 = k1->g > 0 ? k1->g : 1, g2 = (k2 && k2->g > 0) ? k2->g : 1;
     double* r1 = (double*)malloc(sizeof(double) * n1);
     double* r2 = (double*)malloc(sizeof(double) * n2);
     int rc = 0;
@@ -99,9 +106,9 @@ int or3_build(const or_kmodel3* k1, int w1, const or_kmodel3* k2, int w2, const 
                 for (int u2 = 0; c2 + u2 <= (k2 ? w2 : 0) && !rc; ++u2) {
                     const int s = idx3(w1, c1, u1) * n2 + (k2 ? idx3(w2, c2, u2) : 0);
                     const int rd1 = w1 - c1 - u1, rd2 = k2 ? w2 - c2 - u2 : 0;
-                    R[s] = round3(rd1, k1, rd2, k2);
-                    const int idle = c1 + u1 + c2 + u2;
-                    const double n = c1 * k1->r + u1 * k1->ru + (k2 ? c2 * k2->r + u2 * k2->ru : 0.0);
+                    R[s] = round3(g1 * rd1, k1, g2 * rd2, k2);
+                    const int idle = g1 * (c1 + u1) + g2 * (c2 + u2);
+                    const double n = g1 * (c1 * k1->r + u1 * k1->ru) + (k2 ? g2 * (c2 * k2->r + u2 * k2->ru) : 0.0);
                     double pc1, pu1, pc2 = 0.0, pu2 = 0.0;
                     if (lat3(cfg, k1, R[s], idle, n, &pc1, &pu1) ||
                         (k2 && lat3(cfg, k2, R[s], idle, n, &pc2, &pu2))) {
@@ -121,6 +128,12 @@ int or3_build(const or_kmodel3* k1, int w1, const or_kmodel3* k2, int w2, const 
 
 /* Eq.4-7 over the three-state chain: issued instructions (ready warps) over elapsed cycles. */
 void or3_ipc(int w1, int w2, int joint, const double* pi, const double* R, double* ipc1, double* ipc2) {
+    or3_ipc_g(w1, 1, w2, 1, joint, pi, R, ipc1, ipc2);
+}
+
+/* Eq.4-7 with units of g warps: a ready unit issues g instructions per round. */
+void or3_ipc_g(int w1, int g1, int w2, int g2, int joint, const double* pi, const double* R, double* ipc1,
+               double* ipc2) {
     const int n2 = joint ? or3_nstates(w2) : 1;
     double den = 0.0, a = 0.0, b = 0.0;
     for (int c1 = 0; c1 <= w1; ++c1)
@@ -132,26 +145,31 @@ void or3_ipc(int w1, int w2, int joint, const double* pi, const double* R, doubl
                     a += pi[s] * (double)(w1 - c1 - u1);
                     if (joint) b += pi[s] * (double)(w2 - c2 - u2);
                 }
-    *ipc1 = a / den;
-    *ipc2 = joint ? b / den : 0.0;
+    *ipc1 = g1 * a / den;
+    *ipc2 = joint ? g2 * b / den : 0.0;
 }
 
+/* Units of a kernel on the virtual SM: b blocks of wpb warps over nsched schedulers, in units of
+ * g warps (R14, R13); -1 if not whole. */
 static int vsm3(const or_kmodel3* k, int b, int nsched) {
-    const int t = b * k->wpb;
-    return (t % nsched) ? -1 : t / nsched;
+    const int t = b * k->wpb, g = k->g > 0 ? k->g : 1;
+    if (t % nsched) return -1;
+    const int w = t / nsched;
+    return (w % g) ? -1 : w / g;
 }
+static int gof(const or_kmodel3* k) { return k->g > 0 ? k->g : 1; }
 
 double or3_solo_ipc(const or_kmodel3* k, int b, int nsched, const or_smcfg* cfg, int* status) {
     const int w = vsm3(k, b, nsched);
     *status = 0;
-    if (w < 1 || w > cfg->W) { *status = 2; return 0.0; }
+    if (w < 1 || w * gof(k) > cfg->W) { *status = 2; return 0.0; }
     const int S = or3_nstates(w);
     double* P = (double*)malloc(sizeof(double) * (size_t)S * S);
     double* R = (double*)malloc(sizeof(double) * S);
     double* pi = (double*)malloc(sizeof(double) * S);
     double ipc = 0.0, dummy;
     if (or3_build(k, w, 0, 0, cfg, P, R) || or_stationary(S, P, pi)) *status = 6;
-    else or3_ipc(w, 0, 0, pi, R, &ipc, &dummy);
+    else or3_ipc_g(w, gof(k), 0, 1, 0, pi, R, &ipc, &dummy);
     free(P); free(R); free(pi);
     return ipc;
 }
@@ -160,7 +178,7 @@ void or3_predict(const or_kmodel3* k1, int b1, int b1max, const or_kmodel3* k2, 
                  const or_smcfg* cfg, or_pred* out) {
     memset(out, 0, sizeof(*out));
     const int w1 = vsm3(k1, b1, nsched), w2 = vsm3(k2, b2, nsched);
-    if (w1 < 1 || w2 < 1 || w1 + w2 > cfg->W) { out->status = 2; return; }
+    if (w1 < 1 || w2 < 1 || w1 * gof(k1) + w2 * gof(k2) > cfg->W) { out->status = 2; return; }
     int st1, st2;
     out->solo1 = or3_solo_ipc(k1, b1max, nsched, cfg, &st1);
     out->solo2 = or3_solo_ipc(k2, b2max, nsched, cfg, &st2);
@@ -172,7 +190,7 @@ void or3_predict(const or_kmodel3* k1, int b1, int b1max, const or_kmodel3* k2, 
     if (or3_build(k1, w1, k2, w2, cfg, P, R) || or_stationary(S, P, pi)) {
         out->status = 6;
     } else {
-        or3_ipc(w1, w2, 1, pi, R, &out->ipc1, &out->ipc2);
+        or3_ipc_g(w1, gof(k1), w2, gof(k2), 1, pi, R, &out->ipc1, &out->ipc2);
         out->c = out->ipc1 + out->ipc2;
         double cipc[2] = {out->ipc1, out->ipc2}, ipc[2] = {out->solo1, out->solo2};
         out->cp = or_cp(2, cipc, ipc);

@@ -103,12 +103,15 @@ typedef struct {
     int wpb;            /* warps per block */
     double pi;          /* pipe ceiling (R26) */
     int pipe;
+    int g;              /* warps per modelling unit (R13 block granularity); 0/1 = warps */
 } or_kmodel3;
 int or3_nstates(int w);
 void or3_row(const or_kmodel3* k, int w, int c, int u, double pc, double pu, double* row);
 int or3_build(const or_kmodel3* k1, int w1, const or_kmodel3* k2, int w2, const or_smcfg* cfg, double* P,
               double* R);
 void or3_ipc(int w1, int w2, int joint, const double* pi, const double* R, double* ipc1, double* ipc2);
+void or3_ipc_g(int w1, int g1, int w2, int g2, int joint, const double* pi, const double* R, double* ipc1,
+               double* ipc2);
 double or3_solo_ipc(const or_kmodel3* k, int b, int nsched, const or_smcfg* cfg, int* status);
 void or3_predict(const or_kmodel3* k1, int b1, int b1max, const or_kmodel3* k2, int b2, int b2max, int nsched,
                  const or_smcfg* cfg, or_pred* out);

@@ -184,3 +184,63 @@ def test_predict3_reduces_to_predict():
     assert a2.status == 0 and a3.status == 0
     for f in ("ipc1", "ipc2", "solo1", "solo2", "cp", "dT"):
         assert abs(getattr(a2, f) - getattr(a3, f)) <= 1e-9 * max(1.0, abs(getattr(a2, f))), f
+
+
+@pytest.mark.parametrize("g,rm,uc", [(2, 0.3, 0.5), (4, 0.1, 1.0), (3, 0.5, 0.0)])
+def test_units_w1_closed_form(g, rm, uc):
+    """Block granularity (R13): one unit of g warps.  Ready: the round lasts g cycles and issues
+    g instructions; idle: the round lasts 1 cycle with g*r (g*ru) requests outstanding, so
+    IPC = g / (g + Rm(1-uc) L_c + Rm uc L_u)."""
+    L0, a0, B, r, ru = 30.0, 1.0, 0.5, 2.0, 9.0
+    cfg = _cfg(L0=L0, a0=a0, B=B, W=g)
+    Lc = L0 + a0 * g * r / B
+    Lu = L0 + a0 * g * ru / B + a0 * (ru - r) / B
+    expect = g / (g + rm * (1 - uc) * Lc + rm * uc * Lu)
+    P, R = O.build3(O.kmodel3(rm, r=r, uc=uc, ru=ru, g=g), 1, cfg)
+    assert abs(O.ipc3(1, O.stationary(P), R, g1=g) - expect) < 1e-13
+
+
+def test_units_g1_is_warp_model():
+    cfg = _cfg()
+    k1 = O.kmodel3(0.2, r=2.0, uc=0.4, ru=12.0, wpb=8, ipb=700)
+    k2 = O.kmodel3(0.05, r=1.0, uc=0.0, ru=1.0, wpb=4, ipb=3000)
+    a = O.predict3(k1, 2, 8, k2, 4, 16, 4, cfg)
+    k1.g = 1
+    b = O.predict3(k1, 2, 8, k2, 4, 16, 4, cfg)
+    assert a.status == 0 and abs(a.cp - b.cp) < 1e-15
+
+
+def test_units_monte_carlo():
+    """Units of g = 2 warps simulated as g-instruction super-warps (independent of the chain)."""
+    g, W = 2, 3
+    k = dict(rm=0.3, r=2.0, uc=0.5, ru=10.0)
+    L0, a0, B = 40.0, 1.0, 2.0
+    cfg = _cfg(L0=L0, a0=a0, B=B, W=g * W)
+    P, R = O.build3(O.kmodel3(k["rm"], r=k["r"], uc=k["uc"], ru=k["ru"], g=g), W, cfg)
+    model = O.ipc3(W, O.stationary(P), R, g1=g)
+    rng = np.random.default_rng(9)
+    st = np.zeros(W, np.int8)
+    nb, per = 50, 1200
+    ib, cb = np.zeros(nb), np.zeros(nb)
+    for bi in range(nb):
+        inst = cyc = 0.0
+        for _ in range(per):
+            ready = int((st == 0).sum())
+            Rr = max(g * ready, 1)
+            n = g * (float((st == 1).sum()) * k["r"] + float((st == 2).sum()) * k["ru"])
+            Lc = L0 + a0 * n / B
+            Lu = Lc + a0 * (k["ru"] - k["r"]) / B
+            x = rng.random(W)
+            new = st.copy()
+            rd = st == 0
+            inst += g * float(rd.sum())
+            new[rd & (x < k["rm"] * (1 - k["uc"]))] = 1
+            new[rd & (x >= k["rm"] * (1 - k["uc"])) & (x < k["rm"])] = 2
+            new[(st == 1) & (x < min(1.0, Rr / Lc))] = 0
+            new[(st == 2) & (x < min(1.0, Rr / Lu))] = 0
+            st = new
+            cyc += Rr
+        ib[bi], cb[bi] = inst, cyc
+    mc = ib.sum() / cb.sum()
+    sig = np.std(ib / cb, ddof=1) / math.sqrt(nb)
+    assert abs(mc - model) <= 3.5 * sig + 1e-4, (mc, model, sig)
