@@ -198,7 +198,7 @@ def build_queue(rank: int, world: int, instances: int, workload: str = "c2") -> 
     return shard(global_queue(workload, instances, world), rank, world)
 
 
-MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe")
+MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
 
 
 def load_profiles(path: str):

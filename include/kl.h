@@ -126,6 +126,9 @@ typedef struct {
     double ipc_max;        /* pipe ceiling per virtual SM (R26; 0 = 1, the paper's model) */
     int32_t pipe;          /* id of the pipe that ceiling belongs to (0 none, 1 MUFU, 2 ALU, 3 FMA) */
     int32_t pad;
+    double uc;             /* f1: fraction of memory instructions that are
+                              uncoalesced (0 = all coalesced: the two-state model) */
+    double ru;             /* requests per uncoalesced memory instruction (r: per coalesced one) */
 } kl_profile;
 
 typedef struct {
@@ -143,6 +146,11 @@ typedef struct {
     int32_t audit;             /* 1: count executions per virtual block (coverage audit) */
     int32_t retune;            /* 1 (default): a re-plan that keeps a running kernel at another
                                   occupancy re-tunes it in place; 0: stop and relaunch */
+    int32_t model_states;      /* 2 (default): two-state warp model; 3: kinds with
+                                  uc > 0 use the three-state coalesced/uncoalesced chain (f1,
+                                  P:1000-1019, reading R27) */
+    int32_t granularity;       /* 0 (default): warps; 1: thread blocks as the modelling unit
+                                  (reading R13: units of wpb/n_sched warps) */
     int32_t pad0;
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */

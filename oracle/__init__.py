@@ -445,6 +445,27 @@ def kmodel_of(prof: dict) -> KModel:
                   int(prof.get("pipe", 0)))
 
 
+def kmodel3_of(prof: dict, states: int = 3, granularity: int = 0, nsched: int = 4) -> KModel3:
+    """f1 descriptor: three-state only when configured and the kind has uncoalesced accesses
+    (uc > 0); block granularity (R13) models units of wpb/nsched warps when wpb divides evenly."""
+    uc = float(prof.get("uc", 0.0) or 0.0) if states == 3 else 0.0
+    r = prof["r"]
+    ru = float(prof.get("ru", 0.0) or 0.0) or r
+    wpb = prof["wpb"]
+    g = wpb // nsched if (granularity == 1 and wpb % nsched == 0 and wpb >= nsched) else 1
+    return KModel3(prof["rm"], r, uc, ru, prof["ipb"], wpb, prof.get("ipc_max", 1.0) or 1.0,
+                   int(prof.get("pipe", 0)), g)
+
+
+def predict_cfg(p1, b1, p2, b2, cfg, nsched=4, states=2, granularity=0) -> Pred:
+    """The model prediction the runtime's configuration selects: two-state warp model
+    (oracle/model.c) by default, else the f1 chain (oracle/model3.c)."""
+    if states == 2 and granularity == 0:
+        return predict(kmodel_of(p1), b1, solo_b(p1, nsched), kmodel_of(p2), b2, solo_b(p2, nsched), nsched, cfg)
+    return predict3(kmodel3_of(p1, states, granularity, nsched), b1, solo_b(p1, nsched),
+                    kmodel3_of(p2, states, granularity, nsched), b2, solo_b(p2, nsched), nsched, cfg)
+
+
 def pairs_of(pending: list[dict]) -> list[tuple[int, int]]:
     """Candidate pairs over pending instances in arrival order, one pair per
     unordered kind pair (earliest instances), same-kind pairs included when two instances of a
@@ -507,7 +528,8 @@ def _better_split(a, b, rule=0):
 
 
 def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, nsched=4,
-                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0, split_rule=0) -> dict:
+                     ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0, split_rule=0,
+                     states=2, granularity=0) -> dict:
     """Proc. FindCoSchedule: candidates -> prune -> model CP -> argmax.
 
     Per surviving pair the slice ratio is the argmin of dT (Eq.8) over maximal splits; across
@@ -526,8 +548,7 @@ def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, n
             if cache is not None and key in cache:
                 pr = cache[key]
             else:
-                r = predict(kmodel_of(p1), b1, solo_b(p1, nsched), kmodel_of(p2), b2,
-                            solo_b(p2, nsched), nsched, cfg)
+                r = predict_cfg(p1, b1, p2, b2, cfg, nsched, states, granularity)
                 pr = dict(ipc1=r.ipc1, ipc2=r.ipc2, c=r.c, solo1=r.solo1, solo2=r.solo2,
                           cp=r.cp, dT=r.dT, status=r.status)
                 if cache is not None:

@@ -14,7 +14,7 @@ import subprocess
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libkl.so")
-SOURCES = ["csrc/kl_runtime.cpp", "csrc/kl_kernels.cu", "csrc/kl_model.cu", "csrc/kl_mm.cu"]
+SOURCES = ["csrc/kl_runtime.cpp", "csrc/kl_kernels.cu", "csrc/kl_model.cu", "csrc/kl_model3.cu", "csrc/kl_mm.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-shared", "-cudart", "static"]
 
@@ -22,7 +22,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libkl.so in-tree with nvcc for sm_100a (cross-compiles without a GPU)."""
     srcs = [os.path.join(_HERE, s) for s in SOURCES]
-    deps = srcs + [os.path.join(_HERE, "csrc", h) for h in ("kl_internal.h", "kl_launcher.cuh")] + [os.path.join(_ROOT, "include", "kl.h")]
+    deps = srcs + [os.path.join(_HERE, "csrc", h) for h in ("kl_internal.h", "kl_launcher.cuh", "kl_model_common.cuh")] + [os.path.join(_ROOT, "include", "kl.h")]
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= max(map(os.path.getmtime, deps)):
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "nvcc")
@@ -96,7 +96,7 @@ class Profile(C.Structure):
     _fields_ = [("rm", C.c_double), ("r", C.c_double), ("ipb", C.c_double), ("pur", C.c_double),
                 ("mur", C.c_double), ("wpb", C.c_int32), ("regs", C.c_int32), ("smem", C.c_int32),
                 ("tmem", C.c_int32), ("bmax", C.c_int32), ("m_min", C.c_int32), ("ipc_max", C.c_double),
-                ("pipe", C.c_int32), ("pad", C.c_int32)]
+                ("pipe", C.c_int32), ("pad", C.c_int32), ("uc", C.c_double), ("ru", C.c_double)]
 
 
 class Config(C.Structure):
@@ -105,7 +105,8 @@ class Config(C.Structure):
                 ("cp_min", C.c_double), ("n_sched", C.c_int32), ("latency_mode", C.c_int32), ("level_mode", C.c_int32),
                 ("split_rule", C.c_int32), ("model_frozen", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
-                ("retune", C.c_int32), ("pad0", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
+                ("retune", C.c_int32), ("model_states", C.c_int32), ("granularity", C.c_int32),
+                ("pad0", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
                 ("profiles", C.POINTER(Profile)), ("stream_a", _vp), ("stream_b", _vp),
                 ("counters_dev", _vp)]

@@ -129,7 +129,11 @@ int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n_
 // ---- model kernels (kl_model.cu) ---------------------------------------------------------
 struct KlModelKind {       // per-kind model inputs, device table
     double rm, r, ipb, pi;    // pi: pipe ceiling (R26), 1 = none
-    int32_t wpb, bsolo, pipe, pad1;
+    double uc, ru;            // f1: uncoalesced fraction of memory instructions, its requests
+    int32_t wpb, bsolo, pipe;
+    int32_t g;                // warps per modelling unit (R13 block granularity; 1 = warps)
+    int32_t three;            // 1: three-state chain for this kind (f1)
+    int32_t pad1;
 };
 struct KlModelCfg {
     double L0, B, a0, b0;
@@ -160,6 +164,14 @@ KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
 KL_HD unsigned long long kl_tune_req(uint32_t epoch, uint32_t cap) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)cap << 32);
 }
+
+// General model (f1 three-state kinds and/or block-granularity units): one CTA per candidate,
+// the chains in global scratch (`scratch` + `scratch_off[c]` doubles for candidate c, room for
+// (S^2 + 3 S) doubles with S its largest chain); same predictions / fused selection contract.
+int kl_dev_model_general(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands,
+                         kl_prediction* preds, int n_pairs, const int32_t* pair_off,
+                         uint32_t* done_counter, KlDecision* dec, double* scratch,
+                         const int64_t* scratch_off, void* stream);
 
 // Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy
 // selection (a9) and writes *dec.  `done_counter` must be zero on entry (reset by the kernel).

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "kl_internal.h"
+#include "kl_model_common.cuh"
 
 namespace {
 
@@ -22,35 +23,6 @@ constexpr int kThreads = 256;
 // Binomial coefficients C(n,k), n <= 16 (exact in double).
 __constant__ double c_binom[17][17];
 
-
-__device__ double latency(const KlModelCfg& c, double n, int idle) {
-    if (c.latency_mode == 1) return c.L0 + c.B / (c.a0 * (double)(idle > 1 ? idle : 1)) + c.b0;
-    return c.L0 + c.a0 * n / c.B + c.b0;
-}
-
-// Round duration (R1) with the B200 pipe ceilings (R26): issue of all
-// ready warps, each kernel's pipe time (ready / pi), pipes shared between kernels on the same
-// pipe id; at least one cycle.
-__device__ double round_dur(int r1, const KlModelKind* k1, int r2, const KlModelKind* k2) {
-    double R = (double)(r1 + r2);
-    const double p1 = k1 ? k1->pi : 1.0, p2 = k2 ? k2->pi : 1.0;
-    if (k1 && k2 && k1->pipe != 0 && k1->pipe == k2->pipe) {
-        R = fmax(R, r1 / p1 + r2 / p2);
-    } else {
-        R = fmax(R, r1 / p1);
-        R = fmax(R, r2 / p2);
-    }
-    return fmax(R, 1.0);
-}
-
-// P_ir in a state of round duration R (R1); returns false if the guard L > W fails (R22).
-__device__ bool p_ir(const KlModelCfg& c, double R, int idle, double n, double* out) {
-    double L = latency(c, n, idle);
-    if (!(L > (double)c.W)) return false;
-    double p = R / L;
-    *out = p < 1.0 ? p : 1.0;
-    return true;
-}
 
 // One-kernel transition row from i idle of w (Eq.2 summed with binomial weights, R3), one warp:
 // lane a holds Binomial(i, pir) mass at a returns, lane b Binomial(w - i, rm) mass at b stalls;
@@ -231,29 +203,6 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     return KL_OK;
 }
 
-__device__ __forceinline__ double band(double x, double y) {
-    double m = fmax(1.0, fmax(fabs(x), fabs(y)));
-    return 1e-12 * m;
-}
-
-// a9 split order: argmin dT; ties (1e-12 band): larger C, more warps, smaller b1.
-__device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb,
-                             int rule) {
-    if (rule == 1) {   // ablation: highest predicted CP first
-        double t = band(a.cp, b.cp);
-        if (a.cp > b.cp + t) return true;
-        if (a.cp < b.cp - t) return false;
-    }
-    double t = band(a.dT, b.dT);
-    if (a.dT < b.dT - t) return true;
-    if (a.dT > b.dT + t) return false;
-    t = band(a.c, b.c);
-    if (a.c > b.c + t) return true;
-    if (a.c < b.c - t) return false;
-    if (ca.warps != cb.warps) return ca.warps > cb.warps;
-    return ca.b1 < cb.b1;
-}
-
 __global__ void __launch_bounds__(kThreads)
 k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const KlCand* __restrict__ cands,
               kl_prediction* preds, int n_pairs, const int32_t* __restrict__ pair_off,
@@ -264,8 +213,6 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     double* Rs = pi + kMaxS;               // kMaxS
     double* red = Rs + kMaxS;              // 16
     __shared__ double s_binom[kMaxW + 1][kMaxW + 1];
-    __shared__ int s_last;
-    __shared__ int s_best_pair[128];
     for (int x = threadIdx.x; x < (kMaxW + 1) * (kMaxW + 1); x += kThreads)
         s_binom[x / (kMaxW + 1)][x % (kMaxW + 1)] = c_binom[x / (kMaxW + 1)][x % (kMaxW + 1)];
     __syncthreads();
@@ -310,43 +257,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     if (threadIdx.x == 0) preds[blockIdx.x] = out;
     if (n_pairs <= 0) return;
 
-    // ---- fused selection by the last CTA ---------------------------------------------------
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(done_counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int pr = threadIdx.x; pr < n_pairs; pr += kThreads) {
-        int best = -1;
-        kl_prediction bp;
-        KlCand bc;
-        for (int i = pair_off[pr]; i < pair_off[pr + 1]; ++i) {
-            kl_prediction a = preds[i];
-            if (a.status != 0) continue;
-            KlCand ca = cands[i];
-            if (best < 0 || better_split(a, ca, bp, bc, cfg.split_rule)) { best = i; bp = a; bc = ca; }
-        }
-        if (pr < 128) s_best_pair[pr] = best;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int best = -1;
-        double bcp = 0.0;
-        for (int pr = 0; pr < n_pairs && pr < 128; ++pr) {
-            int i = s_best_pair[pr];
-            if (i < 0) continue;
-            double cp = preds[i].cp;
-            if (best < 0 || cp > bcp + band(cp, bcp)) { best = i; bcp = cp; }
-        }
-        // (R25 "no profitable pair -> solo" is applied by the host with the configured cp_min)
-        dec->cand = best;
-        dec->cp = best >= 0 ? bcp : 0.0;
-        dec->n_pairs = n_pairs;
-        *done_counter = 0u;
-        __threadfence_system();
-        dec->done = 1;
-    }
+    select_last<kThreads>(cfg, cands, preds, n_pairs, pair_off, done_counter, dec);
 }
 
 }  // namespace

@@ -156,6 +156,10 @@ struct kl_ctx {
     std::vector<Inst*> arriving;       // submitted, waiting for their ready event (Alg.1 l.2)
     uint64_t next_id = 1, seq = 0;
     // model batch buffers
+    double* scratch_dev = nullptr;      // general model: per-candidate chains
+    int64_t scratch_cap = 0;
+    int64_t* soff_pinned = nullptr;
+    int64_t* soff_dev = nullptr;
     KlModelKind* mk_pinned = nullptr;
     KlModelKind* mk_dev = nullptr;
     KlCand* cand_pinned = nullptr;
@@ -309,6 +313,12 @@ void fill_model_kinds(kl_ctx* c) {
         m.bsolo = (int)solo_level(c, p);
         m.pi = (p.ipc_max > 0.0 && p.ipc_max < 1.0) ? p.ipc_max : 1.0;
         m.pipe = p.pipe;
+        m.uc = p.uc;
+        m.ru = p.ru > 0.0 ? p.ru : p.r;
+        m.three = (c->cfg.model_states == 3 && p.uc > 0.0) ? 1 : 0;
+        m.g = 1;
+        if (c->cfg.granularity == 1 && p.wpb % c->cfg.n_sched == 0 && p.wpb >= c->cfg.n_sched)
+            m.g = p.wpb / c->cfg.n_sched;   // a block's warps per virtual SM (R13)
         c->mk_pinned[k] = m;
     }
 }
@@ -335,6 +345,34 @@ const std::vector<std::pair<uint32_t, uint32_t>>& splits_of(kl_ctx* c, int k1, i
     return c->splits[k1][k2];
 }
 
+// The general model kernel (kl_model3.cu) serves three-state kinds and block granularity.
+bool general_model(const kl_ctx* c) {
+    if (c->cfg.granularity == 1) return true;
+    if (c->cfg.model_states != 3) return false;
+    for (int k = 0; k < KL_NKINDS; ++k)
+        if (c->mk_pinned[k].three) return true;
+    return false;
+}
+
+// States of one kind's chain at w warps (mirror of the device's make_kin / nstates).
+int64_t kind_states(const KlModelKind& m, int w) {
+    const int g = m.g > 0 ? m.g : 1;
+    const int u = std::max(1, w / g);
+    return m.three ? (int64_t)(u + 1) * (u + 2) / 2 : (int64_t)u + 1;
+}
+
+// Global scratch of one candidate in the general model: its largest chain's S^2 + 3 S doubles.
+int64_t scratch_doubles(const kl_ctx* c, const KlCand& cd) {
+    const KlModelKind& a = c->mk_pinned[cd.k1];
+    const KlModelKind& b = c->mk_pinned[cd.k2];
+    const int ns = c->cfg.n_sched;
+    const int w1 = (int)cd.b1 * a.wpb / ns, w2 = (int)cd.b2 * b.wpb / ns;
+    const int ws1 = a.bsolo * a.wpb / ns, ws2 = b.bsolo * b.wpb / ns;
+    int64_t S = std::max(kind_states(a, ws1), kind_states(b, ws2));
+    S = std::max(S, kind_states(a, w1) * (cd.b2 ? kind_states(b, w2) : 1));
+    return S * S + 3 * S;
+}
+
 // Run the device model over cand_pinned[0..n); n_pairs > 0 fuses the selection.
 kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
@@ -344,8 +382,28 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
     KL_CUDA(cudaMemcpyAsync(ctx->cand_dev, ctx->cand_pinned, sizeof(KlCand) * n, cudaMemcpyHostToDevice, ctx->ctrl));
     if (n_pairs > 0)
         KL_CUDA(cudaMemcpyAsync(ctx->off_dev, ctx->off_pinned, sizeof(int32_t) * (n_pairs + 1), cudaMemcpyHostToDevice, ctx->ctrl));
-    int rc = kl_dev_model_batch(ctx->mk_dev, model_cfg(ctx, n), ctx->cand_dev, ctx->pred_dev, n_pairs, ctx->off_dev,
+    int rc;
+    if (general_model(ctx)) {
+        // f1 / block granularity: chains in global scratch, sized per candidate
+        int64_t tot = 0;
+        for (int i = 0; i < n; ++i) {
+            ctx->soff_pinned[i] = tot;
+            tot += scratch_doubles(ctx, ctx->cand_pinned[i]);
+        }
+        if (tot > ctx->scratch_cap) {
+            if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
+            ctx->scratch_dev = nullptr;
+            ctx->scratch_cap = 0;
+            KL_CUDA(cudaMalloc(&ctx->scratch_dev, sizeof(double) * (size_t)tot));
+            ctx->scratch_cap = tot;
+        }
+        KL_CUDA(cudaMemcpyAsync(ctx->soff_dev, ctx->soff_pinned, sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->ctrl));
+        rc = kl_dev_model_general(ctx->mk_dev, model_cfg(ctx, n), ctx->cand_dev, ctx->pred_dev, n_pairs, ctx->off_dev,
+                                  ctx->done_dev, ctx->dec_dev, ctx->scratch_dev, ctx->soff_dev, ctx->ctrl);
+    } else {
+        rc = kl_dev_model_batch(ctx->mk_dev, model_cfg(ctx, n), ctx->cand_dev, ctx->pred_dev, n_pairs, ctx->off_dev,
                                 ctx->done_dev, ctx->dec_dev, ctx->ctrl);
+    }
     if (rc) return ctx->fail(KL_ECUDA, "model batch launch: %s", cudaGetErrorString((cudaError_t)rc));
     KL_CUDA(cudaMemcpyAsync(ctx->pred_pinned, ctx->pred_dev, sizeof(kl_prediction) * n, cudaMemcpyDeviceToHost, ctx->ctrl));
     if (n_pairs > 0)
@@ -942,6 +1000,8 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             ctx->init_pinned = ctx->init_base;
             for (auto& e : ctx->init_done) KL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocDefault));
+            KL_CUDA(cudaHostAlloc(&ctx->soff_pinned, sizeof(int64_t) * kMaxCand, cudaHostAllocDefault));
+            KL_CUDA(cudaMalloc(&ctx->soff_dev, sizeof(int64_t) * kMaxCand));
             KL_CUDA(cudaMalloc(&ctx->mk_dev, sizeof(KlModelKind) * KL_NKINDS));
             KL_CUDA(cudaHostAlloc(&ctx->cand_pinned, sizeof(KlCand) * kMaxCand, cudaHostAllocDefault));
             KL_CUDA(cudaMalloc(&ctx->cand_dev, sizeof(KlCand) * kMaxCand));
@@ -987,6 +1047,9 @@ kl_status kl_destroy(kl_ctx* ctx) {
         for (auto& e : ctx->init_done) if (e) cudaEventDestroy(e);
         cudaFreeHost(ctx->mk_pinned);
         cudaFree(ctx->mk_dev);
+        if (ctx->soff_pinned) cudaFreeHost(ctx->soff_pinned);
+        if (ctx->soff_dev) cudaFree(ctx->soff_dev);
+        if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
         cudaFreeHost(ctx->cand_pinned);
         cudaFree(ctx->cand_dev);
         cudaFreeHost(ctx->off_pinned);
@@ -1267,6 +1330,7 @@ kl_status kl_set_profile(kl_ctx* ctx, kl_kind kind, const kl_profile* p) {
     KL_LIVE(ctx);
     if (kind < 0 || kind >= KL_NKINDS || !p) return KL_EINVAL;
     if (!(p->rm >= 0.0 && p->rm <= 1.0)) return ctx->fail(KL_EINVAL, "Rm outside [0,1]");
+    if (!(p->uc >= 0.0 && p->uc <= 1.0)) return ctx->fail(KL_EINVAL, "uncoalesced fraction outside [0,1]");
     kl_profile q = *p;
     const kl_profile& cur = ctx->prof[kind];
     if (!q.wpb) q.wpb = cur.wpb;
