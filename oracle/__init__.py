@@ -512,7 +512,9 @@ def _better_split(a, b, rule=0):
             return True
         if a["cp"] < b["cp"] - t:
             return False
-    t = _band(a["dT"], b["dT"])
+    # dT ties relative to the Eq.8 terms (R8): dT is a difference of per-wave times, so its
+    # rounding noise scales with them
+    t = 1e-9 * max(a["dT_scale"], b["dT_scale"])
     if a["dT"] < b["dT"] - t:
         return True
     if a["dT"] > b["dT"] + t:
@@ -554,6 +556,8 @@ def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, n
                 if cache is not None:
                     cache[key] = pr
             cand = dict(pr, b1=b1, b2=b2, warps=b1 * p1["wpb"] + b2 * p2["wpb"], ia=ia, ib=ib)
+            cand["dT_scale"] = (max(p1["ipb"] * b1 / pr["ipc1"], p2["ipb"] * b2 / pr["ipc2"])
+                                if pr["status"] == 0 else 0.0)
             evaluated.append(cand)
             if pr["status"] != 0:
                 continue

@@ -257,7 +257,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     if (threadIdx.x == 0) preds[blockIdx.x] = out;
     if (n_pairs <= 0) return;
 
-    select_last<kThreads>(cfg, cands, preds, n_pairs, pair_off, done_counter, dec);
+    select_last<kThreads>(cfg, kinds, cands, preds, n_pairs, pair_off, done_counter, dec);
 }
 
 }  // namespace

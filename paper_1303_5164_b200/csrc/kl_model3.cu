@@ -302,7 +302,7 @@ k_model_general(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, con
     out.status = status;
     if (threadIdx.x == 0) preds[blockIdx.x] = out;
     if (n_pairs <= 0) return;
-    select_last<kThreads>(cfg, cands, preds, n_pairs, pair_off, done_counter, dec);
+    select_last<kThreads>(cfg, kinds, cands, preds, n_pairs, pair_off, done_counter, dec);
 }
 
 }  // namespace

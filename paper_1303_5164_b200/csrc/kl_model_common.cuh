@@ -43,14 +43,23 @@ __device__ __forceinline__ double band(double x, double y) {
 }
 
 // a9 split order: argmin dT; ties (1e-12 band): larger C, more warps, smaller b1.
+// Eq.8 time scale of a split: the larger of its two per-wave times I_k b_k / cIPC_k; dT ties are
+// judged relative to it (R8: dT is a difference of such terms, so its rounding noise scales
+// with them, not with dT).
+__device__ __forceinline__ double dT_scale(const kl_prediction& p, const KlCand& c, const KlModelKind* kinds) {
+    return fmax(kinds[c.k1].ipb * (double)c.b1 / p.ipc1, kinds[c.k2].ipb * (double)c.b2 / p.ipc2);
+}
+
+// a9 split order: argmin dT (ties within 1e-9 of the Eq.8 terms); then larger C (1e-12 band),
+// more warps, smaller b1.  rule 1: highest predicted CP first (R7').
 __device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb,
-                             int rule) {
+                             int rule, const KlModelKind* kinds) {
     if (rule == 1) {   // ablation: highest predicted CP first
         double t = band(a.cp, b.cp);
         if (a.cp > b.cp + t) return true;
         if (a.cp < b.cp - t) return false;
     }
-    double t = band(a.dT, b.dT);
+    double t = 1e-9 * fmax(dT_scale(a, ca, kinds), dT_scale(b, cb, kinds));
     if (a.dT < b.dT - t) return true;
     if (a.dT > b.dT + t) return false;
     t = band(a.c, b.c);
@@ -63,7 +72,8 @@ __device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_
 // Fused selection (a9) by the CTA that finishes last: per pair the best split (better_split),
 // then argmax CP over pairs.  Called by every CTA after writing its prediction.
 template <int kThreads>
-__device__ void select_last(const KlModelCfg& cfg, const KlCand* __restrict__ cands, kl_prediction* preds,
+__device__ void select_last(const KlModelCfg& cfg, const KlModelKind* kinds, const KlCand* __restrict__ cands,
+                            kl_prediction* preds,
                             int n_pairs, const int32_t* __restrict__ pair_off, uint32_t* done_counter,
                             KlDecision* dec) {
     __shared__ int s_last;
@@ -82,7 +92,7 @@ __device__ void select_last(const KlModelCfg& cfg, const KlCand* __restrict__ ca
             kl_prediction a = preds[i];
             if (a.status != 0) continue;
             KlCand ca = cands[i];
-            if (best < 0 || better_split(a, ca, bp, bc, cfg.split_rule)) { best = i; bp = a; bc = ca; }
+            if (best < 0 || better_split(a, ca, bp, bc, cfg.split_rule, kinds)) { best = i; bp = a; bc = ca; }
         }
         if (pr < 128) s_best_pair[pr] = best;
     }

@@ -286,13 +286,20 @@ bool pruned(const kl_profile& a, const kl_profile& b, double ap, double am) {
     return std::fabs(a.pur - b.pur) < ap && std::fabs(a.mur - b.mur) < am;   // R9: AND, strict
 }
 
-bool better_split(const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb, int rule) {
+// Eq.8 time scale of a split (the larger per-wave time I_k b_k / cIPC_k); dT ties are judged
+// relative to it (R8).
+double dT_scale(const kl_ctx* c, const kl_prediction& p, const KlCand& cd) {
+    return std::max(c->prof[cd.k1].ipb * (double)cd.b1 / p.ipc1, c->prof[cd.k2].ipb * (double)cd.b2 / p.ipc2);
+}
+
+bool better_split(const kl_ctx* c, const kl_prediction& a, const KlCand& ca, const kl_prediction& b, const KlCand& cb,
+                  int rule) {
     if (rule == 1) {   // ablation: the split with the highest predicted CP (SURVEY key finding 4)
         double t = band(a.cp, b.cp);
         if (a.cp > b.cp + t) return true;
         if (a.cp < b.cp - t) return false;
     }
-    double t = band(a.dT, b.dT);
+    double t = 1e-9 * std::max(dT_scale(c, a, ca), dT_scale(c, b, cb));
     if (a.dT < b.dT - t) return true;
     if (a.dT > b.dT + t) return false;
     t = band(a.c, b.c);
@@ -526,7 +533,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
                 kl_prediction a{};
                 if (!ctx->lookup(cd.k1, cd.k2, cd.b1, cd.b2, &a)) a.status = KL_EINFEASIBLE;   // frozen, not installed
                 if (a.status != 0) continue;
-                if (bi < 0 || better_split(a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
+                if (bi < 0 || better_split(ctx, a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
             }
             if (bi < 0) continue;
             if (best < 0 || bp.cp > bcp + band(bp.cp, bcp)) { best = bi; bcp = bp.cp; }
