@@ -488,6 +488,34 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     d->n_cand = n;
     int best = -1;
     double bcp = 0.0;
+    if (ctx->cfg.mc_seed) {
+        // MC(s) comparator: a uniformly random pair of the pending kinds and a
+        // uniformly random maximal slice ratio, no model, no pruning (counter-based splitmix64
+        // stream: seed x decision number)
+        std::vector<int> all;
+        for (auto& pq : pairs) {
+            const auto& ms = splits_of(ctx, R[pq.first]->kind, R[pq.second]->kind);
+            for (size_t s = 0; s < ms.size(); ++s) all.push_back((int)((&pq - &pairs[0]) * 4096 + (int)s));
+        }
+        if (!all.empty()) {
+            uint64_t z = (uint64_t)(uint32_t)ctx->cfg.mc_seed * 0x9E3779B97F4A7C15ull + (uint64_t)ctx->st.decisions + 1;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            const int pick = all[z % all.size()];
+            const auto& pq = pairs[pick / 4096];
+            const auto& sp = splits_of(ctx, R[pq.first]->kind, R[pq.second]->kind)[pick % 4096];
+            d->solo = false;
+            d->ia = pq.first;
+            d->ib = pq.second;
+            d->k1 = R[d->ia];
+            d->k2 = R[d->ib];
+            d->b1 = sp.first;
+            d->b2 = sp.second;
+            d->cp = 0.0;
+            return KL_OK;
+        }
+    }
     if (n > 0 && missing && !ctx->cfg.model_frozen) {
         if (ctx->host_only) return ctx->fail(KL_ECUDA, "host-only context cannot run the model");
         // one batch also covers every other pair of the pending kinds (unpruned, pair = -1), so

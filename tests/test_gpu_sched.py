@@ -108,3 +108,21 @@ def test_stop_protocol_stress(retune):
     if not retune:
         assert st.retunes == 0 and st.topups == 0
     ctx.close()
+
+
+def test_mc_random_coschedules_complete():
+    """MC(s) comparator mode: random pairs and slice ratios at every decision still
+    execute every block exactly once with the oracle's results."""
+    K.build()
+    kinds = ["PC", "SPMV", "ST", "BS", "TEA", "MRIQ", "SAD", "SYNTH"]
+    ds = {k: G.gen(k, "small") for k in kinds}
+    refs = {k: O.run_kernel(ds[k]) for k in kinds}
+    for seed in (1, 2):
+        ctx = K.Context(device=0, audit=1, mc_seed=seed)
+        insts = [Instance(ds[k], "cuda") for k in kinds * 2]
+        ids, c = _run_queue(ctx, insts)
+        for i in insts:
+            compare(i.kind, i.result(), refs[i.kind])
+        tr = _check_trace(ctx, ids, insts)
+        assert any(t.partner_kind >= 0 for t in tr)
+        ctx.close()
