@@ -267,6 +267,12 @@ kl_status kl_audit(kl_ctx* ctx, uint64_t id, uint32_t* host_out, size_t n);
 /* FindCoSchedule decision only (no launch) for the current pending set; runs the device model
  * on a prediction-cache miss.  KL_EBUSY while a phase is in flight. */
 kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out);
+/* Arrival clock for online-arrival experiments (Poisson arrivals; f3): enqueue on
+ * `stream` (cudaStream_t) a one-thread kernel that sleeps `ns` nanoseconds of device time after
+ * it starts, then writes its release time (%globaltimer, ns) to *stamp_dev (device uint64, may
+ * be NULL).  Record a kernel's ready_event on the same stream after it: the kernel arrives then.
+ * Consecutive calls on one stream give cumulative arrival times.  Errors: KL_ECUDA. */
+kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev);
 kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out);
 /* ABI self-check: writes sizeof() of kl_config, kl_profile, kl_kernel_desc, kl_slice_plan,
  * kl_candidate, kl_prediction, kl_coschedule, kl_counters, kl_trace_rec, kl_stats, then the ten

@@ -159,7 +159,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch", "kl_delay"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -198,6 +198,7 @@ def lib() -> C.CDLL:
     L.kl_struct_sizes.argtypes = [P(C.c_uint32), C.c_int]
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
     L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
+    L.kl_delay.argtypes = [_vp, C.c_uint64, _vp]
     L.kl_submit_batch.argtypes = [_vp, P(KernelDesc), C.c_size_t, P(C.c_uint64)]
     L.kl_cache_put.argtypes = [_vp, P(Candidate), P(Prediction), C.c_size_t]
     L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
@@ -295,6 +296,12 @@ class Context:
         self._check(self._L.kl_submit(self._h, C.byref(d), C.byref(out)))
         self._keep[out.value] = args
         return out.value
+
+    def delay(self, stream, ns: int, stamp_ptr: int | None = None) -> None:
+        """Arrival clock (kl_delay): sleep `ns` of device time on `stream`, then stamp the release
+        time (globaltimer ns) at device address `stamp_ptr`."""
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self._check(self._L.kl_delay(s, int(ns), stamp_ptr))
 
     def submit_many(self, items) -> list[int]:
         """items: [(kind, grid_blocks, args, tag, ready_event or None)] -> ids (one ABI call)."""

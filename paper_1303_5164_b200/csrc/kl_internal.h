@@ -160,6 +160,9 @@ KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)slice << 32);
 }
 
+// Arrival clock: sleep ns on `stream`, then write the release time (globaltimer) to *stamp.
+int kl_dev_delay(unsigned long long ns, unsigned long long* stamp, void* stream);
+
 // Occupancy re-tune encoding (see KlCtl::tune).
 KL_HD unsigned long long kl_tune_req(uint32_t epoch, uint32_t cap) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)cap << 32);

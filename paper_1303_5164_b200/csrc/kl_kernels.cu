@@ -407,6 +407,25 @@ int kl_dev_launch_plain(int kind, const void* blob, uint32_t offset, uint32_t n,
     KL_DISPATCH(kind, launch_plain, blob, offset, n, stream);
 }
 
+// Arrival clock (online arrivals): one thread sleeps until `ns` after its own start
+// (device %globaltimer), then stamps the release time; the caller records its kernel's ready
+// event after it on the same stream.
+__global__ void k_delay(unsigned long long ns, unsigned long long* stamp) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns) break;
+        __nanosleep(1000);
+    }
+    if (stamp) *stamp = t;
+}
+
+int kl_dev_delay(unsigned long long ns, unsigned long long* stamp, void* stream) {
+    k_delay<<<1, 1, 0, (cudaStream_t)stream>>>(ns, stamp);
+    return (int)cudaGetLastError();
+}
+
 // Initialise slice control blocks from a (host-mapped) list of (slot, len, gen) triples; optionally
 // reset the completion counters (kl_counters layout; t_start = INT64_MAX).
 __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters) {

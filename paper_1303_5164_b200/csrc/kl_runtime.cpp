@@ -1244,6 +1244,11 @@ kl_status kl_sync(kl_ctx* ctx, kl_counters* out) {
     return KL_OK;
 }
 
+kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev) {
+    int rc = kl_dev_delay((unsigned long long)ns, reinterpret_cast<unsigned long long*>(stamp_dev), stream);
+    return rc ? KL_ECUDA : KL_OK;
+}
+
 kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out) {
     KL_LIVE(ctx);
     if (!out) return KL_EINVAL;

@@ -126,3 +126,35 @@ def test_mc_random_coschedules_complete():
         tr = _check_trace(ctx, ids, insts)
         assert any(t.partner_kind >= 0 for t in tr)
         ctx.close()
+
+
+def test_timed_arrivals():
+    """Kernels released by the device arrival clock (kl_delay + ready events) arrive in order,
+    join R when their event completes, and all run exactly once."""
+    K.build()
+    ctx = K.Context(device=0, audit=1)
+    kinds = ["TEA", "PC", "BS", "SPMV", "TEA", "ST"]
+    ds = {k: G.gen(k, "small") for k in set(kinds)}
+    insts = [Instance(ds[k], "cuda") for k in kinds]
+    s = torch.cuda.Stream()
+    stamps = torch.zeros(len(kinds), dtype=torch.int64, device="cuda")
+    evs = []
+    for m in range(len(kinds)):
+        ctx.delay(s, 200_000, stamps.data_ptr() + 8 * m)      # 0.2 ms apart
+        ev = torch.cuda.Event()
+        ev.record(s)
+        evs.append(ev)
+    ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, evs[m]) for m, x in enumerate(insts)])
+    ctx.sync()
+    st = stamps.cpu().numpy()
+    assert np.all(np.diff(st) >= 200_000)
+    tr = _check_trace(ctx, ids, insts)
+    first = {}
+    for t in tr:
+        if t.admitted:
+            first[t.id] = min(first.get(t.id, 1 << 62), t.t0_ns)
+    for m, kid in enumerate(ids):
+        assert first[kid] >= st[m], (kinds[m], first[kid], st[m])   # never before its arrival
+    for i in insts:
+        compare(i.kind, i.result(), O.run_kernel(ds[i.kind]))
+    ctx.close()

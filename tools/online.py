@@ -1,0 +1,137 @@
+#!/usr/bin/env python
+"""f3: online arrivals (Alg.1 l.2-3 in their true online form; Poisson
+arrivals P:1179-1185) with multi-user fairness reporting.
+
+The C5 multi-user queue (16 users, each a Poisson stream from one mix) is replayed at an offered
+load rho x the sequential service rate: a device arrival clock (kl_delay on an arrival stream)
+releases each kernel at its arrival time and records its ready_event; Kernelet re-plans on every
+arrival (the event completes) and every drain, re-tuning running kernels in place.  The same
+arrival process drives two baselines: sequential FIFO (one stream, each kernel waits for its
+arrival) and plain multi-stream (4 streams round robin).  Reported per method: throughput over
+the busy period, mean / p95 response time (arrival -> completion), per-user mean slowdown
+(response / solo time of the kernel) and Jain's fairness index over users' mean slowdowns.
+usage: python tools/online.py [n_kernels] [out.json]      (needs a GPU)"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import kl_inputs as G  # noqa: E402
+import paper_1303_5164_b200 as K  # noqa: E402
+from paper_1303_5164_b200.workload import Instance, alloc_outputs, inputs_to_device  # noqa: E402
+
+
+def jain(x):
+    x = np.asarray(x, dtype=np.float64)
+    return float(x.sum() ** 2 / (len(x) * (x ** 2).sum()))
+
+
+def summarise(resp_ms, users, kinds, solo, t_first, t_last, n):
+    slow = [r / solo[k] for r, k in zip(resp_ms, kinds)]
+    per_user = {}
+    for u, s in zip(users, slow):
+        per_user.setdefault(u, []).append(s)
+    um = {u: float(np.mean(v)) for u, v in sorted(per_user.items())}
+    return {"kernels_per_s": n / ((t_last - t_first) / 1e3), "busy_ms": t_last - t_first,
+            "resp_mean_ms": float(np.mean(resp_ms)), "resp_p95_ms": float(np.percentile(resp_ms, 95)),
+            "slowdown_mean": float(np.mean(slow)), "user_mean_slowdown": um, "jain_users": jain(list(um.values()))}
+
+
+def main(n, out_path):
+    dev = torch.device("cuda", 0)
+    profiles, kcfg = bench.load_profiles(os.path.join(ROOT, "profiles", "kl_profile_b200.json"))
+    q = G.multi_user_queue(n, 16, seed=7)
+    kinds = [e["kind"] for e in q]
+    users = [e["user"] for e in q]
+    arr = np.array([e["arrival"] for e in q])
+    data = {k: G.gen(k, "paper") for k in sorted(set(kinds))}
+    inputs = {k: inputs_to_device(data[k], dev) for k in data}
+    pools, seen, insts = {}, {}, []
+    for k in kinds:
+        j = seen.get(k, 0)
+        seen[k] = j + 1
+        if j < 4:
+            pools.setdefault(k, []).append(alloc_outputs(k, data[k]["params"], dev))
+        insts.append(Instance(data[k], dev, inputs=inputs[k], outputs=pools[k][j % 4]))
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    ctx = K.Context(device=0, profiles=profiles, counters=counters, split_rule=1, **kcfg)
+    # solo time per kind (plain launch, full occupancy)
+    solo = {}
+    for k in data:
+        i = next(x for x in insts if x.kind == k)
+        ts = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.run_plain(k, i.grid, i.args, 0)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        solo[k] = statistics.median(ts)
+    seq_ms = sum(solo[k] for k in kinds)
+    res = {"n": n, "users": 16, "solo_ms": solo, "sequential_work_ms": seq_ms, "loads": {}}
+    arr_stream = torch.cuda.Stream(device=dev)
+    for rho in (0.8, 1.0, 1.25):
+        # arrival times scaled so that the offered load is rho x the sequential service rate
+        span = seq_ms / rho
+        t = (arr - arr[0]) / max(arr[-1] - arr[0], 1e-12) * span * 1e6 if n > 1 else np.zeros(1)
+        gaps = np.diff(np.concatenate([[0.0], t])).astype(np.int64)
+        out = {}
+        # --- Kernelet
+        stamps = torch.zeros(n, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize()
+        ctx.reset_model_cache()
+        ctx.reset_counters()
+        n0 = len(ctx.trace())
+        evs = []
+        for i in range(n):
+            ctx.delay(arr_stream, int(gaps[i]), stamps.data_ptr() + 8 * i)
+            ev = torch.cuda.Event()
+            ev.record(arr_stream)
+            evs.append(ev)
+        ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, evs[m]) for m, x in enumerate(insts)])
+        ctx.sync()
+        torch.cuda.synchronize()
+        tr = ctx.trace()[n0:]
+        done = {t_.id: t_.t1_ns for t_ in tr if t_.exhausted}
+        st = stamps.cpu().numpy()
+        resp = [(done[kid] - st[m]) / 1e6 for m, kid in enumerate(ids)]
+        out["kernelet"] = summarise(resp, users, kinds, solo, st[0] / 1e6, max(done.values()) / 1e6, n)
+        # --- sequential FIFO and plain multi-stream (4 streams), same arrival process
+        for name, nstreams in (("sequential", 1), ("multistream4", 4)):
+            streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
+            torch.cuda.synchronize()
+            a_ev, d_ev = [], []
+            for i in range(n):
+                ctx.delay(arr_stream, int(gaps[i]), None)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(arr_stream)
+                a_ev.append(ev)
+            for m, x in enumerate(insts):
+                s = streams[m % nstreams]
+                s.wait_event(a_ev[m])
+                ctx.run_plain(x.kind, x.grid, x.args, s)
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                d_ev.append(ev)
+            torch.cuda.synchronize()
+            resp = [a.elapsed_time(d) for a, d in zip(a_ev, d_ev)]
+            last = max(a_ev[0].elapsed_time(d) for d in d_ev)
+            out[name] = summarise(resp, users, kinds, solo, 0.0, last, n)
+        res["loads"][str(rho)] = out
+        print(rho, {m: {f: round(v[f], 3) for f in ("kernels_per_s", "resp_mean_ms", "resp_p95_ms",
+                                                     "slowdown_mean", "jain_users")} for m, v in out.items()},
+              flush=True)
+    ctx.close()
+    json.dump(res, open(out_path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 320,
+         sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "online.json"))
