@@ -11,6 +11,12 @@ import ctypes as C
 import os
 import subprocess
 
+# The runtime drives a pool of 8 launch streams plus control, stop and caller streams; with the
+# default 8 hardware work queues, unrelated streams would share a FIFO and falsely serialise
+# (e.g. a launch queued behind an arrival clock).  Effective only if set before the process
+# creates its CUDA context, so entry points (bench.py, tools, tests) import this package first.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "libkl.so")

@@ -43,6 +43,9 @@ def summarise(resp_ms, users, kinds, solo, t_first, t_last, n):
             "slowdown_mean": float(np.mean(slow)), "user_mean_slowdown": um, "jain_users": jain(list(um.values()))}
 
 
+RHOS = [float(x) for x in os.environ.get("RHOS", "0.8,1.0,1.25").split(",")]
+
+
 def main(n, out_path):
     dev = torch.device("cuda", 0)
     profiles, kcfg = bench.load_profiles(os.path.join(ROOT, "profiles", "kl_profile_b200.json"))
@@ -77,7 +80,7 @@ def main(n, out_path):
     seq_ms = sum(solo[k] for k in kinds)
     res = {"n": n, "users": 16, "solo_ms": solo, "sequential_work_ms": seq_ms, "loads": {}}
     arr_stream = torch.cuda.Stream(device=dev)
-    for rho in (0.8, 1.0, 1.25):
+    for rho in RHOS:
         # arrival times scaled so that the offered load is rho x the sequential service rate
         span = seq_ms / rho
         t = (arr - arr[0]) / max(arr[-1] - arr[0], 1e-12) * span * 1e6 if n > 1 else np.zeros(1)
@@ -103,6 +106,15 @@ def main(n, out_path):
         st = stamps.cpu().numpy()
         resp = [(done[kid] - st[m]) / 1e6 for m, kid in enumerate(ids)]
         out["kernelet"] = summarise(resp, users, kinds, solo, st[0] / 1e6, max(done.values()) / 1e6, n)
+        first = {}
+        for t_ in tr:
+            if t_.admitted:
+                first[t_.id] = min(first.get(t_.id, 1 << 62), t_.t0_ns)
+        z = int(st[0])
+        out["kernelet"]["per_kernel"] = [{"kind": kinds[m], "user": users[m], "gap_us": int(gaps[m]) / 1e3,
+                                          "arrive_us": (int(st[m]) - z) / 1e3,
+                                          "start_us": (first.get(kid, z) - z) / 1e3, "done_us": (done[kid] - z) / 1e3}
+                                         for m, kid in enumerate(ids)]
         # --- sequential FIFO and plain multi-stream (4 streams), same arrival process
         for name, nstreams in (("sequential", 1), ("multistream4", 4)):
             streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
