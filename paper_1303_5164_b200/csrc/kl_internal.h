@@ -160,6 +160,11 @@ KL_HD unsigned long long kl_stop_req(uint32_t epoch, uint32_t slice) {
     return 1ull | ((unsigned long long)(epoch & 0x7fu) << 1) | ((unsigned long long)slice << 32);
 }
 
+// Eager one-time setup (kl_create): load every library kernel, model constant tables.
+int kl_dev_preload();
+int kl_dev_model_init();
+int kl_dev_model3_init();
+
 // Arrival clock: sleep ns on `stream`, then write the release time (globaltimer) to *stamp.
 int kl_dev_delay(unsigned long long ns, unsigned long long* stamp, void* stream);
 

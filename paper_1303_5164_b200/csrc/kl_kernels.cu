@@ -384,6 +384,14 @@ static const uint32_t kArgBytes[KL_NKINDS] = {
 
 uint32_t kl_args_size(int kind) { return (kind >= 0 && kind < KL_NKINDS) ? kArgBytes[kind] : 0u; }
 
+template <class Body>
+int preload_of() {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_plain<Body>);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaFuncGetAttributes(&fa, k_persistent<Body>);
+}
+
 int kl_dev_kind_info(int kind, KlKindInfo* out) {
     if (kind == KL_MM) return kl_mm_info(out);
     KL_DISPATCH(kind, info_of, out);
@@ -459,5 +467,21 @@ int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned lon
     const int blocks = n > 0 ? (n + 255) / 256 : 1;
     k_ctl_init<<<blocks, 256, 0, (cudaStream_t)stream>>>(pool, slots_lens, n, counters);
     return (int)cudaGetLastError();
+}
+
+// Load every kernel of this file now (called by kl_create): with lazy module loading, a first
+// launch during scheduling would synchronise the device behind unrelated streams.
+int kl_dev_preload() {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k_ctl_init);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncGetAttributes(&fa, k_delay);
+    if (e != cudaSuccess) return (int)e;
+    for (int kind = 0; kind < KL_NKINDS; ++kind) {
+        if (kind == KL_MM) continue;
+        int rc = [&]() -> int { KL_DISPATCH(kind, preload_of); }();
+        if (rc) return rc;
+    }
+    return 0;
 }
 

@@ -262,6 +262,23 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
 
 }  // namespace
 
+// One-time setup, called by kl_create (eager: a lazily loaded kernel or a symbol copy during
+// scheduling would synchronise the device behind unrelated streams).
+int kl_dev_model_init() {
+    const size_t smem = sizeof(double) * (kMaxS * kMaxS + 2 * kMaxS + 16);
+    cudaError_t e = cudaFuncSetAttribute(k_model_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    double tab[17][17] = {};
+    for (int n = 0; n <= 16; ++n) {
+        tab[n][0] = 1.0;
+        for (int k = 1; k <= n; ++k) tab[n][k] = tab[n - 1][k - 1] + (k <= n - 1 ? tab[n - 1][k] : 0.0);
+    }
+    e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
+    if (e != cudaSuccess) return (int)e;
+    cudaFuncAttributes fa;
+    return (int)cudaFuncGetAttributes(&fa, k_model_batch);
+}
+
 int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands,
                        kl_prediction* preds, int n_pairs, const int32_t* pair_off,
                        uint32_t* done_counter, KlDecision* dec, void* stream) {
@@ -269,15 +286,8 @@ int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* c
     const size_t smem = sizeof(double) * (kMaxS * kMaxS + 2 * kMaxS + 16);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_model_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        double tab[17][17] = {};
-        for (int n = 0; n <= 16; ++n) {
-            tab[n][0] = 1.0;
-            for (int k = 1; k <= n; ++k) tab[n][k] = tab[n - 1][k - 1] + (k <= n - 1 ? tab[n - 1][k] : 0.0);
-        }
-        e = cudaMemcpyToSymbol(c_binom, tab, sizeof(tab));
-        if (e != cudaSuccess) return (int)e;
+        int e = kl_dev_model_init();
+        if (e) return e;
         attr = true;
     }
     k_model_batch<<<cfg.n_cand, kThreads, smem, (cudaStream_t)stream>>>(kinds, cfg, cands, preds, n_pairs,

@@ -307,19 +307,26 @@ k_model_general(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, con
 
 }  // namespace
 
+int kl_dev_model3_init() {
+    double tab[kMaxU + 1][kMaxU + 1] = {};
+    for (int n = 0; n <= kMaxU; ++n) {
+        tab[n][0] = 1.0;
+        for (int k = 1; k <= n; ++k) tab[n][k] = tab[n - 1][k - 1] + (k <= n - 1 ? tab[n - 1][k] : 0.0);
+    }
+    cudaError_t e = cudaMemcpyToSymbol(c_binom3, tab, sizeof(tab));
+    if (e != cudaSuccess) return (int)e;
+    cudaFuncAttributes fa;
+    return (int)cudaFuncGetAttributes(&fa, k_model_general);
+}
+
 int kl_dev_model_general(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands, kl_prediction* preds,
                          int n_pairs, const int32_t* pair_off, uint32_t* done_counter, KlDecision* dec,
                          double* scratch, const int64_t* scratch_off, void* stream) {
     if (cfg.n_cand <= 0) return 0;
     static bool init = false;
     if (!init) {
-        double tab[kMaxU + 1][kMaxU + 1] = {};
-        for (int n = 0; n <= kMaxU; ++n) {
-            tab[n][0] = 1.0;
-            for (int k = 1; k <= n; ++k) tab[n][k] = tab[n - 1][k - 1] + (k <= n - 1 ? tab[n - 1][k] : 0.0);
-        }
-        cudaError_t e = cudaMemcpyToSymbol(c_binom3, tab, sizeof(tab));
-        if (e != cudaSuccess) return (int)e;
+        int e = kl_dev_model3_init();
+        if (e) return e;
         init = true;
     }
     k_model_general<<<cfg.n_cand, kThreads, 0, (cudaStream_t)stream>>>(kinds, cfg, cands, preds, n_pairs, pair_off,

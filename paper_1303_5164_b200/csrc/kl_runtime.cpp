@@ -994,6 +994,10 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             ctx->max_regs = prop.regsPerMultiprocessor;
             ctx->max_smem = (int)prop.sharedMemPerMultiprocessor;
             if (ctx->n_sms > KL_MAX_SMS) return KL_EINVAL;
+            // eager: load every kernel and constant table now, not during scheduling
+            if (int rc = kl_dev_preload()) return ctx->fail(KL_ECUDA, "preload: %s", cudaGetErrorString((cudaError_t)rc));
+            if (int rc = kl_dev_model_init()) return ctx->fail(KL_ECUDA, "model init: %s", cudaGetErrorString((cudaError_t)rc));
+            if (int rc = kl_dev_model3_init()) return ctx->fail(KL_ECUDA, "model3 init: %s", cudaGetErrorString((cudaError_t)rc));
             for (int k = 0; k < KL_NKINDS; ++k) {
                 int rc = kl_dev_kind_info(k, &ctx->info[k]);
                 ctx->info_ok[k] = (rc == 0);
