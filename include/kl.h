@@ -151,9 +151,13 @@ typedef struct {
                                   P:1000-1019, reading R27) */
     int32_t granularity;       /* 0 (default): warps; 1: thread blocks as the modelling unit
                                   (reading R13: units of wpb/n_sched warps) */
+    int32_t age_limit_us;      /* > 0: starvation guard (serving extension, f3; 0 = the paper's
+                                  greedy): once the oldest pending kernel has waited longer than
+                                  this, only co-schedules that include it are considered */
     int32_t mc_seed;           /* != 0: MC(s) comparator: every decision picks a
                                   uniformly random pending kind pair and maximal slice ratio
                                   (no model); the seed selects the random stream */
+    int32_t pad0;
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
@@ -196,6 +200,7 @@ typedef struct {               /* runtime statistics since kl_create */
     int64_t model_ns;          /* host time spent waiting for model batches */
     int64_t retunes;           /* in-place occupancy changes of a running kernel (no stop) */
     int64_t topups;            /* top-up grids launched by re-tunes that raised the occupancy */
+    int64_t aged;              /* decisions restricted by the starvation guard */
 } kl_stats;
 typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;

@@ -73,7 +73,13 @@ struct Inst {
     Launch* inflight = nullptr; // at most one launch in flight per kernel
     uint32_t* audit = nullptr;
     void* ready = nullptr;      // cudaEvent_t: the kernel arrives (joins R) once it completes
+    int64_t t_join = 0;         // host steady-clock ns when it joined R (starvation guard)
 };
+
+inline int64_t now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
 
 struct Launch {
     Inst* k = nullptr;
@@ -448,6 +454,15 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             seen_pair[lo][hi] = true;
             pairs.push_back({reps[a], reps[b]});
         }
+    // starvation guard (serving extension, off by default = the paper's greedy): once the oldest
+    // pending kernel has waited longer than age_limit_us, only co-schedules that include it
+    if (ctx->cfg.age_limit_us > 0 && now_ns() - R[0]->t_join > (int64_t)ctx->cfg.age_limit_us * 1000) {
+        std::vector<std::pair<int, int>> with0;
+        for (auto& pq : pairs)
+            if (pq.first == 0 || pq.second == 0) with0.push_back(pq);
+        pairs.swap(with0);
+        ctx->st.aged++;
+    }
     // pruning with relaxation
     double ap = ctx->cfg.alpha_p, am = ctx->cfg.alpha_m;
     std::vector<std::pair<int, int>> keep;
@@ -794,6 +809,7 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
         if (e == cudaErrorNotReady) { ++i; continue; }
         if (e != cudaSuccess) return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id, cudaGetErrorString(e));
         auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
+        k->t_join = now_ns();
         ctx->R.insert(pos, k);
         ctx->arriving.erase(ctx->arriving.begin() + i);
         *replan = *progress = true;
@@ -1147,7 +1163,10 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     Inst* raw = k.get();
     ctx->by_id[raw->id] = raw;
     if (raw->ready && !ctx->host_only) ctx->arriving.push_back(raw);   // arrives when its inputs land
-    else ctx->R.push_back(raw);
+    else {
+        raw->t_join = now_ns();
+        ctx->R.push_back(raw);
+    }
     ctx->insts.push_back(std::move(k));
     if (out_id) *out_id = raw->id;
     return KL_OK;

@@ -10,6 +10,9 @@ arrival process drives two baselines: sequential FIFO (one stream, each kernel w
 arrival) and plain multi-stream (4 streams round robin).  Reported per method: throughput over
 the busy period, mean / p95 response time (arrival -> completion), per-user mean slowdown
 (response / solo time of the kernel) and Jain's fairness index over users' mean slowdowns.
+Kernelet runs twice: the paper's greedy (throughput only), and with the starvation guard
+(kl_config.age_limit_us: once the oldest pending kernel waited longer, only co-schedules that
+include it are considered).
 usage: python tools/online.py [n_kernels] [out.json]      (needs a GPU)"""
 import json
 import os
@@ -44,6 +47,7 @@ def summarise(resp_ms, users, kinds, solo, t_first, t_last, n):
 
 
 RHOS = [float(x) for x in os.environ.get("RHOS", "0.8,1.0,1.25").split(",")]
+AGE_US = int(os.environ.get("AGE_US", "4000"))   # starvation guard of the kernelet_aged run
 
 
 def main(n, out_path):
@@ -86,35 +90,40 @@ def main(n, out_path):
         t = (arr - arr[0]) / max(arr[-1] - arr[0], 1e-12) * span * 1e6 if n > 1 else np.zeros(1)
         gaps = np.diff(np.concatenate([[0.0], t])).astype(np.int64)
         out = {}
-        # --- Kernelet
-        stamps = torch.zeros(n, dtype=torch.int64, device=dev)
-        torch.cuda.synchronize()
-        ctx.reset_model_cache()
-        ctx.reset_counters()
-        n0 = len(ctx.trace())
-        evs = []
-        for i in range(n):
-            ctx.delay(arr_stream, int(gaps[i]), stamps.data_ptr() + 8 * i)
-            ev = torch.cuda.Event()
-            ev.record(arr_stream)
-            evs.append(ev)
-        ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, evs[m]) for m, x in enumerate(insts)])
-        ctx.sync()
-        torch.cuda.synchronize()
-        tr = ctx.trace()[n0:]
-        done = {t_.id: t_.t1_ns for t_ in tr if t_.exhausted}
-        st = stamps.cpu().numpy()
-        resp = [(done[kid] - st[m]) / 1e6 for m, kid in enumerate(ids)]
-        out["kernelet"] = summarise(resp, users, kinds, solo, st[0] / 1e6, max(done.values()) / 1e6, n)
-        first = {}
-        for t_ in tr:
-            if t_.admitted:
-                first[t_.id] = min(first.get(t_.id, 1 << 62), t_.t0_ns)
-        z = int(st[0])
-        out["kernelet"]["per_kernel"] = [{"kind": kinds[m], "user": users[m], "gap_us": int(gaps[m]) / 1e3,
-                                          "arrive_us": (int(st[m]) - z) / 1e3,
-                                          "start_us": (first.get(kid, z) - z) / 1e3, "done_us": (done[kid] - z) / 1e3}
-                                         for m, kid in enumerate(ids)]
+        # --- Kernelet: the paper's greedy, and with the starvation guard (serving extension)
+        for name, age in (("kernelet", 0), ("kernelet_aged", AGE_US)):
+            ctx.config.age_limit_us = age
+            ctx.close()
+            ctx = K.Context(device=0, profiles=profiles, counters=counters, split_rule=1, age_limit_us=age, **kcfg)
+            stamps = torch.zeros(n, dtype=torch.int64, device=dev)
+            torch.cuda.synchronize()
+            n0 = len(ctx.trace())
+            s0 = ctx.stats()
+            evs = []
+            for i in range(n):
+                ctx.delay(arr_stream, int(gaps[i]), stamps.data_ptr() + 8 * i)
+                ev = torch.cuda.Event()
+                ev.record(arr_stream)
+                evs.append(ev)
+            ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, evs[m]) for m, x in enumerate(insts)])
+            ctx.sync()
+            torch.cuda.synchronize()
+            s1 = ctx.stats()
+            tr = ctx.trace()[n0:]
+            done = {t_.id: t_.t1_ns for t_ in tr if t_.exhausted}
+            st = stamps.cpu().numpy()
+            resp = [(done[kid] - st[m]) / 1e6 for m, kid in enumerate(ids)]
+            out[name] = summarise(resp, users, kinds, solo, st[0] / 1e6, max(done.values()) / 1e6, n)
+            out[name]["stats"] = {f: getattr(s1, f) - getattr(s0, f) for f, _ in K.Stats._fields_}
+            out[name]["age_limit_us"] = age
+            first = {}
+            for t_ in tr:
+                if t_.admitted:
+                    first[t_.id] = min(first.get(t_.id, 1 << 62), t_.t0_ns)
+            z = int(st[0])
+            out[name]["per_kernel"] = [{"kind": kinds[m], "user": users[m], "arrive_us": (int(st[m]) - z) / 1e3,
+                                        "start_us": (first.get(kid, z) - z) / 1e3, "done_us": (done[kid] - z) / 1e3}
+                                       for m, kid in enumerate(ids)]
         # --- sequential FIFO and plain multi-stream (4 streams), same arrival process
         for name, nstreams in (("sequential", 1), ("multistream4", 4)):
             streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
