@@ -47,7 +47,8 @@ def summarise(resp_ms, users, kinds, solo, t_first, t_last, n):
 
 
 RHOS = [float(x) for x in os.environ.get("RHOS", "0.8,1.0,1.25").split(",")]
-AGE_US = int(os.environ.get("AGE_US", "4000"))   # starvation guard of the kernelet_aged run
+AGE_US = int(os.environ.get("AGE_US", "4000"))
+LEAD_MS = 30.0   # starvation guard of the kernelet_aged run
 
 
 def main(n, out_path):
@@ -89,6 +90,9 @@ def main(n, out_path):
         span = seq_ms / rho
         t = (arr - arr[0]) / max(arr[-1] - arr[0], 1e-12) * span * 1e6 if n > 1 else np.zeros(1)
         gaps = np.diff(np.concatenate([[0.0], t])).astype(np.int64)
+        # lead-in: the arrival clock starts before the host has enqueued every submission / launch;
+        # the first arrival waits LEAD_MS so that no method is measured while its host still submits
+        gaps[0] += int(LEAD_MS * 1e6)
         out = {}
         # --- Kernelet: the paper's greedy, and with the starvation guard (serving extension)
         for name, age in (("kernelet", 0), ("kernelet_aged", AGE_US)):
