@@ -174,6 +174,9 @@ typedef struct {
     uint64_t tag;              /* user tag, summed into the completion checksum */
     void* ready_event;         /* cudaEvent_t every launch of the kernel waits on (its inputs
                                   landed: the kernel's arrival), or NULL */
+    const volatile uint32_t* ready_flag;   /* host-visible word (e.g. written by kl_arrival_clock
+                                  through mapped memory): the kernel arrives when it becomes
+                                  non-zero; NULL = no flag.  Checked after ready_event. */
 } kl_kernel_desc;
 
 typedef struct { uint32_t slice_blocks, n_slices, blocks_per_sm, waves; } kl_slice_plan;
@@ -278,6 +281,17 @@ kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out);
  * be NULL).  Record a kernel's ready_event on the same stream after it: the kernel arrives then.
  * Consecutive calls on one stream give cumulative arrival times.  Errors: KL_ECUDA. */
 kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev);
+/* Arrival clock for n arrivals in one resident thread (no per-arrival launch, so the arrivals
+ * never wait for an SM slot): enqueue on `stream` a one-thread kernel that, for i = 0..n-1,
+ * sleeps gaps_dev[i] ns of device time after the previous release, writes the release time
+ * (%globaltimer) to stamps_dev[i] and then sets flags[i] = 1 (flags: host-mapped memory, the
+ * kernels' kl_kernel_desc.ready_flag).  gaps_dev, stamps_dev: device uint64[n].  The kernel
+ * occupies one warp slot of one SM until the last release.  Errors: KL_ECUDA. */
+/* Stream gate / time stamp (one thread): waits until *flag != 0 (flag may be NULL: no wait), then
+ * writes %globaltimer to *stamp_dev (may be NULL).  For baselines driven by kl_arrival_clock. */
+kl_status kl_wait_flag(void* stream, const volatile uint32_t* flag, uint64_t* stamp_dev);
+kl_status kl_arrival_clock(void* stream, const uint64_t* gaps_dev, uint64_t* stamps_dev, uint32_t* flags,
+                           uint32_t n);
 kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out);
 /* ABI self-check: writes sizeof() of kl_config, kl_profile, kl_kernel_desc, kl_slice_plan,
  * kl_candidate, kl_prediction, kl_coschedule, kl_counters, kl_trace_rec, kl_stats, then the ten

@@ -120,7 +120,7 @@ class Config(C.Structure):
 
 class KernelDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("grid_blocks", C.c_uint32), ("args", _vp), ("args_bytes", C.c_uint32),
-                ("profile", C.POINTER(Profile)), ("tag", C.c_uint64), ("ready_event", _vp)]
+                ("profile", C.POINTER(Profile)), ("tag", C.c_uint64), ("ready_event", _vp), ("ready_flag", _vp)]
 
 
 class SlicePlan(C.Structure):
@@ -165,7 +165,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch", "kl_delay"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch", "kl_delay", "kl_arrival_clock", "kl_wait_flag"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -205,6 +205,8 @@ def lib() -> C.CDLL:
     L.kl_stats_get.argtypes = [_vp, P(Stats)]
     L.kl_run_capped.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(C.c_double)]
     L.kl_delay.argtypes = [_vp, C.c_uint64, _vp]
+    L.kl_arrival_clock.argtypes = [_vp, _vp, _vp, _vp, C.c_uint32]
+    L.kl_wait_flag.argtypes = [_vp, _vp, _vp]
     L.kl_submit_batch.argtypes = [_vp, P(KernelDesc), C.c_size_t, P(C.c_uint64)]
     L.kl_cache_put.argtypes = [_vp, P(Candidate), P(Prediction), C.c_size_t]
     L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
@@ -309,14 +311,28 @@ class Context:
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         self._check(self._L.kl_delay(s, int(ns), stamp_ptr))
 
+    def arrival_clock(self, stream, gaps_ptr: int, stamps_ptr: int, flags_ptr: int, n: int) -> None:
+        """kl_arrival_clock: one resident thread releases n arrivals (device pointers gaps/stamps,
+        host-mapped flags)."""
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self._check(self._L.kl_arrival_clock(s, gaps_ptr, stamps_ptr, flags_ptr, n))
+
+    def wait_flag(self, stream, flag_ptr: int | None, stamp_ptr: int | None = None) -> None:
+        """kl_wait_flag: gate `stream` on a host-visible flag and/or stamp the device time."""
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        self._check(self._L.kl_wait_flag(s, flag_ptr, stamp_ptr))
+
     def submit_many(self, items) -> list[int]:
-        """items: [(kind, grid_blocks, args, tag, ready_event or None)] -> ids (one ABI call)."""
+        """items: [(kind, grid_blocks, args, tag, ready_event or None[, ready_flag address])]
+        -> ids (one ABI call)."""
         n = len(items)
         arr = (KernelDesc * max(n, 1))()
-        for i, (kind, grid, args, tag, ev) in enumerate(items):
+        for i, it in enumerate(items):
+            kind, grid, args, tag, ev = it[:5]
+            flag = it[5] if len(it) > 5 else None
             kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
             e = getattr(ev, "cuda_event", ev) if ev is not None else None
-            arr[i] = KernelDesc(kid, grid, C.cast(C.pointer(args), _vp), C.sizeof(args), None, tag, e)
+            arr[i] = KernelDesc(kid, grid, C.cast(C.pointer(args), _vp), C.sizeof(args), None, tag, e, flag)
         ids = (C.c_uint64 * max(n, 1))()
         self._check(self._L.kl_submit_batch(self._h, arr, n, ids))
         out = list(ids)[:n]

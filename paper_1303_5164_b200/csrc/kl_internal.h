@@ -167,6 +167,9 @@ int kl_dev_model3_init();
 
 // Arrival clock: sleep ns on `stream`, then write the release time (globaltimer) to *stamp.
 int kl_dev_delay(unsigned long long ns, unsigned long long* stamp, void* stream);
+int kl_dev_wait_flag(const volatile uint32_t* flag, unsigned long long* stamp, void* stream);
+int kl_dev_arrival_clock(const unsigned long long* gaps, unsigned long long* stamps, uint32_t* flags, uint32_t n,
+                         void* stream);
 
 // Occupancy re-tune encoding (see KlCtl::tune).
 KL_HD unsigned long long kl_tune_req(uint32_t epoch, uint32_t cap) {

@@ -429,6 +429,47 @@ __global__ void k_delay(unsigned long long ns, unsigned long long* stamp) {
     if (stamp) *stamp = t;
 }
 
+// Resident arrival clock: one thread releases n arrivals at cumulative device-time gaps.
+__global__ void k_arrival_clock(const unsigned long long* gaps, unsigned long long* stamps, volatile uint32_t* flags,
+                                uint32_t n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned long long due = t;
+    for (uint32_t i = 0; i < n; ++i) {
+        due += gaps[i];
+        for (;;) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t >= due) break;
+            __nanosleep(500);
+        }
+        stamps[i] = t;
+        __threadfence_system();
+        flags[i] = 1u;
+        __threadfence_system();
+    }
+}
+
+int kl_dev_arrival_clock(const unsigned long long* gaps, unsigned long long* stamps, uint32_t* flags, uint32_t n,
+                         void* stream) {
+    k_arrival_clock<<<1, 1, 0, (cudaStream_t)stream>>>(gaps, stamps, flags, n);
+    return (int)cudaGetLastError();
+}
+
+__global__ void k_wait_flag(const volatile uint32_t* flag, unsigned long long* stamp) {
+    if (flag)
+        while (*flag == 0u) __nanosleep(500);
+    if (stamp) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        *stamp = t;
+    }
+}
+
+int kl_dev_wait_flag(const volatile uint32_t* flag, unsigned long long* stamp, void* stream) {
+    k_wait_flag<<<1, 1, 0, (cudaStream_t)stream>>>(flag, stamp);
+    return (int)cudaGetLastError();
+}
+
 int kl_dev_delay(unsigned long long ns, unsigned long long* stamp, void* stream) {
     k_delay<<<1, 1, 0, (cudaStream_t)stream>>>(ns, stamp);
     return (int)cudaGetLastError();
@@ -476,6 +517,10 @@ int kl_dev_preload() {
     cudaError_t e = cudaFuncGetAttributes(&fa, k_ctl_init);
     if (e != cudaSuccess) return (int)e;
     e = cudaFuncGetAttributes(&fa, k_delay);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncGetAttributes(&fa, k_arrival_clock);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncGetAttributes(&fa, k_wait_flag);
     if (e != cudaSuccess) return (int)e;
     for (int kind = 0; kind < KL_NKINDS; ++kind) {
         if (kind == KL_MM) continue;

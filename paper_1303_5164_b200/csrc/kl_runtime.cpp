@@ -73,6 +73,7 @@ struct Inst {
     Launch* inflight = nullptr; // at most one launch in flight per kernel
     uint32_t* audit = nullptr;
     void* ready = nullptr;      // cudaEvent_t: the kernel arrives (joins R) once it completes
+    const volatile uint32_t* ready_flag = nullptr;   // host-visible arrival word (non-zero = arrived)
     int64_t t_join = 0;         // host steady-clock ns when it joined R (starvation guard)
 };
 
@@ -805,9 +806,13 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
     // only the oldest few are queried per poll: ready events of one copy stream complete in order
     for (size_t i = 0; i < ctx->arriving.size() && i < 4;) {
         Inst* k = ctx->arriving[i];
-        cudaError_t e = cudaEventQuery((cudaEvent_t)k->ready);
-        if (e == cudaErrorNotReady) { ++i; continue; }
-        if (e != cudaSuccess) return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id, cudaGetErrorString(e));
+        if (k->ready) {
+            cudaError_t e = cudaEventQuery((cudaEvent_t)k->ready);
+            if (e == cudaErrorNotReady) { ++i; continue; }
+            if (e != cudaSuccess)
+                return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id, cudaGetErrorString(e));
+        }
+        if (k->ready_flag && *k->ready_flag == 0u) { ++i; continue; }
         auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
         k->t_join = now_ns();
         ctx->R.insert(pos, k);
@@ -1143,6 +1148,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     k->grid = d->grid_blocks;
     k->tag = d->tag;
     k->ready = d->ready_event;
+    k->ready_flag = d->ready_flag;
     if (!ctx->host_only) {
         if (kl_dev_prepare(d->kind, d->args, d->args_bytes, k->blob, kBlob))
             return ctx->fail(KL_EINVAL, "cannot prepare args of kind %d", d->kind);
@@ -1162,7 +1168,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     }
     Inst* raw = k.get();
     ctx->by_id[raw->id] = raw;
-    if (raw->ready && !ctx->host_only) ctx->arriving.push_back(raw);   // arrives when its inputs land
+    if ((raw->ready || raw->ready_flag) && !ctx->host_only) ctx->arriving.push_back(raw);   // arrives later
     else {
         raw->t_join = now_ns();
         ctx->R.push_back(raw);
@@ -1269,6 +1275,19 @@ kl_status kl_sync(kl_ctx* ctx, kl_counters* out) {
 
 kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev) {
     int rc = kl_dev_delay((unsigned long long)ns, reinterpret_cast<unsigned long long*>(stamp_dev), stream);
+    return rc ? KL_ECUDA : KL_OK;
+}
+
+kl_status kl_wait_flag(void* stream, const volatile uint32_t* flag, uint64_t* stamp_dev) {
+    int rc = kl_dev_wait_flag(flag, reinterpret_cast<unsigned long long*>(stamp_dev), stream);
+    return rc ? KL_ECUDA : KL_OK;
+}
+
+kl_status kl_arrival_clock(void* stream, const uint64_t* gaps_dev, uint64_t* stamps_dev, uint32_t* flags, uint32_t n) {
+    if (!n) return KL_OK;
+    if (!gaps_dev || !stamps_dev || !flags) return KL_EINVAL;
+    int rc = kl_dev_arrival_clock(reinterpret_cast<const unsigned long long*>(gaps_dev),
+                                  reinterpret_cast<unsigned long long*>(stamps_dev), flags, n, stream);
     return rc ? KL_ECUDA : KL_OK;
 }
 

@@ -3,11 +3,12 @@
 arrivals P:1179-1185) with multi-user fairness reporting.
 
 The C5 multi-user queue (16 users, each a Poisson stream from one mix) is replayed at an offered
-load rho x the sequential service rate: a device arrival clock (kl_delay on an arrival stream)
-releases each kernel at its arrival time and records its ready_event; Kernelet re-plans on every
-arrival (the event completes) and every drain, re-tuning running kernels in place.  The same
-arrival process drives two baselines: sequential FIFO (one stream, each kernel waits for its
-arrival) and plain multi-stream (4 streams round robin).  Reported per method: throughput over
+load rho x the sequential service rate: a resident device arrival clock (kl_arrival_clock, one
+thread for the whole run, so arrivals never wait for an SM slot) releases each kernel at its
+arrival time by setting its host-mapped ready_flag; Kernelet re-plans on every arrival and every
+drain, re-tuning running kernels in place.  The same clock drives two baselines: sequential FIFO
+(one stream) and plain multi-stream (4 streams round robin), each launch gated on its flag
+(kl_wait_flag) and its completion stamped on the device.  Reported per method: throughput over
 the busy period, mean / p95 response time (arrival -> completion), per-user mean slowdown
 (response / solo time of the kernel) and Jain's fairness index over users' mean slowdowns.
 Kernelet runs twice: the paper's greedy (throughput only), and with the starvation guard
@@ -90,26 +91,28 @@ def main(n, out_path):
         span = seq_ms / rho
         t = (arr - arr[0]) / max(arr[-1] - arr[0], 1e-12) * span * 1e6 if n > 1 else np.zeros(1)
         gaps = np.diff(np.concatenate([[0.0], t])).astype(np.int64)
-        # lead-in: the arrival clock starts before the host has enqueued every submission / launch;
-        # the first arrival waits LEAD_MS so that no method is measured while its host still submits
+        # lead-in: every method has enqueued all its work before the first arrival
         gaps[0] += int(LEAD_MS * 1e6)
+        gaps_d = torch.tensor(gaps, dtype=torch.int64, device=dev)
         out = {}
+
+        def clock():
+            """Fresh flags (host-mapped) and stamps; start the resident arrival clock."""
+            flags = torch.zeros(n, dtype=torch.int32).pin_memory()
+            stamps = torch.zeros(n, dtype=torch.int64, device=dev)
+            return flags, stamps
+
         # --- Kernelet: the paper's greedy, and with the starvation guard (serving extension)
         for name, age in (("kernelet", 0), ("kernelet_aged", AGE_US)):
-            ctx.config.age_limit_us = age
             ctx.close()
             ctx = K.Context(device=0, profiles=profiles, counters=counters, split_rule=1, age_limit_us=age, **kcfg)
-            stamps = torch.zeros(n, dtype=torch.int64, device=dev)
+            flags, stamps = clock()
             torch.cuda.synchronize()
             n0 = len(ctx.trace())
             s0 = ctx.stats()
-            evs = []
-            for i in range(n):
-                ctx.delay(arr_stream, int(gaps[i]), stamps.data_ptr() + 8 * i)
-                ev = torch.cuda.Event()
-                ev.record(arr_stream)
-                evs.append(ev)
-            ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, evs[m]) for m, x in enumerate(insts)])
+            ids = ctx.submit_many([(x.kind, x.grid, x.args, m + 1, None, flags.data_ptr() + 4 * m)
+                                   for m, x in enumerate(insts)])
+            ctx.arrival_clock(arr_stream, gaps_d.data_ptr(), stamps.data_ptr(), flags.data_ptr(), n)
             ctx.sync()
             torch.cuda.synchronize()
             s1 = ctx.stats()
@@ -128,30 +131,27 @@ def main(n, out_path):
             out[name]["per_kernel"] = [{"kind": kinds[m], "user": users[m], "arrive_us": (int(st[m]) - z) / 1e3,
                                         "start_us": (first.get(kid, z) - z) / 1e3, "done_us": (done[kid] - z) / 1e3}
                                        for m, kid in enumerate(ids)]
-        # --- sequential FIFO and plain multi-stream (4 streams), same arrival process
+        # --- sequential FIFO and plain multi-stream (4 streams): each launch gated on its arrival
+        # flag (kl_wait_flag), completion stamped on the device after it
         for name, nstreams in (("sequential", 1), ("multistream4", 4)):
             streams = [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
+            flags, stamps = clock()
+            dstamp = torch.zeros(n, dtype=torch.int64, device=dev)
             torch.cuda.synchronize()
-            a_ev, d_ev = [], []
-            for i in range(n):
-                ctx.delay(arr_stream, int(gaps[i]), None)
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(arr_stream)
-                a_ev.append(ev)
             for m, x in enumerate(insts):
                 s = streams[m % nstreams]
-                s.wait_event(a_ev[m])
+                ctx.wait_flag(s, flags.data_ptr() + 4 * m, None)
                 ctx.run_plain(x.kind, x.grid, x.args, s)
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(s)
-                d_ev.append(ev)
+                ctx.wait_flag(s, None, dstamp.data_ptr() + 8 * m)
+            ctx.arrival_clock(arr_stream, gaps_d.data_ptr(), stamps.data_ptr(), flags.data_ptr(), n)
             torch.cuda.synchronize()
-            resp = [a.elapsed_time(d) for a, d in zip(a_ev, d_ev)]
-            last = max(a_ev[0].elapsed_time(d) for d in d_ev)
-            out[name] = summarise(resp, users, kinds, solo, 0.0, last, n)
+            st = stamps.cpu().numpy()
+            dn = dstamp.cpu().numpy()
+            resp = [(int(dn[m]) - int(st[m])) / 1e6 for m in range(n)]
+            out[name] = summarise(resp, users, kinds, solo, st[0] / 1e6, dn.max() / 1e6, n)
         res["loads"][str(rho)] = out
-        print(rho, {m: {f: round(v[f], 3) for f in ("kernels_per_s", "resp_mean_ms", "resp_p95_ms",
-                                                     "slowdown_mean", "jain_users")} for m, v in out.items()},
+        print(rho, {m: {f: round(float(v[f]), 3) for f in ("kernels_per_s", "resp_mean_ms", "resp_p95_ms",
+                                                            "slowdown_mean", "jain_users")} for m, v in out.items()},
               flush=True)
     ctx.close()
     json.dump(res, open(out_path, "w"), indent=1)
