@@ -58,6 +58,8 @@ def parse():
                     help="slice ratio per pair: 1 argmax CP over all co-schedules (FindCoSchedule l.3-4, "
                          "default), 0 argmin dT (Eq.8 balanced ratio)")
     ap.add_argument("--cp-min", type=float, default=None)
+    ap.add_argument("--alpha", type=float, nargs=2, default=None, metavar=("AP", "AM"),
+                    help="pruning thresholds alpha_p alpha_m (default: the profile JSON's, else the paper's 0.4 0.1)")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
@@ -249,6 +251,8 @@ def run_kernelet(args, rank, world, local_rank):
     lane_b = torch.cuda.Stream(device=dev)
     cfg = dict(kcfg)
     cfg["split_rule"] = args.split_rule
+    if args.alpha:
+        cfg["alpha_p"], cfg["alpha_m"] = args.alpha
     if args.cp_min is not None:
         cfg["cp_min"] = args.cp_min
     if args.opt:
