@@ -157,7 +157,9 @@ typedef struct {
     int32_t mc_seed;           /* != 0: MC(s) comparator: every decision picks a
                                   uniformly random pending kind pair and maximal slice ratio
                                   (no model); the seed selects the random stream */
-    int32_t pad0;
+    int32_t speculative;       /* 1 (default): while a cold-cache model batch runs, the oldest
+                                  pending kernel starts solo (nothing else in flight) and the
+                                  decision re-tunes or stops it (needs retune = 1) */
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
@@ -204,6 +206,7 @@ typedef struct {               /* runtime statistics since kl_create */
     int64_t retunes;           /* in-place occupancy changes of a running kernel (no stop) */
     int64_t topups;            /* top-up grids launched by re-tunes that raised the occupancy */
     int64_t aged;              /* decisions restricted by the starvation guard */
+    int64_t speculative;       /* speculative solo starts that hid a model batch */
 } kl_stats;
 typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;

@@ -112,7 +112,7 @@ class Config(C.Structure):
                 ("split_rule", C.c_int32), ("model_frozen", C.c_int32),
                 ("n_sms", C.c_int32), ("chunk", C.c_int32), ("audit", C.c_int32),
                 ("retune", C.c_int32), ("model_states", C.c_int32), ("granularity", C.c_int32),
-                ("age_limit_us", C.c_int32), ("mc_seed", C.c_int32), ("pad0", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
+                ("age_limit_us", C.c_int32), ("mc_seed", C.c_int32), ("speculative", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
                 ("profiles", C.POINTER(Profile)), ("stream_a", _vp), ("stream_b", _vp),
                 ("counters_dev", _vp)]
@@ -151,7 +151,7 @@ class Counters(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("decisions", "launches", "stops", "model_batches", "model_candidates",
-                                         "device_launches", "decide_ns", "model_ns", "retunes", "topups", "aged")]
+                                         "device_launches", "decide_ns", "model_ns", "retunes", "topups", "aged", "speculative")]
 
 
 class TraceRec(C.Structure):

@@ -359,6 +359,9 @@ const std::vector<std::pair<uint32_t, uint32_t>>& splits_of(kl_ctx* c, int k1, i
     return c->splits[k1][k2];
 }
 
+kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp);
+uint32_t slice_of(const kl_ctx* c, uint32_t b, int m);
+
 // The general model kernel (kl_model3.cu) serves three-state kinds and block granularity.
 bool general_model(const kl_ctx* c) {
     if (c->cfg.granularity == 1) return true;
@@ -388,7 +391,7 @@ int64_t scratch_doubles(const kl_ctx* c, const KlCand& cd) {
 }
 
 // Run the device model over cand_pinned[0..n); n_pairs > 0 fuses the selection.
-kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
+kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* spec = nullptr) {
     if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
     const auto t_model = std::chrono::steady_clock::now();
     fill_model_kinds(ctx);
@@ -419,6 +422,24 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out) {
                                 ctx->done_dev, ctx->dec_dev, ctx->ctrl);
     }
     if (rc) return ctx->fail(KL_ECUDA, "model batch launch: %s", cudaGetErrorString((cudaError_t)rc));
+    if (spec && !spec->inflight && !spec->drained) {
+        // speculative start: while the batch runs, the oldest pending kernel starts solo, capped
+        // so that every SM keeps room for a model CTA (persistent blocks would otherwise hold the
+        // SMs the model needs); the decision then re-tunes it in place or stops it
+        kl_profile model_cta{};
+        model_cta.wpb = 8;
+        model_cta.regs = 80;
+        model_cta.smem = 58 * 1024;
+        const kl_profile& p0 = ctx->prof[spec->kind];
+        uint32_t cap = 0;
+        for (uint32_t b = 1; b <= (uint32_t)std::max(1, p0.bmax); ++b)
+            if (fits(ctx, p0, b, &model_cta, 1) == 0) cap = b;
+        if (cap) {
+            kl_status st = launch_kernel(ctx, spec, cap, slice_of(ctx, cap, 1), -1, 0.0);
+            if (st) return st;
+            ctx->st.speculative++;
+        }
+    }
     KL_CUDA(cudaMemcpyAsync(ctx->pred_pinned, ctx->pred_dev, sizeof(kl_prediction) * n, cudaMemcpyDeviceToHost, ctx->ctrl));
     if (n_pairs > 0)
         KL_CUDA(cudaMemcpyAsync(ctx->dec_pinned, ctx->dec_dev, sizeof(KlDecision), cudaMemcpyDeviceToHost, ctx->ctrl));
@@ -562,7 +583,8 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
                 }
             }
         KlDecision dec{};
-        kl_status st = run_model(ctx, ne, np, &dec);
+        Inst* spec = (ctx->cfg.speculative && ctx->cfg.retune && ctx->inflight.empty()) ? R[0] : nullptr;
+        kl_status st = run_model(ctx, ne, np, &dec, spec);
         if (st) return st;
         best = dec.cand;
         bcp = dec.cp;
@@ -985,6 +1007,7 @@ kl_status kl_config_default(kl_config* c) {
     c->b0 = 0.0;
     c->n_sched = 4;            // B200: 4 SMSPs per SM -> W_v = 16
     c->retune = 1;
+    c->speculative = 1;
     return KL_OK;
 }
 
@@ -1051,7 +1074,11 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaHostAlloc(&ctx->stop_pinned, sizeof(unsigned long long) * kStopRing, cudaHostAllocDefault));
             std::memset(ctx->recs, 0, sizeof(KlLaunchRec) * kRecRing);
             for (int r = kRecRing - 1; r >= 0; --r) ctx->free_recs.push_back(r);
-            KL_CUDA(cudaStreamCreateWithFlags(&ctx->ctrl, cudaStreamNonBlocking));
+            {
+                int lo = 0, hi = 0;
+                KL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                KL_CUDA(cudaStreamCreateWithPriority(&ctx->ctrl, cudaStreamNonBlocking, hi));   // model first
+            }
             KL_CUDA(cudaEventCreateWithFlags(&ctx->init_ev, cudaEventDisableTiming));
             KL_CUDA(cudaEventCreateWithFlags(&ctx->tune_ev, cudaEventDisableTiming));
             KL_CUDA(cudaMalloc(&ctx->ctl_pool, sizeof(KlCtl) * kCtlPool));
