@@ -156,6 +156,7 @@ struct kl_ctx {
     uint32_t* init_pinned = nullptr;   // mapped (slot, len) pairs awaiting k_ctl_init (2 buffers)
     uint32_t* init_base = nullptr;
     int n_init = 0;
+    bool in_schedule = false;            // decide() called by the scheduler (may launch)
     uint32_t slot_gen[kCtlPool] = {};
     std::vector<std::unique_ptr<Inst>> insts;
     std::unordered_map<uint64_t, Inst*> by_id;
@@ -583,7 +584,8 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
                 }
             }
         KlDecision dec{};
-        Inst* spec = (ctx->cfg.speculative && ctx->cfg.retune && ctx->inflight.empty()) ? R[0] : nullptr;
+        Inst* spec = (ctx->in_schedule && ctx->cfg.speculative && ctx->cfg.retune && ctx->inflight.empty()) ? R[0]
+                                                                                                        : nullptr;
         kl_status st = run_model(ctx, ne, np, &dec, spec);
         if (st) return st;
         best = dec.cand;
@@ -947,7 +949,9 @@ kl_status schedule_step(kl_ctx* ctx, kl_coschedule* out) {
         }
     }
     Decision d;
+    ctx->in_schedule = true;
     st = decide(ctx, &d);
+    ctx->in_schedule = false;
     if (st) return st;
     ctx->desired = d;
     ctx->have_desired = true;
