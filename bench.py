@@ -122,11 +122,15 @@ def ncu_traffic(kind: str):
 
 
 def alu_peak(kind: str, sm_mhz: float, n_sm: int = 148) -> tuple[float, str]:
-    """ALU-pipe peaks from unit counts x clock (DESIGN.md §6): MUFU 16/clk/SM (sin, cos);
-    integer ALU pipe 64 lanes/clk/SM (IADD3/LOP3/SHF/VABSDIFF4)."""
+    """ALU peaks from unit counts x clock (B300_MICROARCH pipe rates): MUFU 16
+    ops/clk/SM (sin, cos); SAD's VABSDIFF4 on the alu pipe, 64 lanes/clk/SM (rt 2 per SMSP);
+    TEA's integer mix spreads over the alu pipe (IADD3/LOP3/SHF) and the fma pipe (IMAD), so its
+    ceiling is the issue rate, 128 lanes/clk/SM."""
     f = sm_mhz * 1e6
     if kind == "MRIQ":
         return 16 * n_sm * f, "MUFU ops/s (16/clk/SM)"
+    if kind == "TEA":
+        return 128 * n_sm * f, "int ops/s (alu+fma pipes, issue 128/clk/SM)"
     return 64 * n_sm * f, "int ALU ops/s (64/clk/SM)"
 
 
