@@ -72,7 +72,7 @@ typedef struct {   /* SPMV: CSR, one warp per row, 8 rows per block             
     float* y;
     int32_t n_rows;
 } kl_args_spmv;
-typedef struct {   /* ST: 7-point stencil, in[z][y][x]; block = 32x4 (x,y) tile x 64 z-points   */
+typedef struct {   /* ST: 7-point stencil, in[z][y][x]; block = 128x4 (x,y) tile x 32 z-points, nx % 4 == 0 */
     const float* in; float* out;
     int32_t nx, ny, nz;
     float c0, c1;          /* interior out = c1*(6 neighbours) - c0*in; boundary out = in */

@@ -74,7 +74,7 @@ THREADS = {"PC": 256, "SAD": 32, "SPMV": 256, "ST": 128, "MM": 256, "MRIQ": 256,
 SAD_MB = 16            # macroblock edge
 SAD_RANGE = 16         # search offsets in [-16, 16]
 SPMV_ROWS_PER_BLOCK = 8
-ST_TILE = (32, 4, 64)  # x, y, z points per block
+ST_TILE = (128, 4, 32)  # x, y, z points per block (32 threads x float4 in x, 4 rows)
 MM_TILE = (128, 256)   # output tile (M, N) per block
 BS_PER_BLOCK = 128 * 20
 TEA_PER_BLOCK = 128 * 10
