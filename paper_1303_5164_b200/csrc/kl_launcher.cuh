@@ -203,23 +203,23 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
         bool counted = true;   // this block still holds an sm_count slot
-        // Thread 0 runs a one-deep fetch pipeline: the atomicAdd for the next chunk is issued
-        // before the current chunk executes and resolved after it, so the fetch latency (one
-        // contended L2 atomic) hides behind the work.  A fetched chunk below the limit is always
-        // executed; a block leaving for a lowered cap stops issuing and drains what it holds.
-        unsigned long long pend_old = 0ull, pend_req = 0ull;
-        bool have_pend = false;
-        if (threadIdx.x == 0) {
-            pend_req = ctl->stop_req;
-            pend_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-            have_pend = true;
-        }
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
                 uint32_t vb = 0, end = 0;
-                if (have_pend) {
-                    unsigned long long old = pend_old;
-                    const unsigned long long req = pend_req;
+                // occupancy lowered by a re-tune: surplus blocks on this SM leave (no fetch)
+                const uint32_t cap = cap_now(L, ctl);
+                bool leave = false;
+                if (cap) {
+                    uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                    while (c > cap) {
+                        const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                        if (prev == c) { leave = true; counted = false; break; }
+                        c = prev;
+                    }
+                }
+                if (!leave) {
+                    const unsigned long long req = ctl->stop_req;
+                    unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
                     if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
                         // a host re-plan asked this epoch to stop: set the boundary (>= this fetch)
                         stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
@@ -234,25 +234,6 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                             L.rec->drained = 1u;
                             __threadfence_system();
                         }
-                    }
-                    have_pend = false;
-                }
-                if (vb < end) {
-                    // occupancy lowered by a re-tune: surplus blocks on this SM stop fetching
-                    const uint32_t cap = cap_now(L, ctl);
-                    bool leave = false;
-                    if (cap) {
-                        uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
-                        while (c > cap) {
-                            const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
-                            if (prev == c) { leave = true; counted = false; break; }
-                            c = prev;
-                        }
-                    }
-                    if (!leave) {
-                        pend_req = ctl->stop_req;
-                        pend_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-                        have_pend = true;
                     }
                 }
                 s_vb[it & 1] = vb;
