@@ -13,8 +13,10 @@ import kl_inputs as G  # noqa: E402
 import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
 
-ctx = K.Context(device=0)
-for kind in ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA"]:
+CHUNK = int(os.environ.get("CHUNK", "0"))
+KINDS = os.environ.get("KINDS", "PC,SAD,SPMV,ST,MM,MRIQ,BS,TEA").split(",")
+ctx = K.Context(device=0, chunk=CHUNK)
+for kind in KINDS:
     i = Instance(G.gen(kind, "paper"), "cuda")
     res = {}
     for mode in ("plain", "persistent"):
