@@ -1360,9 +1360,9 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     KL_CUDA(cudaEventCreate(&e1));
     int si = pick_stream(ctx);
     KL_CUDA(cudaEventRecord(e0, ctx->pool[si]));
-    ctx->pool_busy[si] += 1000;            // keep launch_kernel on the same stream
+    ctx->pool_busy[si] -= 1000;            // launch_kernel picks the least busy stream: this one
     st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0);
-    ctx->pool_busy[si] -= 1000;
+    ctx->pool_busy[si] += 1000;
     if (st) return st;
     KL_CUDA(cudaEventRecord(e1, ctx->pool[k->inflight->stream]));
     KL_CUDA(cudaEventSynchronize(e1));
