@@ -138,20 +138,18 @@ __device__ void leave_epoch(KlCtl* ctl) {
 // Join the grid's epoch (false: closed, another epoch, or a recycled slot -> exit untouched).
 __device__ bool join_epoch(const KlLaunch& L) {
     KlCtl* ctl = L.ctl;
-    const unsigned long long j0 = *(volatile unsigned long long*)&ctl->join;
-    if (kl_j_closed(j0) || kl_j_ticket(j0) != L.ticket) return false;   // late block: no atomics
+    // one round trip: a late block (slack of a closed epoch, recycled slot) undoes its stray join
     const unsigned long long j = atomicAdd(&ctl->join, 1ull);
     if (kl_j_closed(j) || kl_j_ticket(j) != L.ticket) {
-        // raced with a close/reopen: undo the stray count (and close if it was the last)
         leave_epoch(ctl);
         return false;
     }
+    // the finalizing block reads these after the epoch's last leave (fenced there)
     KlFin* f = &ctl->fin;
-    if (f->rec != L.rec) f->rec = L.rec;
-    if (f->counters != L.counters) f->counters = L.counters;
-    if (f->tag != L.tag) f->tag = L.tag;
-    if (f->n_sms != L.n_sms) f->n_sms = L.n_sms;
-    __threadfence();
+    f->rec = L.rec;
+    f->counters = L.counters;
+    f->tag = L.tag;
+    f->n_sms = L.n_sms;
     return true;
 }
 
@@ -185,7 +183,9 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         if (joined) {
             sm = smid_u32();
             const uint32_t cap = cap_now(L, ctl);
-            const uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
+            uint32_t c = 0;
+            if (cap) c = atomicAdd(&ctl->sm_count[sm], 1u);
+            else atomicAdd(&ctl->sm_count[sm], 1u);   // no return value needed: fire and forget
             if (cap && c >= cap) {
                 atomicSub(&ctl->sm_count[sm], 1u);
             } else {
@@ -203,21 +203,13 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
         bool counted = true;   // this block still holds an sm_count slot
+        bool leaving = false;  // thread 0: a lowered cap asked this block to leave
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
                 uint32_t vb = 0, end = 0;
-                // occupancy lowered by a re-tune: surplus blocks on this SM leave (no fetch)
-                const uint32_t cap = cap_now(L, ctl);
-                bool leave = false;
-                if (cap) {
-                    uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
-                    while (c > cap) {
-                        const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
-                        if (prev == c) { leave = true; counted = false; break; }
-                        c = prev;
-                    }
-                }
-                if (!leave) {
+                if (!leaving) {
+                    // one round trip: the control reads and the fetch are issued back to back
+                    const unsigned long long tw = ctl->tune;
                     const unsigned long long req = ctl->stop_req;
                     unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
                     if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
@@ -233,6 +225,18 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                         if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
                             L.rec->drained = 1u;
                             __threadfence_system();
+                        }
+                    }
+                    // occupancy lowered by a re-tune: surplus blocks on this SM leave after the
+                    // chunk they just fetched (the fetch is never given back)
+                    const uint32_t cap =
+                        ((tw & 1ull) && ((tw >> 1) & 0x7full) == (L.ticket & 0x7fu)) ? (uint32_t)(tw >> 32) : L.cap;
+                    if (cap && vb < end) {
+                        uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                        while (c > cap) {
+                            const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                            if (prev == c) { leaving = true; counted = false; break; }
+                            c = prev;
                         }
                     }
                 }
