@@ -77,6 +77,8 @@ struct KlCtl {
     volatile unsigned long long tune;
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
+    uint32_t sm_adm[KL_MAX_SMS];     // admissions per SM in the epoch (per-SM: no hot address)
+    unsigned long long sm_t0[KL_MAX_SMS];   // earliest admitted start per SM in the epoch
 };
 
 // Host-mapped (pinned) record of one launch: `drained` is raised by the first block that finds

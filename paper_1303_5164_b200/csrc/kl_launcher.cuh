@@ -70,13 +70,21 @@ __device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
     // over-fetched ids (>= limit) are discarded
     const uint32_t lim = min(word_limit(w, len), kl_w_next(w));
     const uint32_t executed = atomicExch(&ctl->executed, 0u);
-    const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
-    uint32_t mx = 0;
+    uint32_t mx = 0, admitted = 0;
+    unsigned long long t0 = ~0ull;
+    // every member has left (late blocks fail to join and never touch these): plain L2 reads
+    // and resets, pipelined across SMs
     for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
-        mx = max(mx, ctl->sm_hwm[s]);
-        ctl->sm_hwm[s] = 0;
+        mx = max(mx, __ldcg(&ctl->sm_hwm[s]));
+        admitted += __ldcg(&ctl->sm_adm[s]);
+        t0 = min(t0, __ldcg(&ctl->sm_t0[s]));
     }
-    const unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
+    for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
+        __stcg(&ctl->sm_hwm[s], 0u);
+        __stcg(&ctl->sm_adm[s], 0u);
+        __stcg(&ctl->sm_t0[s], ~0ull);
+    }
+    __threadfence();
     const unsigned long long t1 = gtimer();
     const uint32_t start = ctl->base;
     ctl->base = lim;
@@ -144,12 +152,15 @@ __device__ bool join_epoch(const KlLaunch& L) {
         leave_epoch(ctl);
         return false;
     }
-    // the finalizing block reads these after the epoch's last leave (fenced there)
-    KlFin* f = &ctl->fin;
-    f->rec = L.rec;
-    f->counters = L.counters;
-    f->tag = L.tag;
-    f->n_sms = L.n_sms;
+    // the epoch's first member records what the finalizing block needs (every grid of an epoch
+    // carries the same values; read after the epoch's last leave, which is fenced)
+    if (kl_j_count(j) == 0) {
+        KlFin* f = &ctl->fin;
+        f->rec = L.rec;
+        f->counters = L.counters;
+        f->tag = L.tag;
+        f->n_sms = L.n_sms;
+    }
     return true;
 }
 
@@ -190,9 +201,9 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                 atomicSub(&ctl->sm_count[sm], 1u);
             } else {
                 adm = 1;
-                atomicMax(&ctl->sm_hwm[sm], c + 1);
-                atomicAdd(&ctl->admitted, 1u);
-                atomicMin(&ctl->t0, gtimer());
+                if (cap) atomicMax(&ctl->sm_hwm[sm], c + 1);
+                atomicAdd(&ctl->sm_adm[sm], 1u);
+                atomicMin(&ctl->sm_t0[sm], gtimer());
             }
         }
         s_adm = adm;
