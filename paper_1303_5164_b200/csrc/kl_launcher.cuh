@@ -215,14 +215,27 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         uint32_t nexec = 0;
         bool counted = true;   // this block still holds an sm_count slot
         bool leaving = false;  // thread 0: a lowered cap asked this block to leave
+        // Thread 0's fetch = the control reads and the atomic, issued back to back (one round
+        // trip).  Far from the end of the range it is issued one chunk ahead, so its latency
+        // hides behind the current chunk; near the end (or when leaving) it is issued on demand,
+        // so no block holds a second chunk while others run dry (a fetched chunk below the limit
+        // is always executed, never given back).
+        bool have_pend = false;
+        unsigned long long p_old = 0ull, p_req = 0ull, p_tw = 0ull;
+        const uint32_t ahead = 2u * gridDim.x * L.chunk;
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
                 uint32_t vb = 0, end = 0;
-                if (!leaving) {
-                    // one round trip: the control reads and the fetch are issued back to back
-                    const unsigned long long tw = ctl->tune;
-                    const unsigned long long req = ctl->stop_req;
-                    unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                if (!have_pend && !leaving) {
+                    p_tw = ctl->tune;
+                    p_req = ctl->stop_req;
+                    p_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                    have_pend = true;
+                }
+                if (have_pend) {
+                    have_pend = false;
+                    unsigned long long old = p_old;
+                    const unsigned long long req = p_req, tw = p_tw;
                     if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
                         // a host re-plan asked this epoch to stop: set the boundary (>= this fetch)
                         stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
@@ -239,7 +252,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                         }
                     }
                     // occupancy lowered by a re-tune: surplus blocks on this SM leave after the
-                    // chunk they just fetched (the fetch is never given back)
+                    // chunk they hold
                     const uint32_t cap =
                         ((tw & 1ull) && ((tw >> 1) & 0x7full) == (L.ticket & 0x7fu)) ? (uint32_t)(tw >> 32) : L.cap;
                     if (cap && vb < end) {
@@ -249,6 +262,12 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                             if (prev == c) { leaving = true; counted = false; break; }
                             c = prev;
                         }
+                    }
+                    if (vb < end && !leaving && len > end && len - end > ahead) {
+                        p_tw = ctl->tune;
+                        p_req = ctl->stop_req;
+                        p_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                        have_pend = true;
                     }
                 }
                 s_vb[it & 1] = vb;
