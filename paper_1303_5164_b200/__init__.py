@@ -19,7 +19,7 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "libkl.so")
+LIB_PATH = os.environ.get("KL_LIB_PATH") or os.path.join(_HERE, "libkl.so")   # override: A/B builds
 SOURCES = ["csrc/kl_runtime.cpp", "csrc/kl_kernels.cu", "csrc/kl_model.cu", "csrc/kl_model3.cu", "csrc/kl_mm.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-shared", "-cudart", "static"]
