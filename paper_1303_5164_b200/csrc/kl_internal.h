@@ -59,30 +59,24 @@ struct KlFin {             // what the finalizing block needs, written by every 
 };
 
 struct KlCtl {
-    // 128-B lines by access pattern: the fetch word alone (an atomic per fetch); the host control
-    // words (read per fetch, written by the copy engine); membership and the epoch record
-    // (atomics at block start / end only); the per-SM arrays.
-    alignas(128) unsigned long long word;
+    unsigned long long word;
+    unsigned long long join;   // membership word (kl_j_*)
+    KlFin fin;
+    uint32_t len;
+    uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
+    uint32_t admitted;    // admitted blocks of the current launch
+    uint32_t executed;    // virtual blocks executed in the current launch
+    uint32_t base;        // first virtual block of the current launch (slice boundaries)
+    unsigned long long t0;  // earliest admitted-block start (globaltimer ns), current launch
     // host stop request, written by the copy engine (no SM needed): bit 0 valid, bits [1,8) epoch
     // of the launch to stop, bits [32,64) slice size; the next fetching block performs the stop
-    alignas(128) volatile unsigned long long stop_req;
+    volatile unsigned long long stop_req;
     // host occupancy re-tune, written by the copy engine: bit 0 valid, bits [1,8) epoch, bits
     // [32,64) blocks per SM (0 = uncapped).  Blocks above the cap on their SM leave at their next
     // fetch; raising the cap is served by a top-up grid of the same epoch.
     volatile unsigned long long tune;
-    uint32_t len;
-    uint32_t base;        // first virtual block of the current launch (slice boundaries)
-    alignas(128) unsigned long long join;   // membership word (kl_j_*)
-    KlFin fin;
-    uint32_t drained;     // 1 once a block found the range exhausted (kernel has no more blocks)
-    uint32_t admitted;    // (unused: per-SM sm_adm)
-    uint32_t executed;    // virtual blocks executed in the current launch
-    uint32_t pad;
-    unsigned long long t0;  // (unused: per-SM sm_t0)
-    alignas(128) uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
+    uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
-    uint32_t sm_adm[KL_MAX_SMS];     // admissions per SM in the epoch (per-SM: no hot address)
-    unsigned long long sm_t0[KL_MAX_SMS];   // earliest admitted start per SM in the epoch
 };
 
 // Host-mapped (pinned) record of one launch: `drained` is raised by the first block that finds

@@ -532,10 +532,6 @@ __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsig
         c->base = 0;
         c->t0 = ~0ull;
         c->stop_req = 0ull;
-        for (int s = 0; s < KL_MAX_SMS; ++s) {
-            c->sm_adm[s] = 0u;
-            c->sm_t0[s] = ~0ull;
-        }
     }
 }
 

@@ -70,21 +70,13 @@ __device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
     // over-fetched ids (>= limit) are discarded
     const uint32_t lim = min(word_limit(w, len), kl_w_next(w));
     const uint32_t executed = atomicExch(&ctl->executed, 0u);
-    uint32_t mx = 0, admitted = 0;
-    unsigned long long t0 = ~0ull;
-    // every member has left (late blocks fail to join and never touch these): plain L2 reads
-    // and resets, pipelined across SMs
+    const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
+    uint32_t mx = 0;
     for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
-        mx = max(mx, __ldcg(&ctl->sm_hwm[s]));
-        admitted += __ldcg(&ctl->sm_adm[s]);
-        t0 = min(t0, __ldcg(&ctl->sm_t0[s]));
+        mx = max(mx, ctl->sm_hwm[s]);
+        ctl->sm_hwm[s] = 0;
     }
-    for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
-        __stcg(&ctl->sm_hwm[s], 0u);
-        __stcg(&ctl->sm_adm[s], 0u);
-        __stcg(&ctl->sm_t0[s], ~0ull);
-    }
-    __threadfence();
+    const unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
     const unsigned long long t1 = gtimer();
     const uint32_t start = ctl->base;
     ctl->base = lim;
@@ -146,21 +138,20 @@ __device__ void leave_epoch(KlCtl* ctl) {
 // Join the grid's epoch (false: closed, another epoch, or a recycled slot -> exit untouched).
 __device__ bool join_epoch(const KlLaunch& L) {
     KlCtl* ctl = L.ctl;
-    // one round trip: a late block (slack of a closed epoch, recycled slot) undoes its stray join
+    const unsigned long long j0 = *(volatile unsigned long long*)&ctl->join;
+    if (kl_j_closed(j0) || kl_j_ticket(j0) != L.ticket) return false;   // late block: no atomics
     const unsigned long long j = atomicAdd(&ctl->join, 1ull);
     if (kl_j_closed(j) || kl_j_ticket(j) != L.ticket) {
+        // raced with a close/reopen: undo the stray count (and close if it was the last)
         leave_epoch(ctl);
         return false;
     }
-    // the epoch's first member records what the finalizing block needs (every grid of an epoch
-    // carries the same values; read after the epoch's last leave, which is fenced)
-    if (kl_j_count(j) == 0) {
-        KlFin* f = &ctl->fin;
-        f->rec = L.rec;
-        f->counters = L.counters;
-        f->tag = L.tag;
-        f->n_sms = L.n_sms;
-    }
+    KlFin* f = &ctl->fin;
+    if (f->rec != L.rec) f->rec = L.rec;
+    if (f->counters != L.counters) f->counters = L.counters;
+    if (f->tag != L.tag) f->tag = L.tag;
+    if (f->n_sms != L.n_sms) f->n_sms = L.n_sms;
+    __threadfence();
     return true;
 }
 
@@ -194,16 +185,14 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         if (joined) {
             sm = smid_u32();
             const uint32_t cap = cap_now(L, ctl);
-            uint32_t c = 0;
-            if (cap) c = atomicAdd(&ctl->sm_count[sm], 1u);
-            else atomicAdd(&ctl->sm_count[sm], 1u);   // no return value needed: fire and forget
+            const uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
             if (cap && c >= cap) {
                 atomicSub(&ctl->sm_count[sm], 1u);
             } else {
                 adm = 1;
-                if (cap) atomicMax(&ctl->sm_hwm[sm], c + 1);
-                atomicAdd(&ctl->sm_adm[sm], 1u);
-                atomicMin(&ctl->sm_t0[sm], gtimer());
+                atomicMax(&ctl->sm_hwm[sm], c + 1);
+                atomicAdd(&ctl->admitted, 1u);
+                atomicMin(&ctl->t0, gtimer());
             }
         }
         s_adm = adm;
@@ -214,28 +203,23 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
         bool counted = true;   // this block still holds an sm_count slot
-        bool leaving = false;  // thread 0: a lowered cap asked this block to leave
-        // Thread 0's fetch = the control reads and the atomic, issued back to back (one round
-        // trip).  Far from the end of the range it is issued one chunk ahead, so its latency
-        // hides behind the current chunk; near the end (or when leaving) it is issued on demand,
-        // so no block holds a second chunk while others run dry (a fetched chunk below the limit
-        // is always executed, never given back).
-        bool have_pend = false;
-        unsigned long long p_old = 0ull, p_req = 0ull, p_tw = 0ull;
-        const uint32_t ahead = 2u * gridDim.x * L.chunk;
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0) {
                 uint32_t vb = 0, end = 0;
-                if (!have_pend && !leaving) {
-                    p_tw = ctl->tune;
-                    p_req = ctl->stop_req;
-                    p_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-                    have_pend = true;
+                // occupancy lowered by a re-tune: surplus blocks on this SM leave (no fetch)
+                const uint32_t cap = cap_now(L, ctl);
+                bool leave = false;
+                if (cap) {
+                    uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                    while (c > cap) {
+                        const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                        if (prev == c) { leave = true; counted = false; break; }
+                        c = prev;
+                    }
                 }
-                if (have_pend) {
-                    have_pend = false;
-                    unsigned long long old = p_old;
-                    const unsigned long long req = p_req, tw = p_tw;
+                if (!leave) {
+                    const unsigned long long req = ctl->stop_req;
+                    unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
                     if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
                         // a host re-plan asked this epoch to stop: set the boundary (>= this fetch)
                         stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
@@ -250,24 +234,6 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
                             L.rec->drained = 1u;
                             __threadfence_system();
                         }
-                    }
-                    // occupancy lowered by a re-tune: surplus blocks on this SM leave after the
-                    // chunk they hold
-                    const uint32_t cap =
-                        ((tw & 1ull) && ((tw >> 1) & 0x7full) == (L.ticket & 0x7fu)) ? (uint32_t)(tw >> 32) : L.cap;
-                    if (cap && vb < end) {
-                        uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
-                        while (c > cap) {
-                            const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
-                            if (prev == c) { leaving = true; counted = false; break; }
-                            c = prev;
-                        }
-                    }
-                    if (vb < end && !leaving && len > end && len - end > ahead) {
-                        p_tw = ctl->tune;
-                        p_req = ctl->stop_req;
-                        p_old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
-                        have_pend = true;
                     }
                 }
                 s_vb[it & 1] = vb;
