@@ -184,7 +184,8 @@ def run(out_path):
     L0_ns = t * 1e6 / 4096
     L0 = L0_ns * clock / 1e3
     B = hbm / 32.0 / (n_sm * 4) / (clock * 1e6)      # sectors / cycle / virtual SM
-    cfg = {"L0": L0, "B": B, "a0": 1.0, "b0": 0.0}
+    # pruning thresholds recalibrated for B200 by tools/pruning_study.py (f4): no pruning
+    cfg = {"L0": L0, "B": B, "a0": 1.0, "b0": 0.0, "alpha_p": 0.0, "alpha_m": 0.0}
     fit_effective(ctx, insts, profiles, measured, cfg, clock, n_sm)
     out = {"device": torch.cuda.get_device_name(0), "n_sm": n_sm, "clock_mhz_under_ncu": clock,
            "latency_ns": L0_ns, "config": cfg, "profiles": profiles, "measured": measured,
