@@ -9,6 +9,11 @@ if [ "${CALIB:-0}" = "1" ]; then
   grep -E " fit |wrote" gpurun_out/calib.log | cut -c1-160
   cp gpurun_out/kl_profile_b200.json profiles/kl_profile_b200.json
 fi
+if [ "${CALIB:-0}" = "1" ]; then
+  echo "== OPT pair table (measured co-runs)"; timeout 1200 python tools/opt_table.py gpurun_out/opt_table.json > gpurun_out/opt_table.log 2>&1
+  cp gpurun_out/opt_table.json profiles/r01_opt_table.json
+  python tools/pruning_study.py gpurun_out/pruning_b200.json | head -12
+fi
 echo "== bench c2"; timeout 900 python bench.py --json-out gpurun_out/bench_c2.json > gpurun_out/bench_c2.log 2>&1
 python - <<'PY'
 import json
@@ -33,4 +38,9 @@ done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_model_batch -c 1 -o gpurun_out/prof_MODEL python tools/model_bench.py 1 > gpurun_out/ncu_full_MODEL.log 2>&1
 python tools/model_bench.py 20 > gpurun_out/model_bench.json
 python tools/ncu_summary.py gpurun_out/ncu_summary.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
+echo "== MC(1000)"; timeout 900 python tools/mc_cdf.py 1000 gpurun_out/mc_cdf.json 2>&1 | tail -1 | cut -c1-400
+echo "== online"; timeout 900 python tools/online.py 320 gpurun_out/online.json 2>&1 | tail -3 | cut -c1-600
+echo "== f1 study"; timeout 600 python tools/model3_study.py gpurun_out/model3_study.json 2>&1 | tail -3
+echo "== model bench"; python tools/model_bench.py 20
+echo "== launcher overhead"; python tools/launcher_overhead.py > gpurun_out/launcher_overhead.txt 2>&1; cat gpurun_out/launcher_overhead.txt
 echo "== done"; ls gpurun_out
