@@ -12,7 +12,7 @@ fi
 if [ "${CALIB:-0}" = "1" ]; then
   echo "== OPT pair table (measured co-runs)"; timeout 1200 python tools/opt_table.py gpurun_out/opt_table.json > gpurun_out/opt_table.log 2>&1
   cp gpurun_out/opt_table.json profiles/r01_opt_table.json
-  python tools/pruning_study.py gpurun_out/pruning_b200.json | head -12
+  python tools/pruning_study.py gpurun_out/pruning_b200.json > gpurun_out/pruning_b200.log 2>&1
 fi
 echo "== bench c2"; timeout 900 python bench.py --json-out gpurun_out/bench_c2.json > gpurun_out/bench_c2.log 2>&1
 python - <<'PY'
