@@ -162,6 +162,7 @@ struct kl_ctx {
     std::unordered_map<uint64_t, Inst*> by_id;
     std::vector<Inst*> R;              // pending set, arrival order (Alg.1 l.1)
     std::vector<Inst*> arriving;       // submitted, waiting for their ready event (Alg.1 l.2)
+    std::vector<std::pair<void*, bool>> ev_seen;   // per-poll cache of ready-event queries
     uint64_t next_id = 1, seq = 0;
     // model batch buffers
     double* scratch_dev = nullptr;      // general model: per-candidate chains
@@ -827,21 +828,38 @@ void mark_drained(kl_ctx* ctx, Inst* k) {
 // through *progress whether anything happened at all.
 kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
     // arrivals (Alg.1 l.2-3; "the arrival of new kernels trigger the recalculation")
-    // only the oldest few are queried per poll: ready events of one copy stream complete in order
-    for (size_t i = 0; i < ctx->arriving.size() && i < 4;) {
-        Inst* k = ctx->arriving[i];
-        if (k->ready) {
-            cudaError_t e = cudaEventQuery((cudaEvent_t)k->ready);
-            if (e == cudaErrorNotReady) { ++i; continue; }
-            if (e != cudaSuccess)
-                return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id, cudaGetErrorString(e));
+    // every pending arrival is checked, each distinct ready event queried once per poll (the
+    // instances of a kind usually share their inputs' event); arrivals need not complete in
+    // submission order (e.g. copies ordered by kernel time per byte)
+    if (!ctx->arriving.empty()) {
+        std::vector<std::pair<void*, bool>>& seen = ctx->ev_seen;
+        seen.clear();
+        for (size_t i = 0; i < ctx->arriving.size();) {
+            Inst* k = ctx->arriving[i];
+            if (k->ready) {
+                int hit = -1;
+                for (size_t s = 0; s < seen.size(); ++s)
+                    if (seen[s].first == k->ready) { hit = (int)s; break; }
+                bool done;
+                if (hit >= 0) {
+                    done = seen[hit].second;
+                } else {
+                    cudaError_t e = cudaEventQuery((cudaEvent_t)k->ready);
+                    if (e != cudaSuccess && e != cudaErrorNotReady)
+                        return ctx->fail(KL_ECUDA, "ready event of kernel %llu: %s", (unsigned long long)k->id,
+                                         cudaGetErrorString(e));
+                    done = (e == cudaSuccess);
+                    seen.push_back({k->ready, done});
+                }
+                if (!done) { ++i; continue; }
+            }
+            if (k->ready_flag && *k->ready_flag == 0u) { ++i; continue; }
+            auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
+            k->t_join = now_ns();
+            ctx->R.insert(pos, k);
+            ctx->arriving.erase(ctx->arriving.begin() + i);
+            *replan = *progress = true;
         }
-        if (k->ready_flag && *k->ready_flag == 0u) { ++i; continue; }
-        auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
-        k->t_join = now_ns();
-        ctx->R.insert(pos, k);
-        ctx->arriving.erase(ctx->arriving.begin() + i);
-        *replan = *progress = true;
     }
     for (size_t i = 0; i < ctx->inflight.size();) {
         Launch* L = ctx->inflight[i].get();
