@@ -207,6 +207,7 @@ typedef struct {               /* runtime statistics since kl_create */
     int64_t topups;            /* top-up grids launched by re-tunes that raised the occupancy */
     int64_t aged;              /* decisions restricted by the starvation guard */
     int64_t speculative;       /* speculative solo starts that hid a model batch */
+    int64_t memops;            /* control words written as stream memory operations */
 } kl_stats;
 typedef struct {               /* one launch of a kernel (trace / residency evidence) */
     uint64_t id;

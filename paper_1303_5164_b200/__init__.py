@@ -151,7 +151,7 @@ class Counters(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("decisions", "launches", "stops", "model_batches", "model_candidates",
-                                         "device_launches", "decide_ns", "model_ns", "retunes", "topups", "aged", "speculative")]
+                                         "device_launches", "decide_ns", "model_ns", "retunes", "topups", "aged", "speculative", "memops")]
 
 
 class TraceRec(C.Structure):

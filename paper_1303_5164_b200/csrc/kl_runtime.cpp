@@ -397,10 +397,7 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* 
     if (n > kMaxCand) return ctx->fail(KL_ENOMEM, "too many candidates (%d)", n);
     const auto t_model = std::chrono::steady_clock::now();
     fill_model_kinds(ctx);
-    KL_CUDA(cudaMemcpyAsync(ctx->mk_dev, ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaMemcpyHostToDevice, ctx->ctrl));
-    KL_CUDA(cudaMemcpyAsync(ctx->cand_dev, ctx->cand_pinned, sizeof(KlCand) * n, cudaMemcpyHostToDevice, ctx->ctrl));
-    if (n_pairs > 0)
-        KL_CUDA(cudaMemcpyAsync(ctx->off_dev, ctx->off_pinned, sizeof(int32_t) * (n_pairs + 1), cudaMemcpyHostToDevice, ctx->ctrl));
+    std::atomic_thread_fence(std::memory_order_seq_cst);   // mapped inputs written before the launch
     int rc;
     if (general_model(ctx)) {
         // f1 / block granularity: chains in global scratch, sized per candidate
@@ -416,7 +413,6 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* 
             KL_CUDA(cudaMalloc(&ctx->scratch_dev, sizeof(double) * (size_t)tot));
             ctx->scratch_cap = tot;
         }
-        KL_CUDA(cudaMemcpyAsync(ctx->soff_dev, ctx->soff_pinned, sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->ctrl));
         rc = kl_dev_model_general(ctx->mk_dev, model_cfg(ctx, n), ctx->cand_dev, ctx->pred_dev, n_pairs, ctx->off_dev,
                                   ctx->done_dev, ctx->dec_dev, ctx->scratch_dev, ctx->soff_dev, ctx->ctrl);
     } else {
@@ -442,9 +438,6 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* 
             ctx->st.speculative++;
         }
     }
-    KL_CUDA(cudaMemcpyAsync(ctx->pred_pinned, ctx->pred_dev, sizeof(kl_prediction) * n, cudaMemcpyDeviceToHost, ctx->ctrl));
-    if (n_pairs > 0)
-        KL_CUDA(cudaMemcpyAsync(ctx->dec_pinned, ctx->dec_dev, sizeof(KlDecision), cudaMemcpyDeviceToHost, ctx->ctrl));
     KL_CUDA(cudaStreamSynchronize(ctx->ctrl));
     ctx->model_batches++;
     ctx->model_cands += n;
@@ -726,6 +719,39 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     return KL_OK;
 }
 
+// Control-word writes (stop / re-tune) as stream memory operations (cuStreamWriteValue64: executed
+// by the GPU front end, needs neither an SM -- co-runners may fill every SM -- nor a copy engine --
+// a caller's bulk H2D copy would queue it for milliseconds); copy from a pinned slot if the driver
+// does not offer 64-bit stream memory operations.
+typedef int (*PfnWriteValue64)(void* stream, unsigned long long addr, unsigned long long value, unsigned int flags);
+
+PfnWriteValue64 write_value64() {
+    static PfnWriteValue64 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PfnWriteValue64>(p);
+    }
+    return fn;
+}
+
+kl_status write_ctl_word(kl_ctx* ctx, volatile unsigned long long* dst, unsigned long long v) {
+    if (PfnWriteValue64 fn = write_value64()) {
+        if (fn(ctx->stopper, (unsigned long long)(uintptr_t)dst, v, 0u) == 0) {
+            ctx->st.memops++;
+            return KL_OK;
+        }
+    }
+    unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
+    *slot = v;
+    KL_CUDA(cudaMemcpyAsync((void*)dst, slot, sizeof(*slot), cudaMemcpyHostToDevice, ctx->stopper));
+    return KL_OK;
+}
+
 // Re-plan that keeps a running kernel but changes its occupancy (slice ratio): the copy engine
 // writes the new cap into the control block; surplus blocks leave at their next fetch, and a raise
 // is served by a top-up grid joining the same epoch.  No drain, no relaunch.
@@ -733,10 +759,8 @@ kl_status retune(kl_ctx* ctx, Launch* L, uint32_t cap, int partner_kind, double 
     const KlKindInfo& inf = ctx->info[L->k->kind];
     const uint32_t bmax = (uint32_t)std::max(1, inf.bmax);
     const uint32_t old_eff = L->cap ? L->cap : bmax, new_eff = cap ? cap : bmax;
-    unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
-    *slot = kl_tune_req(L->epoch, cap);
-    KL_CUDA(cudaMemcpyAsync((void*)&ctx->ctl_pool[L->k->slot].tune, slot, sizeof(*slot), cudaMemcpyHostToDevice,
-                            ctx->stopper));
+    kl_status ws = write_ctl_word(ctx, &ctx->ctl_pool[L->k->slot].tune, kl_tune_req(L->epoch, cap));
+    if (ws) return ws;
     ctx->st.retunes++;
     L->cap = cap;
     if (L->cap_max && (cap == 0 || cap > L->cap_max)) L->cap_max = cap;
@@ -767,13 +791,11 @@ kl_status retune(kl_ctx* ctx, Launch* L, uint32_t cap, int partner_kind, double 
 // every SM); the next block that fetches work sets the boundary.
 kl_status request_stop(kl_ctx* ctx, Launch* L) {
     if (L->stop_requested) return KL_OK;
-    unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
     // stop at the next fetch (at least one chunk into the epoch): persistent blocks have no
     // per-slice launch cost, so waiting for the p% slice boundary would only delay the re-plan
     const uint32_t chunk = L->params.chunk ? L->params.chunk : 1u;
-    *slot = kl_stop_req(L->epoch, chunk);
-    KL_CUDA(cudaMemcpyAsync((void*)&ctx->ctl_pool[L->k->slot].stop_req, slot, sizeof(*slot), cudaMemcpyHostToDevice,
-                            ctx->stopper));
+    kl_status ws = write_ctl_word(ctx, &ctx->ctl_pool[L->k->slot].stop_req, kl_stop_req(L->epoch, chunk));
+    if (ws) return ws;
     L->stop_requested = true;
     ctx->st.stops++;
     return KL_OK;
@@ -1108,20 +1130,23 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaHostAlloc(&ctx->init_base, sizeof(uint32_t) * 6 * kCtlPool, cudaHostAllocMapped));
             ctx->init_pinned = ctx->init_base;
             for (auto& e : ctx->init_done) KL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocDefault));
-            KL_CUDA(cudaHostAlloc(&ctx->soff_pinned, sizeof(int64_t) * kMaxCand, cudaHostAllocDefault));
-            KL_CUDA(cudaMalloc(&ctx->soff_dev, sizeof(int64_t) * kMaxCand));
-            KL_CUDA(cudaMalloc(&ctx->mk_dev, sizeof(KlModelKind) * KL_NKINDS));
-            KL_CUDA(cudaHostAlloc(&ctx->cand_pinned, sizeof(KlCand) * kMaxCand, cudaHostAllocDefault));
-            KL_CUDA(cudaMalloc(&ctx->cand_dev, sizeof(KlCand) * kMaxCand));
-            KL_CUDA(cudaHostAlloc(&ctx->off_pinned, sizeof(int32_t) * (kMaxCand + 1), cudaHostAllocDefault));
-            KL_CUDA(cudaMalloc(&ctx->off_dev, sizeof(int32_t) * (kMaxCand + 1)));
-            KL_CUDA(cudaMalloc(&ctx->pred_dev, sizeof(kl_prediction) * kMaxCand));
-            KL_CUDA(cudaHostAlloc(&ctx->pred_pinned, sizeof(kl_prediction) * kMaxCand, cudaHostAllocDefault));
+            // model I/O in host-mapped memory: the batch reads its candidates and writes its
+            // predictions over PCIe directly (no copy-engine transfer that could queue behind a
+            // caller's bulk H2D copy)
+            KL_CUDA(cudaHostAlloc(&ctx->mk_pinned, sizeof(KlModelKind) * KL_NKINDS, cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->mk_dev, ctx->mk_pinned, 0));
+            KL_CUDA(cudaHostAlloc(&ctx->soff_pinned, sizeof(int64_t) * kMaxCand, cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->soff_dev, ctx->soff_pinned, 0));
+            KL_CUDA(cudaHostAlloc(&ctx->cand_pinned, sizeof(KlCand) * kMaxCand, cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->cand_dev, ctx->cand_pinned, 0));
+            KL_CUDA(cudaHostAlloc(&ctx->off_pinned, sizeof(int32_t) * (kMaxCand + 1), cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->off_dev, ctx->off_pinned, 0));
+            KL_CUDA(cudaHostAlloc(&ctx->pred_pinned, sizeof(kl_prediction) * kMaxCand, cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->pred_dev, ctx->pred_pinned, 0));
             KL_CUDA(cudaMalloc(&ctx->done_dev, sizeof(uint32_t)));
             KL_CUDA(cudaMemset(ctx->done_dev, 0, sizeof(uint32_t)));
-            KL_CUDA(cudaMalloc(&ctx->dec_dev, sizeof(KlDecision)));
-            KL_CUDA(cudaHostAlloc(&ctx->dec_pinned, sizeof(KlDecision), cudaHostAllocDefault));
+            KL_CUDA(cudaHostAlloc(&ctx->dec_pinned, sizeof(KlDecision), cudaHostAllocMapped));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->dec_dev, ctx->dec_pinned, 0));
         }
     } else {
         ctx->cand_pinned = new KlCand[kMaxCand];
@@ -1155,18 +1180,12 @@ kl_status kl_destroy(kl_ctx* ctx) {
         cudaFreeHost(ctx->init_base);
         for (auto& e : ctx->init_done) if (e) cudaEventDestroy(e);
         cudaFreeHost(ctx->mk_pinned);
-        cudaFree(ctx->mk_dev);
         if (ctx->soff_pinned) cudaFreeHost(ctx->soff_pinned);
-        if (ctx->soff_dev) cudaFree(ctx->soff_dev);
         if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
         cudaFreeHost(ctx->cand_pinned);
-        cudaFree(ctx->cand_dev);
         cudaFreeHost(ctx->off_pinned);
-        cudaFree(ctx->off_dev);
-        cudaFree(ctx->pred_dev);
         cudaFreeHost(ctx->pred_pinned);
         cudaFree(ctx->done_dev);
-        cudaFree(ctx->dec_dev);
         cudaFreeHost(ctx->dec_pinned);
     } else {
         delete[] ctx->cand_pinned;

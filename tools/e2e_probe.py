@@ -52,3 +52,10 @@ for rep in range(3):
     for k in order:
         ts = [t for t in tr if K.KINDS[t.kind] == k and t.admitted]
         print(f"  {k:5s} kernels {(min(t.t0_ns for t in ts) - z) / 1e6:7.2f} .. {(max(t.t1_ns for t in ts) - z) / 1e6:7.2f} ms")
+    if rep == 2:
+        for t in sorted(tr, key=lambda t: t.t0_ns):
+            if not t.admitted:
+                continue
+            print(f"    {K.KINDS[t.kind]:5s} cap{t.cap:3d}/{t.cap_max:2d} g{t.grids} [{t.start:6d},{t.end:6d}) exh{t.exhausted} "
+                  f"{(t.t0_ns - z) / 1e6:7.2f}..{(t.t1_ns - z) / 1e6:7.2f} dec{t.phase} "
+                  f"{K.KINDS[t.partner_kind] if t.partner_kind >= 0 else None} cp{t.cp:.3f}")
