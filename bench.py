@@ -374,6 +374,7 @@ def run_kernelet(args, rank, world, local_rank):
         "timed_kernels": timed,
         "retunes_per_step": st.retunes / max(1, args.warmup + args.steps),
         "stops_per_step": st.stops / max(1, args.warmup + args.steps),
+        "memops_per_step": st.memops / max(1, args.warmup + args.steps),
         "host_decide_ms_per_step": st.decide_ns / 1e6 / max(1, args.warmup + args.steps),
         "model_ms_per_step": st.model_ns / 1e6 / max(1, args.warmup + args.steps),
     }
