@@ -713,6 +713,7 @@ def main():
                 "speedup_vs_multistream": res["value"] / world / ms4 if ms4 else None,
                 "baselines": bl, "roofline_all": roof_all, "device_ms_per_step": res["device_ms_per_step"],
                 "phases_per_step": res["phases_per_step"], "parity": res["parity"],
+                "engine_per_step": {k: res.get(k) for k in ("retunes_per_step", "stops_per_step", "memops_per_step")},
                 "lease_conflicts": res["lease_conflicts"], "host_decide_ms_per_step": res["host_decide_ms_per_step"],
                 "model_ms_per_step": res["model_ms_per_step"],
                 "schedule_first_step": res["schedule_first_step"]}

@@ -730,6 +730,7 @@ PfnWriteValue64 write_value64() {
     static bool tried = false;
     if (!tried) {
         tried = true;
+        if (std::getenv("KL_NO_MEMOPS")) return nullptr;   // A/B switch: copy-engine writes
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q{};
         if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess &&
