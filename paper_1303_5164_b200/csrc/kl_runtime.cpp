@@ -742,10 +742,14 @@ PfnWriteValue64 write_value64() {
 
 kl_status write_ctl_word(kl_ctx* ctx, volatile unsigned long long* dst, unsigned long long v) {
     if (PfnWriteValue64 fn = write_value64()) {
-        if (fn(ctx->stopper, (unsigned long long)(uintptr_t)dst, v, 0u) == 0) {
+        const int rc = fn(ctx->stopper, (unsigned long long)(uintptr_t)dst, v, 0u);
+        if (rc == 0) {
             ctx->st.memops++;
             return KL_OK;
         }
+        if (std::getenv("KL_DEBUG")) std::fprintf(stderr, "cuStreamWriteValue64 failed: %d\n", rc);
+    } else if (std::getenv("KL_DEBUG")) {
+        std::fprintf(stderr, "cuStreamWriteValue64 entry point unavailable\n");
     }
     unsigned long long* slot = ctx->stop_pinned + (ctx->stop_slot++ % kStopRing);
     *slot = v;
