@@ -135,10 +135,13 @@ struct KlModelKind {       // per-kind model inputs, device table
     int32_t three;            // 1: three-state chain for this kind (f1)
     int32_t pad1;
 };
+struct KlCand;
 struct KlModelCfg {
     double L0, B, a0, b0;
     int32_t W, n_sched, latency_mode, n_cand;
     int32_t split_rule, pad;
+    kl_prediction* preds_host;   // host-mapped copy of the predictions (may be null)
+    KlCand* cands_dev;           // device copy of the candidates (the fused selection reads it)
 };
 struct KlCand {            // one candidate, and its grouping for the fused selection
     int32_t k1, k2;

@@ -254,10 +254,14 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
         }
     }
     out.status = status;
-    if (threadIdx.x == 0) preds[blockIdx.x] = out;
+    if (threadIdx.x == 0) {
+        preds[blockIdx.x] = out;
+        if (cfg.preds_host) cfg.preds_host[blockIdx.x] = out;   // the host reads these (mapped)
+        if (cfg.cands_dev) cfg.cands_dev[blockIdx.x] = cd;
+    }
     if (n_pairs <= 0) return;
 
-    select_last<kThreads>(cfg, kinds, cands, preds, n_pairs, pair_off, done_counter, dec);
+    select_last<kThreads>(cfg, kinds, cfg.cands_dev ? cfg.cands_dev : cands, preds, n_pairs, pair_off, done_counter, dec);
 }
 
 }  // namespace

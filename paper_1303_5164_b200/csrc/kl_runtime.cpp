@@ -177,6 +177,8 @@ struct kl_ctx {
     int32_t* off_dev = nullptr;
     kl_prediction* pred_dev = nullptr;
     kl_prediction* pred_pinned = nullptr;
+    kl_prediction* pred_host_dev = nullptr;   // device alias of pred_pinned (mapped)
+    KlCand* cand_scratch = nullptr;           // device copy of the candidates (selection)
     uint32_t* done_dev = nullptr;
     KlDecision* dec_dev = nullptr;
     KlDecision* dec_pinned = nullptr;
@@ -350,6 +352,8 @@ KlModelCfg model_cfg(const kl_ctx* c, int n) {
     m.latency_mode = c->cfg.latency_mode;
     m.n_cand = n;
     m.split_rule = c->cfg.split_rule;
+    m.preds_host = c->pred_host_dev;
+    m.cands_dev = c->cand_scratch;
     return m;
 }
 
@@ -1147,7 +1151,9 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaHostAlloc(&ctx->off_pinned, sizeof(int32_t) * (kMaxCand + 1), cudaHostAllocMapped));
             KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->off_dev, ctx->off_pinned, 0));
             KL_CUDA(cudaHostAlloc(&ctx->pred_pinned, sizeof(kl_prediction) * kMaxCand, cudaHostAllocMapped));
-            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->pred_dev, ctx->pred_pinned, 0));
+            KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->pred_host_dev, ctx->pred_pinned, 0));
+            KL_CUDA(cudaMalloc(&ctx->pred_dev, sizeof(kl_prediction) * kMaxCand));   // fused selection
+            KL_CUDA(cudaMalloc(&ctx->cand_scratch, sizeof(KlCand) * kMaxCand));
             KL_CUDA(cudaMalloc(&ctx->done_dev, sizeof(uint32_t)));
             KL_CUDA(cudaMemset(ctx->done_dev, 0, sizeof(uint32_t)));
             KL_CUDA(cudaHostAlloc(&ctx->dec_pinned, sizeof(KlDecision), cudaHostAllocMapped));
@@ -1186,6 +1192,8 @@ kl_status kl_destroy(kl_ctx* ctx) {
         for (auto& e : ctx->init_done) if (e) cudaEventDestroy(e);
         cudaFreeHost(ctx->mk_pinned);
         if (ctx->soff_pinned) cudaFreeHost(ctx->soff_pinned);
+        if (ctx->pred_dev) cudaFree(ctx->pred_dev);
+        if (ctx->cand_scratch) cudaFree(ctx->cand_scratch);
         if (ctx->scratch_dev) cudaFree(ctx->scratch_dev);
         cudaFreeHost(ctx->cand_pinned);
         cudaFreeHost(ctx->off_pinned);
