@@ -62,7 +62,7 @@ def parse():
                     help="pruning thresholds alpha_p alpha_m (default: the profile JSON's, else the paper's 0.4 0.1)")
     ap.add_argument("--age-limit-us", type=int, default=None,
                     help="starvation guard (kl_config.age_limit_us; default 0 = the paper's greedy)")
-    ap.add_argument("--no-speculative", action="store_true", help="disable the speculative start (kl_config.speculative)")
+    ap.add_argument("--speculative", action="store_true", help="enable the speculative start (kl_config.speculative)")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
@@ -260,8 +260,8 @@ def run_kernelet(args, rank, world, local_rank):
     cfg["split_rule"] = args.split_rule
     if args.alpha:
         cfg["alpha_p"], cfg["alpha_m"] = args.alpha
-    if args.no_speculative:
-        cfg["speculative"] = 0
+    if args.speculative:
+        cfg["speculative"] = 1
     if args.age_limit_us is not None:
         cfg["age_limit_us"] = args.age_limit_us
     if args.cp_min is not None:

@@ -157,9 +157,10 @@ typedef struct {
     int32_t mc_seed;           /* != 0: MC(s) comparator: every decision picks a
                                   uniformly random pending kind pair and maximal slice ratio
                                   (no model); the seed selects the random stream */
-    int32_t speculative;       /* 1 (default): while a cold-cache model batch runs, the oldest
-                                  pending kernel starts solo (nothing else in flight) and the
-                                  decision re-tunes or stops it (needs retune = 1) */
+    int32_t speculative;       /* 1: while a cold-cache model batch runs, the oldest pending
+                                  kernel starts solo (nothing else in flight) and the decision
+                                  re-tunes or stops it (needs retune = 1); 0 (default): measured
+                                  no gain on B200 (the batch then shares the SMs with it) */
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */

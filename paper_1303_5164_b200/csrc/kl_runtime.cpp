@@ -1060,7 +1060,7 @@ kl_status kl_config_default(kl_config* c) {
     c->b0 = 0.0;
     c->n_sched = 4;            // B200: 4 SMSPs per SM -> W_v = 16
     c->retune = 1;
-    c->speculative = 1;
+    c->speculative = 0;   // measured: no gain (the model batch then shares the SMs with the kernel)
     return KL_OK;
 }
 
