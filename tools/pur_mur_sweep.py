@@ -29,8 +29,8 @@ def ncu_solo(fmas):
             "from paper_1303_5164_b200.workload import Instance;ctx=K.Context(device=0);"
             f"i=Instance(G.gen('SYNTH',dict(n={N},fmas={fmas})),'cuda');"
             "ctx.run_plain('SYNTH',i.grid,i.args,0);ctx.run_plain('SYNTH',i.grid,i.args,0);torch.cuda.synchronize()")
-    out = subprocess.run(["ncu", "--metrics", "smsp__inst_executed.sum,sm__cycles_elapsed.avg,dram__bytes.sum,"
-                          "gpu__time_duration.sum", "-k", "regex:k_plain", "-s", "1", "-c", "1", "--csv",
+    out = subprocess.run(["ncu", "--metrics", "smsp__inst_executed.sum,sm__cycles_elapsed.avg,dram__bytes_read.sum,"
+                          "dram__bytes_write.sum,gpu__time_duration.sum", "-k", "regex:k_plain", "-s", "1", "-c", "1", "--csv",
                           sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT).stdout
     rows = list(csv.reader(io.StringIO("\n".join(l for l in out.splitlines() if l.startswith('"')))))
     h = rows[0]
@@ -57,7 +57,7 @@ def main(out_path):
     for c in FMAS:
         m = ncu_solo(c)
         pur = m["smsp__inst_executed.sum"] / (m["sm__cycles_elapsed.avg"] * 4 * n_sm)
-        mur = m["dram__bytes.sum"] / m["gpu__time_duration.sum"] / (peaks["hbm_gbs"] * 1e9)
+        mur = (m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]) / m["gpu__time_duration.sum"] / (peaks["hbm_gbs"] * 1e9)
         solo[c] = {"pur": pur, "mur": mur, "ncu": m}
         print("fmas", c, "PUR", round(pur, 3), "MUR", round(mur, 3), flush=True)
     ctx = K.Context(device=0)
