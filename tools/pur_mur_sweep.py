@@ -38,8 +38,9 @@ def ncu_solo(fmas):
     for r in rows[1:]:
         v = float(r[h.index("Metric Value")].replace(",", ""))
         unit = r[h.index("Metric Unit")]
-        mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-               "msecond": 1e-3}.get(unit, 1.0)
+        mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+               "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+               "second": 1.0, "s": 1.0}.get(unit, 1.0)
         m[r[h.index("Metric Name")]] = v * mul
     return m
 
@@ -82,7 +83,7 @@ def main(out_path):
     cp = np.array([p["cp"] for p in pairs])
     dp = np.array([p["dpur"] for p in pairs])
     dm = np.array([p["dmur"] for p in pairs])
-    res = {"fmas": FMAS, "n": N, "solo": {str(k): {"pur": v["pur"], "mur": v["mur"]} for k, v in solo.items()},
+    res = {"fmas": FMAS, "n": N, "solo": {str(k): v for k, v in solo.items()},
            "pairs": pairs, "pearson_cp_dpur": float(np.corrcoef(cp, dp)[0, 1]),
            "pearson_cp_dmur": float(np.corrcoef(cp, dm)[0, 1]), "how": __doc__.split("\n")[0]}
     print(json.dumps({k: res[k] for k in ("pearson_cp_dpur", "pearson_cp_dmur")}))
