@@ -143,7 +143,8 @@ typedef struct {
     int32_t model_frozen;      /* 1: decide from installed predictions only (OPT, kl_cache_put) */
     int32_t n_sms;             /* 0 = from the device */
     int32_t chunk;             /* virtual blocks per work fetch; 0 = per-kind default */
-    int32_t audit;             /* 1: count executions per virtual block (coverage audit) */
+    int32_t audit;             /* 1: count executions per virtual block (coverage audit);
+                                  2: also record each block's start and end time (kl_timeline) */
     int32_t retune;            /* 1 (default): a re-plan that keeps a running kernel at another
                                   occupancy re-tunes it in place; 0: stop and relaunch */
     int32_t model_states;      /* 2 (default): two-state warp model; 3: kinds with
@@ -277,6 +278,11 @@ kl_status kl_trace(kl_ctx* ctx, kl_trace_rec* out, size_t cap, size_t* n_out);
 /* Coverage audit (config.audit = 1): copy kernel `id`'s per-virtual-block execution counts
  * (uint32[grid_blocks], device-maintained) into host_out[0..n). */
 kl_status kl_audit(kl_ctx* ctx, uint64_t id, uint32_t* host_out, size_t n);
+/* Per-block start and end times (%globaltimer ns, pairs [2v, 2v+1]; 0 = never ran) of kernel
+ * `id`, config.audit = 2: the measurement tools' co-run windows (progress inside the window where
+ * both kernels are resident).  host_out: uint64[n], n >= 2 * grid_blocks.  Synchronises the
+ * device.  Errors: KL_ENOTFOUND, KL_EINVAL (audit != 2 or n too small). */
+kl_status kl_timeline(kl_ctx* ctx, uint64_t id, uint64_t* host_out, size_t n);
 /* FindCoSchedule decision only (no launch) for the current pending set; runs the device model
  * on a prediction-cache miss.  KL_EBUSY while a phase is in flight. */
 kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out);

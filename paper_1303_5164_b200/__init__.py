@@ -165,7 +165,7 @@ class TraceRec(C.Structure):
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",
                "kl_submit", "kl_slice", "kl_predict", "kl_schedule", "kl_sync", "kl_run_plain",
                "kl_get_profile", "kl_set_profile", "kl_reset_model_cache", "kl_reset_counters",
-               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch", "kl_delay", "kl_arrival_clock", "kl_wait_flag"]
+               "kl_trace", "kl_audit", "kl_decide", "kl_struct_sizes", "kl_stats_get", "kl_run_capped", "kl_run_pair", "kl_cache_put", "kl_submit_batch", "kl_delay", "kl_arrival_clock", "kl_wait_flag", "kl_timeline"]
 STRUCTS = ["Config", "Profile", "KernelDesc", "SlicePlan", "Candidate", "Prediction", "CoSchedule",
            "Counters", "TraceRec", "Stats", "ArgsPC", "ArgsSAD", "ArgsSPMV", "ArgsST", "ArgsMM", "ArgsMRIQ",
            "ArgsBS", "ArgsTEA", "ArgsMATADD", "ArgsSYNTH"]
@@ -207,6 +207,7 @@ def lib() -> C.CDLL:
     L.kl_delay.argtypes = [_vp, C.c_uint64, _vp]
     L.kl_arrival_clock.argtypes = [_vp, _vp, _vp, _vp, C.c_uint32]
     L.kl_wait_flag.argtypes = [_vp, _vp, _vp]
+    L.kl_timeline.argtypes = [_vp, C.c_uint64, _vp, C.c_size_t]
     L.kl_submit_batch.argtypes = [_vp, P(KernelDesc), C.c_size_t, P(C.c_uint64)]
     L.kl_cache_put.argtypes = [_vp, P(Candidate), P(Prediction), C.c_size_t]
     L.kl_run_pair.argtypes = [_vp, P(KernelDesc), C.c_uint32, P(KernelDesc), C.c_uint32, P(TraceRec)]
@@ -444,6 +445,14 @@ class Context:
         out = np.zeros(n, dtype=np.uint32)
         self._check(self._L.kl_audit(self._h, kid, out.ctypes.data_as(C.POINTER(C.c_uint32)), n))
         return out
+
+    def timeline(self, kid: int, grid: int):
+        """(start, end) per block, globaltimer ns (0 = never ran), of kernel `kid` (config audit=2):
+        an int64 array of shape (grid, 2)."""
+        import numpy as np
+        out = np.zeros(2 * grid, dtype=np.uint64)
+        self._check(self._L.kl_timeline(self._h, kid, out.ctypes.data, 2 * grid))
+        return out.astype(np.int64).reshape(grid, 2)
 
 
 def profile_dict(p: Profile) -> dict:

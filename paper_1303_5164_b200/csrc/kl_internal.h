@@ -100,6 +100,7 @@ struct KlLaunch {
     KlLaunchRec* rec;
     unsigned long long* counters;   // kl_counters on the device (may be null)
     uint32_t* audit;                // per-virtual-block execution counts (may be null)
+    unsigned long long* stamps;     // per-virtual-block end time, %globaltimer (may be null)
     unsigned long long tag;
 };
 

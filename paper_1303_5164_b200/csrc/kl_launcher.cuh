@@ -243,8 +243,10 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
             const uint32_t vb = s_vb[it & 1], end = s_end[it & 1];
             if (vb >= end) break;
             for (uint32_t v = vb; v < end; ++v) {
+                if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v] = gtimer();
                 Body::block(P, st, dsmem, v);
                 if (L.audit && threadIdx.x == 0) atomicAdd(L.audit + v, 1u);
+                if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v + 1] = gtimer();
             }
             nexec += end - vb;
         }

@@ -72,6 +72,7 @@ struct Inst {
     bool finished = false;      // drained and every launch retired
     Launch* inflight = nullptr; // at most one launch in flight per kernel
     uint32_t* audit = nullptr;
+    unsigned long long* stamps = nullptr;   // audit = 2: per-block end times (timeline)
     void* ready = nullptr;      // cudaEvent_t: the kernel arrives (joins R) once it completes
     const volatile uint32_t* ready_flag = nullptr;   // host-visible arrival word (non-zero = arrived)
     int64_t t_join = 0;         // host steady-clock ns when it joined R (starvation guard)
@@ -701,6 +702,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     P.rec = rec;
     P.counters = reinterpret_cast<unsigned long long*>(ctx->counters);
     P.audit = k->audit;
+    P.stamps = k->stamps;
     P.tag = k->tag;
     // grid: cap blocks per SM plus slack, so SMs whose slots free up late (the predecessor's tail
     // blocks) still receive their share; surplus blocks fail admission and exit at once
@@ -1183,7 +1185,10 @@ kl_status kl_destroy(kl_ctx* ctx) {
         if (ctx->stopper) cudaStreamDestroy(ctx->stopper);
         if (ctx->recs) cudaFreeHost(ctx->recs);
         if (ctx->stop_pinned) cudaFreeHost(ctx->stop_pinned);
-        for (auto& k : ctx->insts) if (k->audit) cudaFree(k->audit);
+        for (auto& k : ctx->insts) {
+            if (k->audit) cudaFree(k->audit);
+            if (k->stamps) cudaFree(k->stamps);
+        }
         if (ctx->ctrl) cudaStreamDestroy(ctx->ctrl);
         if (ctx->init_ev) cudaEventDestroy(ctx->init_ev);
         if (ctx->tune_ev) cudaEventDestroy(ctx->tune_ev);
@@ -1243,6 +1248,10 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
         if (ctx->cfg.audit) {
             KL_CUDA(cudaMalloc(&k->audit, sizeof(uint32_t) * d->grid_blocks));
             KL_CUDA(cudaMemset(k->audit, 0, sizeof(uint32_t) * d->grid_blocks));
+            if (ctx->cfg.audit == 2) {
+                KL_CUDA(cudaMalloc(&k->stamps, 2 * sizeof(unsigned long long) * d->grid_blocks));
+                KL_CUDA(cudaMemset(k->stamps, 0, 2 * sizeof(unsigned long long) * d->grid_blocks));
+            }
         }
     } else {
         std::memcpy(k->blob, d->args, d->args_bytes);
@@ -1536,6 +1545,18 @@ kl_status kl_trace(kl_ctx* ctx, kl_trace_rec* out, size_t cap, size_t* n_out) {
     size_t n = std::min(cap, ctx->trace.size());
     if (out && n) std::memcpy(out, ctx->trace.data(), n * sizeof(kl_trace_rec));
     if (n_out) *n_out = ctx->trace.size();
+    return KL_OK;
+}
+
+kl_status kl_timeline(kl_ctx* ctx, uint64_t id, uint64_t* host_out, size_t n) {
+    KL_LIVE(ctx);
+    auto it = ctx->by_id.find(id);
+    if (it == ctx->by_id.end()) return ctx->fail(KL_ENOTFOUND, "no kernel %llu", (unsigned long long)id);
+    Inst* k = it->second;
+    if (!k->stamps) return ctx->fail(KL_EINVAL, "timeline disabled (config.audit != 2)");
+    if (!host_out || n < 2 * (size_t)k->grid) return KL_EINVAL;
+    KL_CUDA(cudaDeviceSynchronize());
+    KL_CUDA(cudaMemcpy(host_out, k->stamps, 2 * sizeof(uint64_t) * k->grid, cudaMemcpyDeviceToHost));
     return KL_OK;
 }
 

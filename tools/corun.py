@@ -1,0 +1,48 @@
+"""Co-run measurement shared by the OPT table (f2) and the model-error study (C3): both kernels run
+concurrently through the slice launcher (kl_run_pair, each at its cap), every block's start and end
+are recorded on the device (config.audit = 2, kl_timeline), and each kernel's progress is counted
+inside the window where both are resident -- from the later first-block start to the earlier
+last-block end -- with blocks that straddle a window edge credited by the fraction of their
+duration inside it.  Progress rates are blocks per ns; the solo rate of a kind is measured the
+same way at its solo occupancy."""
+import numpy as np
+
+
+def progress(tl, t0, t1):
+    """Blocks of timeline tl (grid x 2: start, end) completed inside [t0, t1], edge blocks pro rata."""
+    s, e = tl[:, 0].astype(np.float64), tl[:, 1].astype(np.float64)
+    ran = e > 0
+    s, e = s[ran], e[ran]
+    ov = np.clip(np.minimum(e, t1) - np.maximum(s, t0), 0.0, None)
+    dur = np.maximum(e - s, 1.0)
+    return float((ov / dur).sum())
+
+
+def span(tl):
+    ran = tl[:, 1] > 0
+    return int(tl[ran, 0].min()), int(tl[ran, 1].max())
+
+
+def solo_rate(ctx, kind, inst, cap):
+    """Blocks per ns of `kind` alone at `cap` blocks per SM, from its own block timestamps (first
+    block start to last block end; no launch latency), second of two runs."""
+    rate = 0.0
+    for _ in range(2):
+        ctx.run_capped(kind, inst.grid, inst.args, cap)
+        tl = ctx.timeline(ctx.trace()[-1].id, inst.grid)
+        a, z = span(tl)
+        rate = inst.grid / max(z - a, 1)
+    return rate
+
+
+def corun(ctx, k1, i1, b1, k2, i2, b2):
+    """Co-run k1 (cap b1) with k2 (cap b2); returns (rate1, rate2, window_ns) in blocks/ns."""
+    r1, r2 = ctx.run_pair(k1, i1.grid, i1.args, b1, k2, i2.grid, i2.args, b2)
+    tl1, tl2 = ctx.timeline(r1.id, i1.grid), ctx.timeline(r2.id, i2.grid)
+    a1, z1 = span(tl1)
+    a2, z2 = span(tl2)
+    t0, t1 = max(a1, a2), min(z1, z2)
+    if t1 <= t0:
+        return 0.0, 0.0, 0
+    w = float(t1 - t0)
+    return progress(tl1, t0, t1) / w, progress(tl2, t0, t1) / w, int(w)

@@ -7,8 +7,9 @@ model picks by argmax CP (split_rule 1), the balanced ratio of Eq.8 (split_rule 
 even 1:1 warp split -- both kernels run concurrently through the slice launcher (kl_run_pair)
 until the first runs out of thread blocks.  Measured concurrent IPC per virtual SM:
     cIPC_k = I_k * blocks_executed_k / (window_k * f * 4 * n_SM)
-and measured CP = 1 - 1/(sum cIPC_k / IPC_k^solo) with the solo IPC measured at b_max
-(kl_run_capped).  Reports the paper's metric, the average absolute IPC error per virtual SM
+and measured CP = 1 - 1/(sum cIPC_k / IPC_k^solo) with the solo IPC measured at b_max; each kernel's
+progress is counted inside the window where both are resident (tools/corun.py, per-block device
+timestamps), so neither the ramp-up nor the survivor's solo tail enters the co-run rates.  Reports the paper's metric, the average absolute IPC error per virtual SM
 (0.08 on C2050), and the CP error.
 usage: python tools/model_error.py [out.json]"""
 import itertools
@@ -25,6 +26,7 @@ import bench  # noqa: E402
 import kl_inputs as G  # noqa: E402
 import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
+from tools.corun import corun, solo_rate  # noqa: E402
 
 KINDS = G.MIXES["ALL"]
 
@@ -42,7 +44,7 @@ def main(out_path):
     profiles, kcfg = bench.load_profiles(path)
     calib = json.load(open(path))
     clock = calib.get("clock_mhz_under_ncu", 1965.0) * 1e6
-    ctx = K.Context(device=0, profiles=profiles, **kcfg)
+    ctx = K.Context(device=0, profiles=profiles, audit=2, **kcfg)
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     smem_sm = torch.cuda.get_device_properties(0).shared_memory_per_multiprocessor
     insts = {k: Instance(G.gen(k, "paper"), "cuda") for k in KINDS}
@@ -50,15 +52,10 @@ def main(out_path):
     lv = {k: [b for b in range(1, prof[k].bmax + 1) if (b * prof[k].wpb) % 4 == 0] for k in KINDS}
     solo_b = {k: lv[k][-1] for k in KINDS}
 
-    def ipc_of(k, executed, t0, t1):
-        return prof[k].ipb * executed / ((t1 - t0) * 1e-9 * clock * 4 * n_sm)
+    def ipc_of(k, rate):       # blocks per ns -> warp instructions per cycle per virtual SM
+        return prof[k].ipb * rate * 1e9 / (clock * 4 * n_sm)
 
-    solo = {}
-    for k in KINDS:
-        i = insts[k]
-        ctx.run_capped(k, i.grid, i.args, solo_b[k])
-        ms = ctx.run_capped(k, i.grid, i.args, solo_b[k])
-        solo[k] = prof[k].ipb * i.grid / (ms * 1e-3 * clock * 4 * n_sm)
+    solo = {k: ipc_of(k, solo_rate(ctx, k, insts[k], solo_b[k])) for k in KINDS}
     cases = []
     for k1, k2 in itertools.combinations(KINDS, 2):
         p1, p2 = prof[k1], prof[k2]
@@ -75,14 +72,13 @@ def main(out_path):
                 "one_to_one": min(ok, key=lambda t: abs(t[0][0] * p1.wpb - t[0][1] * p2.wpb))[0]}
         for rule, (b1, b2) in pick.items():
             pr = dict(ok)[(b1, b2)]
-            ra, rb = ctx.run_pair(k1, insts[k1].grid, insts[k1].args, b1, k2, insts[k2].grid, insts[k2].args, b2)
-            c1 = ipc_of(k1, ra.executed, ra.t0_ns, ra.t1_ns)
-            c2 = ipc_of(k2, rb.executed, rb.t0_ns, rb.t1_ns)
+            q1, q2, wns = corun(ctx, k1, insts[k1], b1, k2, insts[k2], b2)
+            c1, c2 = ipc_of(k1, q1), ipc_of(k2, q2)
             cp_meas = 1.0 - 1.0 / (c1 / solo[k1] + c2 / solo[k2])
             cases.append({"k1": k1, "k2": k2, "b1": b1, "b2": b2, "rule": rule,
                           "pred": {"ipc1": pr.ipc1, "ipc2": pr.ipc2, "cp": pr.cp},
                           "meas": {"ipc1": c1, "ipc2": c2, "cp": cp_meas},
-                          "executed": [ra.executed, rb.executed], "ms": [(ra.t1_ns - ra.t0_ns) / 1e6, (rb.t1_ns - rb.t0_ns) / 1e6]})
+                          "window_ms": wns / 1e6})
             print(k1, k2, b1, b2, rule, "pred", round(pr.ipc1, 3), round(pr.ipc2, 3), round(pr.cp, 3),
                   "meas", round(c1, 3), round(c2, 3), round(cp_meas, 3), flush=True)
     e_ipc = [abs(c["pred"][f] - c["meas"][f]) for c in cases for f in ("ipc1", "ipc2")]

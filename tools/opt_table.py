@@ -4,7 +4,8 @@ ratios for all combinations to obtain the CP".  Every pair of ALL-mix kinds (sam
 included) at every maximal occupancy split is co-run on the B200 (kl_run_pair) and its measured
 concurrent IPCs, CP and Eq.8 dT become the 'prediction' table that `bench.py --opt` installs
 (kl_cache_put, model_frozen) so the same greedy Alg.1 decides from measurements instead of the
-Markov model.  usage: python tools/opt_table.py [out.json]"""
+Markov model.  Co-run progress is measured inside the window where both kernels are resident
+(tools/corun.py, per-block device timestamps).  usage: python tools/opt_table.py [out.json]"""
 import itertools
 import json
 import os
@@ -18,6 +19,7 @@ import bench  # noqa: E402
 import kl_inputs as G  # noqa: E402
 import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
+from tools.corun import corun, solo_rate  # noqa: E402
 from tools.model_error import fits  # noqa: E402
 
 KINDS = G.MIXES["ALL"]
@@ -27,7 +29,7 @@ def main(out_path):
     path = os.path.join(ROOT, "profiles", "kl_profile_b200.json")
     profiles, kcfg = bench.load_profiles(path)
     clock = json.load(open(path)).get("clock_mhz_under_ncu", 1965.0) * 1e6
-    ctx = K.Context(device=0, profiles=profiles, **kcfg)
+    ctx = K.Context(device=0, profiles=profiles, audit=2, **kcfg)
     props = torch.cuda.get_device_properties(0)
     n_sm, smem_sm = props.multi_processor_count, props.shared_memory_per_multiprocessor
     data = {k: G.gen(k, "paper") for k in KINDS}
@@ -36,13 +38,10 @@ def main(out_path):
     prof = {k: ctx.get_profile(k) for k in KINDS}
     lv = {k: [x for x in range(1, prof[k].bmax + 1) if (x * prof[k].wpb) % 4 == 0] for k in KINDS}
 
-    def ipc(k, executed, ns):
-        return prof[k].ipb * executed / (ns * 1e-9 * clock * 4 * n_sm)
+    def ipc(k, rate):          # blocks per ns -> warp instructions per cycle per virtual SM
+        return prof[k].ipb * rate * 1e9 / (clock * 4 * n_sm)
 
-    solo = {}
-    for k in KINDS:
-        ctx.run_capped(k, a[k].grid, a[k].args, lv[k][-1])
-        solo[k] = ipc(k, a[k].grid, ctx.run_capped(k, a[k].grid, a[k].args, lv[k][-1]) * 1e6)
+    solo = {k: ipc(k, solo_rate(ctx, k, a[k], lv[k][-1])) for k in KINDS}
     table = []
     for k1, k2 in itertools.combinations_with_replacement(KINDS, 2):
         p1, p2 = prof[k1], prof[k2]
@@ -50,9 +49,8 @@ def main(out_path):
         maxi = [(x, y) for x, y in feas if not any((u, v) != (x, y) and u >= x and v >= y for u, v in feas)]
         i1, i2 = a[k1], (b[k2] if k1 == k2 else a[k2])
         for b1, b2 in maxi:
-            r1, r2 = ctx.run_pair(k1, i1.grid, i1.args, b1, k2, i2.grid, i2.args, b2)
-            c1 = ipc(k1, r1.executed, r1.t1_ns - r1.t0_ns)
-            c2 = ipc(k2, r2.executed, r2.t1_ns - r2.t0_ns)
+            q1, q2, _ = corun(ctx, k1, i1, b1, k2, i2, b2)
+            c1, c2 = ipc(k1, q1), ipc(k2, q2)
             ok = c1 > 0 and c2 > 0
             cp = 1.0 - 1.0 / (c1 / solo[k1] + c2 / solo[k2]) if ok else 0.0
             dT = abs(p1.ipb * b1 / c1 - p2.ipb * b2 / c2) if ok else 0.0
@@ -60,7 +58,7 @@ def main(out_path):
                           "solo1": solo[k1], "solo2": solo[k2], "cp": cp, "dT": dT, "status": 0 if ok else 2})
         print(k1, k2, len(maxi), "splits; best measured CP",
               round(max([t["cp"] for t in table if t["k1"] == k1 and t["k2"] == k2] or [0]), 3), flush=True)
-    json.dump({"solo_ipc": solo, "table": table, "how": "tools/opt_table.py (kl_run_pair co-runs, paper size)"},
+    json.dump({"solo_ipc": solo, "table": table, "how": "tools/opt_table.py (kl_run_pair co-runs at paper size, progress inside the common window)"},
               open(out_path, "w"), indent=1)
 
 
