@@ -191,3 +191,22 @@ def test_arrival_clock_flags():
     for i in insts:
         compare(i.kind, i.result(), O.run_kernel(ds[i.kind]))
     ctx.close()
+
+
+def test_block_timeline():
+    """config.audit = 2 records every block's start and end on the device (kl_timeline): all blocks
+    ran once, start <= end, and the launch records bracket them."""
+    K.build()
+    ctx = K.Context(device=0, audit=2, alpha_p=0.0, alpha_m=0.0)
+    kinds = ["TEA", "PC", "BS", "ST"]
+    ds = {k: G.gen(k, "small") for k in kinds}
+    insts = [Instance(ds[k], "cuda") for k in kinds]
+    ids, c = _run_queue(ctx, insts)
+    tr = _check_trace(ctx, ids, insts)
+    for kid, inst in zip(ids, insts):
+        tl = ctx.timeline(kid, inst.grid)
+        assert np.all(tl[:, 0] > 0) and np.all(tl[:, 1] >= tl[:, 0])
+        recs = [t for t in tr if t.id == kid and t.admitted]
+        assert min(t.t0_ns for t in recs) <= tl[:, 0].min()
+        assert max(t.t1_ns for t in recs) >= tl[:, 1].max()
+    ctx.close()
