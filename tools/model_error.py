@@ -74,6 +74,9 @@ def main(out_path):
             pr = dict(ok)[(b1, b2)]
             q1, q2, wns = corun(ctx, k1, insts[k1], b1, k2, insts[k2], b2)
             c1, c2 = ipc_of(k1, q1), ipc_of(k2, q2)
+            if not (c1 > 0 and c2 > 0):     # the two never ran at the same time (no window)
+                print(k1, k2, b1, b2, rule, "no co-run window", flush=True)
+                continue
             cp_meas = 1.0 - 1.0 / (c1 / solo[k1] + c2 / solo[k2])
             cases.append({"k1": k1, "k2": k2, "b1": b1, "b2": b2, "rule": rule,
                           "pred": {"ipc1": pr.ipc1, "ipc2": pr.ipc2, "cp": pr.cp},
