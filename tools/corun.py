@@ -3,7 +3,8 @@ concurrently through the slice launcher (kl_run_pair, each at its cap), every bl
 are recorded on the device (config.audit = 2, kl_timeline), and each kernel's progress is counted
 inside the window where both are resident -- from the later first-block start to the earlier
 last-block end -- with blocks that straddle a window edge credited by the fraction of their
-duration inside it.  Progress rates are blocks per ns; the solo rate of a kind is measured the
+duration inside it; when that window covers less than half of the shorter run (a short kernel
+ending while its partner ramps up), each kernel's own run is used.  Progress rates are blocks per ns; the solo rate of a kind is measured the
 same way at its solo occupancy."""
 import numpy as np
 
@@ -35,14 +36,17 @@ def solo_rate(ctx, kind, inst, cap):
     return rate
 
 
-def corun(ctx, k1, i1, b1, k2, i2, b2):
-    """Co-run k1 (cap b1) with k2 (cap b2); returns (rate1, rate2, window_ns) in blocks/ns."""
+def corun(ctx, k1, i1, b1, k2, i2, b2, min_overlap=0.5):
+    """Co-run k1 (cap b1) with k2 (cap b2); returns (rate1, rate2, window_ns) in blocks/ns.
+    When the common window covers less than `min_overlap` of the shorter run (a short kernel that
+    ends while its partner still ramps up), each kernel's own run is used instead."""
     r1, r2 = ctx.run_pair(k1, i1.grid, i1.args, b1, k2, i2.grid, i2.args, b2)
     tl1, tl2 = ctx.timeline(r1.id, i1.grid), ctx.timeline(r2.id, i2.grid)
     a1, z1 = span(tl1)
     a2, z2 = span(tl2)
     t0, t1 = max(a1, a2), min(z1, z2)
-    if t1 <= t0:
-        return 0.0, 0.0, 0
-    w = float(t1 - t0)
-    return progress(tl1, t0, t1) / w, progress(tl2, t0, t1) / w, int(w)
+    if t1 - t0 >= min_overlap * min(z1 - a1, z2 - a2) and t1 > t0:
+        w = float(t1 - t0)
+        return progress(tl1, t0, t1) / w, progress(tl2, t0, t1) / w, int(w)
+    n1, n2 = float((tl1[:, 1] > 0).sum()), float((tl2[:, 1] > 0).sum())
+    return n1 / max(z1 - a1, 1), n2 / max(z2 - a2, 1), 0
