@@ -25,6 +25,8 @@ print("e2e", d["e2e"]["value"], "roofline", d["roofline"])
 PY
 echo "== bench c2 rule 0"; timeout 600 python bench.py --no-cpu --split-rule 0 --json-out gpurun_out/bench_c2_rule0.json > gpurun_out/bench_c2_rule0.log 2>&1
 python -c "import json;d=json.load(open('gpurun_out/bench_c2_rule0.json'));print(d['value'], d['ms_per_step'], d['speedup_vs_sequential'])"
+echo "== bench OPT"; timeout 600 python bench.py --no-cpu --no-baselines --opt profiles/r01_opt_table.json --json-out gpurun_out/bench_opt.json > gpurun_out/bench_opt.log 2>&1
+python -c "import json;d=json.load(open('gpurun_out/bench_opt.json'));print(d['value'], d['ms_per_step'], d['device_ms_per_step'])"
 echo "== bench c4"; timeout 900 python bench.py --workload c4 --steps 3 --warmup 1 --no-cpu --json-out gpurun_out/bench_c4.json > gpurun_out/bench_c4.log 2>&1
 python -c "import json;d=json.load(open('gpurun_out/bench_c4.json'));print(d['value'], d['ms_per_step'], d['speedup_vs_sequential'], d['lease_conflicts'])"
 echo "== model error"; timeout 900 python tools/model_error.py gpurun_out/model_error.json > gpurun_out/model_error.log 2>&1
