@@ -77,6 +77,9 @@ struct KlCtl {
     volatile unsigned long long tune;
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
+#ifdef KL_STRIPED_EXPERIMENT
+    uint32_t xs[16 * 32];            // experiment: 16 stripe counters, one 128-B line each
+#endif
 };
 
 // Host-mapped (pinned) record of one launch: `drained` is raised by the first block that finds
