@@ -77,6 +77,10 @@ struct KlCtl {
     volatile unsigned long long tune;
     uint32_t sm_count[KL_MAX_SMS];   // resident admitted blocks per SM (occupancy cap)
     uint32_t sm_hwm[KL_MAX_SMS];     // high-water mark per SM (residency evidence)
+    // per-SM epoch statistics (no hot address at block start / exit; summed at finalize)
+    uint32_t sm_adm[KL_MAX_SMS];             // admissions
+    uint32_t sm_exec[KL_MAX_SMS];            // virtual blocks executed
+    unsigned long long sm_t0[KL_MAX_SMS];    // earliest admitted start (0 = none)
 #ifdef KL_STRIPED_EXPERIMENT
     uint32_t xs[16 * 32];            // experiment: 16 stripe counters, one 128-B line each
 #endif

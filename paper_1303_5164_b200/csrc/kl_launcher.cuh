@@ -57,7 +57,72 @@ __device__ __forceinline__ uint32_t word_limit(unsigned long long w, uint32_t le
     return lim;
 }
 
-__device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
+struct EpochStats {
+    uint32_t mx, executed, admitted;
+    unsigned long long t0;
+};
+
+// Per-SM epoch statistics gathered and reset by one thread (rare path: a late block's undo closes
+// the epoch).  Every member has left, so plain L2 accesses suffice.
+__device__ EpochStats gather_stats_serial(KlCtl* ctl, uint32_t n_sms) {
+    EpochStats s{0u, 0u, 0u, ~0ull};
+    for (uint32_t i = 0; i < n_sms && i < KL_MAX_SMS; ++i) {
+        s.mx = max(s.mx, __ldcg(&ctl->sm_hwm[i]));
+        s.executed += __ldcg(&ctl->sm_exec[i]);
+        s.admitted += __ldcg(&ctl->sm_adm[i]);
+        const unsigned long long ts = __ldcg(&ctl->sm_t0[i]);
+        if (ts) s.t0 = min(s.t0, ts);
+        __stcg(&ctl->sm_hwm[i], 0u);
+        __stcg(&ctl->sm_exec[i], 0u);
+        __stcg(&ctl->sm_adm[i], 0u);
+        __stcg(&ctl->sm_t0[i], 0ull);
+    }
+    __threadfence();
+    return s;
+}
+
+// The same by the whole closing block (normal path): one SM entry per thread, block reduction;
+// the result is valid in thread 0.
+template <int kThreads>
+__device__ EpochStats gather_stats_block(KlCtl* ctl, uint32_t n_sms) {
+    __shared__ uint32_t r_mx[kThreads / 32], r_ex[kThreads / 32], r_ad[kThreads / 32];
+    __shared__ unsigned long long r_t0[kThreads / 32];
+    uint32_t mx = 0, ex = 0, ad = 0;
+    unsigned long long t0 = ~0ull;
+    for (uint32_t i = threadIdx.x; i < n_sms && i < KL_MAX_SMS; i += kThreads) {
+        mx = max(mx, __ldcg(&ctl->sm_hwm[i]));
+        ex += __ldcg(&ctl->sm_exec[i]);
+        ad += __ldcg(&ctl->sm_adm[i]);
+        const unsigned long long ts = __ldcg(&ctl->sm_t0[i]);
+        if (ts) t0 = min(t0, ts);
+        __stcg(&ctl->sm_hwm[i], 0u);
+        __stcg(&ctl->sm_exec[i], 0u);
+        __stcg(&ctl->sm_adm[i], 0u);
+        __stcg(&ctl->sm_t0[i], 0ull);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ex += __shfl_xor_sync(0xffffffffu, ex, o);
+        ad += __shfl_xor_sync(0xffffffffu, ad, o);
+        t0 = min(t0, __shfl_xor_sync(0xffffffffu, t0, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { r_mx[w] = mx; r_ex[w] = ex; r_ad[w] = ad; r_t0[w] = t0; }
+    __threadfence();
+    __syncthreads();
+    EpochStats s{0u, 0u, 0u, ~0ull};
+    if (threadIdx.x == 0)
+        for (int i = 0; i < kThreads / 32; ++i) {
+            s.mx = max(s.mx, r_mx[i]);
+            s.executed += r_ex[i];
+            s.admitted += r_ad[i];
+            s.t0 = min(s.t0, r_t0[i]);
+        }
+    return s;
+}
+
+__device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j, const EpochStats& S) {
     __threadfence();
     volatile KlFin* vf = &ctl->fin;
     KlFin F;
@@ -69,14 +134,8 @@ __device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
     // every id below min(next, limit) was handed out and executed by a block that has left;
     // over-fetched ids (>= limit) are discarded
     const uint32_t lim = min(word_limit(w, len), kl_w_next(w));
-    const uint32_t executed = atomicExch(&ctl->executed, 0u);
-    const uint32_t admitted = atomicExch(&ctl->admitted, 0u);
-    uint32_t mx = 0;
-    for (uint32_t s = 0; s < F.n_sms && s < KL_MAX_SMS; ++s) {
-        mx = max(mx, ctl->sm_hwm[s]);
-        ctl->sm_hwm[s] = 0;
-    }
-    const unsigned long long t0 = atomicExch(&ctl->t0, ~0ull);
+    const uint32_t mx = S.mx, executed = S.executed, admitted = S.admitted;
+    const unsigned long long t0 = S.t0;
     const unsigned long long t1 = gtimer();
     const uint32_t start = ctl->base;
     ctl->base = lim;
@@ -125,14 +184,24 @@ __device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j) {
 
 // Leave the epoch; the block that brings the count to zero closes and finalizes it once its range
 // is finished (exhausted, or stopped and drained to the boundary).
-__device__ void leave_epoch(KlCtl* ctl) {
+// Leave the epoch; true (and the membership word through *jout) if this block closed it -- the
+// caller then finalizes.
+__device__ bool leave_epoch_try(KlCtl* ctl, unsigned long long* jout) {
     __threadfence();
     const unsigned long long j = atomicAdd(&ctl->join, ~0ull) - 1ull;   // count - 1
-    if (kl_j_count(j) != 0 || kl_j_closed(j)) return;
+    if (kl_j_count(j) != 0 || kl_j_closed(j)) return false;
     const uint32_t len = ctl->len;
     const unsigned long long w = atomicAdd(&ctl->word, 0ull);
-    if (kl_w_next(w) < word_limit(w, len)) return;   // not finished: live blocks will come
-    if (atomicCAS(&ctl->join, j, j | KL_J_CLOSED) == j) finalize_epoch(ctl, len, j);
+    if (kl_w_next(w) < word_limit(w, len)) return false;   // not finished: live blocks will come
+    if (atomicCAS(&ctl->join, j, j | KL_J_CLOSED) != j) return false;
+    *jout = j;
+    return true;
+}
+
+// Single-thread leave (a late block undoing a stray join): finalizes serially if it closes.
+__device__ void leave_epoch(KlCtl* ctl) {
+    unsigned long long j;
+    if (leave_epoch_try(ctl, &j)) finalize_epoch(ctl, ctl->len, j, gather_stats_serial(ctl, ctl->fin.n_sms));
 }
 
 // Join the grid's epoch (false: closed, another epoch, or a recycled slot -> exit untouched).
@@ -191,8 +260,9 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
             } else {
                 adm = 1;
                 atomicMax(&ctl->sm_hwm[sm], c + 1);
-                atomicAdd(&ctl->admitted, 1u);
-                atomicMin(&ctl->t0, gtimer());
+                atomicAdd(&ctl->sm_adm[sm], 1u);
+                const unsigned long long now = gtimer();
+                if (atomicCAS(&ctl->sm_t0[sm], 0ull, now) != 0ull) atomicMin(&ctl->sm_t0[sm], now);
             }
         }
         s_adm = adm;
@@ -280,11 +350,24 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         }
         Body::fini(P, st, dsmem);
         if (threadIdx.x == 0) {
-            atomicAdd(&ctl->executed, nexec);
+            atomicAdd(&ctl->sm_exec[sm], nexec);
             if (counted) atomicSub(&ctl->sm_count[sm], 1u);
         }
     }
-    if (threadIdx.x == 0 && joined) leave_epoch(ctl);
+    // leave; the block whose leave closes the epoch finalizes it, gathering the per-SM statistics
+    // with all its threads
+    __shared__ int s_close;
+    __shared__ unsigned long long s_j;
+    if (threadIdx.x == 0) {
+        unsigned long long j = 0ull;
+        s_close = (joined && leave_epoch_try(ctl, &j)) ? 1 : 0;
+        s_j = j;
+    }
+    __syncthreads();
+    if (s_close) {
+        const EpochStats S = gather_stats_block<Body::kThreads>(ctl, L.n_sms);
+        if (threadIdx.x == 0) finalize_epoch(ctl, len, s_j, S);
+    }
 }
 
 // Plain grid: blockIdx rectified by the slice offset.
