@@ -81,9 +81,6 @@ struct KlCtl {
     uint32_t sm_adm[KL_MAX_SMS];             // admissions
     uint32_t sm_exec[KL_MAX_SMS];            // virtual blocks executed
     unsigned long long sm_t0[KL_MAX_SMS];    // earliest admitted start (0 = none)
-#ifdef KL_STRIPED_EXPERIMENT
-    uint32_t xs[16 * 32];            // experiment: 16 stripe counters, one 128-B line each
-#endif
 };
 
 // Host-mapped (pinned) record of one launch: `drained` is raised by the first block that finds

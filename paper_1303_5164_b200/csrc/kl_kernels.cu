@@ -532,9 +532,6 @@ __global__ void k_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsig
         c->base = 0;
         c->t0 = ~0ull;
         c->stop_req = 0ull;
-#ifdef KL_STRIPED_EXPERIMENT
-        for (int s = 0; s < 16; ++s) c->xs[s * 32] = 0u;
-#endif
     }
 }
 

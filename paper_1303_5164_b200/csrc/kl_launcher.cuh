@@ -273,35 +273,7 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
         bool counted = true;   // this block still holds an sm_count slot
-#ifdef KL_STRIPED_EXPERIMENT
-        // experiment (solo, uncapped, no stops): 16 stripes of the range, one counter each;
-        // a block starts on stripe (blockIdx % 16) and moves on when it is exhausted
-        uint32_t stripe = blockIdx.x % 16u, tried = 0;
-#endif
         for (uint32_t it = 0;; ++it) {
-#ifdef KL_STRIPED_EXPERIMENT
-            if (threadIdx.x == 0) {
-                uint32_t vb = 0, end = 0;
-                while (tried < 16) {
-                    const uint32_t lo = (uint32_t)((unsigned long long)len * stripe / 16u);
-                    const uint32_t hi = (uint32_t)((unsigned long long)len * (stripe + 1u) / 16u);
-                    const uint32_t o = atomicAdd(&ctl->xs[stripe * 32u], L.chunk);
-                    if (lo + o < hi) { vb = lo + o; end = min(vb + L.chunk, hi); break; }
-                    stripe = (stripe + 1u) % 16u;
-                    ++tried;
-                }
-                if (vb >= end) {   // all stripes exhausted: mark the range consumed for finalize
-                    atomicMax(&ctl->word, kl_w_make(len, 0u, kl_w_epoch(atomicAdd(&ctl->word, 0ull)), false));
-                    if (atomicCAS(&ctl->drained, 0u, 1u) == 0u && L.rec) {
-                        L.rec->drained = 1u;
-                        __threadfence_system();
-                    }
-                }
-                s_vb[it & 1] = vb;
-                s_end[it & 1] = end;
-            }
-            if (false)
-#endif
             if (threadIdx.x == 0) {
                 uint32_t vb = 0, end = 0;
                 // occupancy lowered by a re-tune: surplus blocks on this SM leave (no fetch)
