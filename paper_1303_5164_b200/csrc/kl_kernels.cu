@@ -221,49 +221,12 @@ struct BodyST {
 // with 2*pi folded into k at staging time, so the inner loop is 3 FMA for the phase, the two
 // MUFU ops (MUFU.SIN/COS reduce the argument themselves) and 2 FMA accumulates.  MUFU-bound:
 // 2 MUFU ops per (voxel, k) at 16 lanes/clk/SM.
-// sin and cos of 2 pi r on the FMA pipe (r in revolutions): quadrant q = rint(4r) by the
-// 1.5*2^23 rounding trick, f = r - q/4 in [-1/8, 1/8] (exact), Taylor polynomials of degree 9
-// (sin) and 8 (cos) in x = 2 pi f (|x| <= pi/4: truncation < 2e-9), quadrant rotation by swap
-// and sign flips.  fp32 emulation: max abs error 9e-8 for |r| <= 50 (MUFU: ~1e-6 at |t| ~ 300).
-__device__ __forceinline__ void sincos_2pi_poly(float r, float* s_out, float* c_out) {
-    const float magic = 12582912.0f;                       // 1.5 * 2^23
-    const float qm = fmaf(r, 4.0f, magic);
-    const float qf = qm - magic;
-    const int q = __float_as_int(qm);                      // low bits = rint(4r) mod 4
-    const float x = fmaf(qf, -0.25f, r) * 6.28318530717958648f;   // r - q/4 is exact
-    const float x2 = x * x;
-    float s = fmaf(x2, 2.75573192e-6f, -1.98412698e-4f);
-    s = fmaf(x2, s, 8.33333333e-3f);
-    s = fmaf(x2, s, -1.66666667e-1f);
-    s = x * fmaf(x2, s, 1.0f);
-    float c = fmaf(x2, 2.48015873e-5f, -1.38888889e-3f);
-    c = fmaf(x2, c, 4.16666667e-2f);
-    c = fmaf(x2, c, -0.5f);
-    c = fmaf(x2, c, 1.0f);
-    // (sin, cos)(x + q pi/2): q=1 -> (c, -s), q=2 -> (-s, -c), q=3 -> (-c, s)
-    const float sw_s = (q & 1) ? c : s, sw_c = (q & 1) ? s : c;
-    *s_out = __int_as_float(__float_as_int(sw_s) ^ ((q & 2) << 30));
-    *c_out = __int_as_float(__float_as_int(sw_c) ^ (((q + 1) & 2) << 30));
-}
-
 struct BodyMRIQ {
-    // One voxel per thread, k-points staged in shared memory (2 pi folded in).  Of every four
-    // k-points three take sin/cos from the MUFU pipe (__sincosf) and one from FMA-pipe polynomials
-    // (sincos_2pi_poly): the MUFU pipe was the bound (ncu XU 93 %, FMA 35 %), so the split moves
-    // a quarter of the transcendental work onto the idle pipe.
     using Params = kl_args_mriq;
     using State = Empty;
     static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
-    __device__ static void term(const float4 q, float x, float y, float z, bool poly, float& qr, float& qi) {
-        const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
-        float sn, cs;
-        if (poly) sincos_2pi_poly(t * 0.159154943091895336f, &sn, &cs);
-        else __sincosf(t, &sn, &cs);
-        qr = fmaf(q.w, cs, qr);
-        qi = fmaf(q.w, sn, qi);
-    }
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
         __shared__ float4 sk[256];   // (2 pi kx, 2 pi ky, 2 pi kz, phiMag)
         const int i = (int)vb * 256 + threadIdx.x;
@@ -281,15 +244,15 @@ struct BodyMRIQ {
                                               two_pi * __ldg(a.kz + k), __ldg(a.phimag + k));
             }
             __syncthreads();
-            int k = 0;
-#pragma unroll 2
-            for (; k + 4 <= n; k += 4) {
-                term(sk[k], x, y, z, false, qr, qi);
-                term(sk[k + 1], x, y, z, false, qr, qi);
-                term(sk[k + 2], x, y, z, false, qr, qi);
-                term(sk[k + 3], x, y, z, true, qr, qi);
+#pragma unroll 8
+            for (int k = 0; k < n; ++k) {
+                const float4 q = sk[k];
+                const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
+                float sn, cs;
+                __sincosf(t, &sn, &cs);
+                qr = fmaf(q.w, cs, qr);
+                qi = fmaf(q.w, sn, qi);
             }
-            for (; k < n; ++k) term(sk[k], x, y, z, false, qr, qi);
         }
         if (live) {
             a.qr[i] = qr;
