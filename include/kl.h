@@ -233,7 +233,9 @@ const char* kl_last_error(const kl_ctx* ctx);
 
 /* Alg.1 lines 2-3: add kernel K to the pending set R; returns its id (>= 1). */
 kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* desc, uint64_t* out_id);
-/* kl_submit for n descriptors in order (one ABI crossing for a whole queue). */
+/* kl_submit for n descriptors in order (one ABI crossing for a whole queue); out_ids[n] (may be
+ * NULL).  Errors as kl_submit: the first failing descriptor's status is returned, the ones before
+ * it stay submitted. */
 kl_status kl_submit_batch(kl_ctx* ctx, const kl_kernel_desc* descs, size_t n, uint64_t* out_ids);
 /* Slicing plan: slices of slice_blocks contiguous blocks at
  * blocks_per_sm resident blocks per SM; slice_blocks = 0 applies the p% rule (m_min waves). */
@@ -260,7 +262,7 @@ kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* desc, void* stream,
  * Occupancy sweeps for the calibration (solo IPC vs warps, the E4 analog). */
 kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* desc, uint32_t cap, double* ms);
 /* Co-run two whole kernels outside the scheduler at caps (cap1, cap2): both are launched through
- * the slice launcher, the survivor is stopped at its slice boundary when the first runs out of
+ * the slice launcher, the survivor is stopped at its next fetch when the first runs out of
  * blocks, and the two launch records are returned (config C3: measured concurrent progress vs
  * the model's cIPC; E5/E7 analogs). */
 kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, const kl_kernel_desc* d2,
@@ -292,15 +294,15 @@ kl_status kl_decide(kl_ctx* ctx, kl_coschedule* out);
  * be NULL).  Record a kernel's ready_event on the same stream after it: the kernel arrives then.
  * Consecutive calls on one stream give cumulative arrival times.  Errors: KL_ECUDA. */
 kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev);
+/* Stream gate / time stamp (one thread): waits until *flag != 0 (flag may be NULL: no wait), then
+ * writes %globaltimer to *stamp_dev (may be NULL).  For baselines driven by kl_arrival_clock. */
+kl_status kl_wait_flag(void* stream, const volatile uint32_t* flag, uint64_t* stamp_dev);
 /* Arrival clock for n arrivals in one resident thread (no per-arrival launch, so the arrivals
  * never wait for an SM slot): enqueue on `stream` a one-thread kernel that, for i = 0..n-1,
  * sleeps gaps_dev[i] ns of device time after the previous release, writes the release time
  * (%globaltimer) to stamps_dev[i] and then sets flags[i] = 1 (flags: host-mapped memory, the
  * kernels' kl_kernel_desc.ready_flag).  gaps_dev, stamps_dev: device uint64[n].  The kernel
  * occupies one warp slot of one SM until the last release.  Errors: KL_ECUDA. */
-/* Stream gate / time stamp (one thread): waits until *flag != 0 (flag may be NULL: no wait), then
- * writes %globaltimer to *stamp_dev (may be NULL).  For baselines driven by kl_arrival_clock. */
-kl_status kl_wait_flag(void* stream, const volatile uint32_t* flag, uint64_t* stamp_dev);
 kl_status kl_arrival_clock(void* stream, const uint64_t* gaps_dev, uint64_t* stamps_dev, uint32_t* flags,
                            uint32_t n);
 kl_status kl_stats_get(kl_ctx* ctx, kl_stats* out);
