@@ -299,8 +299,9 @@ kl_status kl_delay(void* stream, uint64_t ns, uint64_t* stamp_dev);
 kl_status kl_wait_flag(void* stream, const volatile uint32_t* flag, uint64_t* stamp_dev);
 /* Arrival clock for n arrivals in one resident thread (no per-arrival launch, so the arrivals
  * never wait for an SM slot): enqueue on `stream` a one-thread kernel that, for i = 0..n-1,
- * sleeps gaps_dev[i] ns of device time after the previous release, writes the release time
- * (%globaltimer) to stamps_dev[i] and then sets flags[i] = 1 (flags: host-mapped memory, the
+ * waits until device time t_start + gaps_dev[0] + ... + gaps_dev[i] (a cumulative schedule: a
+ * late release does not delay the later ones), writes the release time (%globaltimer) to
+ * stamps_dev[i] and then sets flags[i] = 1 (flags: host-mapped memory, the
  * kernels' kl_kernel_desc.ready_flag).  gaps_dev, stamps_dev: device uint64[n].  The kernel
  * occupies one warp slot of one SM until the last release.  Errors: KL_ECUDA. */
 kl_status kl_arrival_clock(void* stream, const uint64_t* gaps_dev, uint64_t* stamps_dev, uint32_t* flags,
