@@ -217,42 +217,88 @@ struct BodyST {
     }
 };
 
-// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks
-// with 2*pi folded into k at staging time, so the inner loop is 3 FMA for the phase, the two
-// MUFU ops (MUFU.SIN/COS reduce the argument themselves) and 2 FMA accumulates.  MUFU-bound:
-// 2 MUFU ops per (voxel, k) at 16 lanes/clk/SM.
+// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks.
+// A pure __sincosf loop is MUFU-bound: 2 MUFU ops per (voxel, k) take 16 pipe cycles per warp
+// on an SMSP while the loop issues only 9 instructions (ncu: XU 96 %, issue 56 %).  So in every
+// group of KL_MRIQ_G consecutive k-points the last KL_MRIQ_P take sin/cos from FMA-pipe
+// polynomials (sincos_2pi_poly, ~22 issue slots, no MUFU) and the rest from MUFU.  The issue /
+// MUFU balance max(16 (1-f), 9 (1-f) + 22 f) predicts f = P/G = 1/4; measured (variants built by
+// tools/exp_mriq_mix.py, ncu in tools/ncu_mriq_mix.sh) f = 1/8 is the fastest, 1.97 -> 1.82 ms
+// plain grid, 1.98 -> 1.90 ms persistent; at f = 1/4 the XU pipe drops to 71 % but the kernel
+// does not speed up (issue 76 %, MIO-throttle and not-selected stalls).  MUFU terms are staged
+// with 2 pi folded into k (radians for __sincosf), polynomial terms in revolutions (the argument
+// reduction is then t - rint(t)).
+#ifndef KL_MRIQ_G
+#define KL_MRIQ_G 8
+#endif
+#ifndef KL_MRIQ_P
+#define KL_MRIQ_P 1
+#endif
+// sin(2 pi t), cos(2 pi t) on the FMA pipe: r = t - rint(t) in [-1/2, 1/2] (rint by the
+// 1.5*2^23 rounding trick, exact for |t| < 2^22), then sin = r P(r^2) (degree 5 in r^2) and
+// cos = Q(r^2) (degree 6), near-minimax coefficients (Lawson-weighted least squares on
+// [-1/2, 1/2], rounded to fp32).  Max abs error in fp32 arithmetic: 7.1e-7 (sin), 4.0e-7 (cos),
+// the same order as MUFU.SIN/COS (2^-21 near 0, growing with |t|).
+__device__ __forceinline__ void sincos_2pi_poly(float t, float& s, float& c) {
+    const float magic = 12582912.0f;                       // 1.5 * 2^23
+    const float r = t - ((t + magic) - magic);
+    const float u = r * r;
+    float ps = fmaf(u, -12.271262168884277f, 41.20539474487305f);
+    ps = fmaf(u, ps, -76.5801010131836f);
+    ps = fmaf(u, ps, 81.59618377685547f);
+    ps = fmaf(u, ps, -41.34142303466797f);
+    ps = fmaf(u, ps, 6.283182621002197f);
+    s = r * ps;
+    float pc = fmaf(u, 6.5296101570129395f, -25.968313217163086f);
+    pc = fmaf(u, pc, 60.16783142089844f);
+    pc = fmaf(u, pc, -85.45016479492188f);
+    pc = fmaf(u, pc, 64.93911743164062f);
+    pc = fmaf(u, pc, -19.73920440673828f);
+    c = fmaf(u, pc, 1.0f);
+}
+
 struct BodyMRIQ {
     using Params = kl_args_mriq;
     using State = Empty;
     static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
+    static constexpr int kG = KL_MRIQ_G, kP = KL_MRIQ_P;
+    static_assert(kP >= 0 && kP < kG, "KL_MRIQ_P in [0, KL_MRIQ_G)");
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
+    __device__ static __forceinline__ void term(const float4 q, float x, float y, float z, bool poly,
+                                                float& qr, float& qi) {
+        const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
+        float sn, cs;
+        if (poly) sincos_2pi_poly(t, sn, cs);
+        else __sincosf(t, &sn, &cs);
+        qr = fmaf(q.w, cs, qr);
+        qi = fmaf(q.w, sn, qi);
+    }
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        __shared__ float4 sk[256];   // (2 pi kx, 2 pi ky, 2 pi kz, phiMag)
+        __shared__ float4 sk[256];   // (kx, ky, kz) x 2 pi (MUFU terms) or x 1 (polynomial terms), phiMag
         const int i = (int)vb * 256 + threadIdx.x;
         const bool live = i < a.num_x;
         const float x = live ? __ldg(a.x + i) : 0.f, y = live ? __ldg(a.y + i) : 0.f,
                     z = live ? __ldg(a.z + i) : 0.f;
         float qr = 0.f, qi = 0.f;
-        const float two_pi = 6.28318530717958647692f;
         for (int k0 = 0; k0 < a.num_k; k0 += 256) {
             const int n = min(256, a.num_k - k0);
+            const int n_full = n - n % kG;                  // whole groups; the tail is all MUFU
             __syncthreads();
             if ((int)threadIdx.x < n) {
                 const int k = k0 + threadIdx.x;
-                sk[threadIdx.x] = make_float4(two_pi * __ldg(a.kx + k), two_pi * __ldg(a.ky + k),
-                                              two_pi * __ldg(a.kz + k), __ldg(a.phimag + k));
+                const bool poly = (int)threadIdx.x < n_full && (int)threadIdx.x % kG >= kG - kP;
+                const float sc = poly ? 1.0f : 6.28318530717958647692f;
+                sk[threadIdx.x] = make_float4(sc * __ldg(a.kx + k), sc * __ldg(a.ky + k),
+                                              sc * __ldg(a.kz + k), __ldg(a.phimag + k));
             }
             __syncthreads();
-#pragma unroll 8
-            for (int k = 0; k < n; ++k) {
-                const float4 q = sk[k];
-                const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
-                float sn, cs;
-                __sincosf(t, &sn, &cs);
-                qr = fmaf(q.w, cs, qr);
-                qi = fmaf(q.w, sn, qi);
+            int k = 0;
+            for (; k < n_full; k += kG) {
+#pragma unroll
+                for (int j = 0; j < kG; ++j) term(sk[k + j], x, y, z, j >= kG - kP, qr, qi);
             }
+            for (; k < n; ++k) term(sk[k], x, y, z, false, qr, qi);
         }
         if (live) {
             a.qr[i] = qr;
