@@ -192,7 +192,8 @@ int kl_dev_model_general(const KlModelKind* kinds, KlModelCfg cfg, const KlCand*
                          uint32_t* done_counter, KlDecision* dec, double* scratch,
                          const int64_t* scratch_off, void* stream);
 
-// Batched model: one CTA per candidate; if n_pairs > 0 the last CTA to finish runs the greedy
+// Batched model: one CTA per candidate plus one per kind (solo chains); `preds` holds n_cand +
+// KL_NKINDS entries (the tail is scratch).  If n_pairs > 0 the last CTA to finish runs the greedy
 // selection (a9) and writes *dec.  `done_counter` must be zero on entry (reset by the kernel).
 int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* cands,
                        kl_prediction* preds, int n_pairs, const int32_t* pair_rank,

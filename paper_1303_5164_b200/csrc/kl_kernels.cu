@@ -24,6 +24,15 @@ namespace {
 struct Empty {};
 
 // PC: 256 threads; dependent loads through the read-only path.
+#ifndef KL_MINB_ST
+#define KL_MINB_ST 16
+#endif
+#ifndef KL_MINB_MRIQ
+#define KL_MINB_MRIQ 8
+#endif
+#ifndef KL_MINB_BS
+#define KL_MINB_BS 9
+#endif
 struct BodyPC {
     using Params = kl_args_pc;
     using State = Empty;
@@ -158,7 +167,7 @@ struct BodyST {
     // the oracle's definition (bit-identical); boundary points copy the input.  nx % 4 == 0.
     using Params = kl_args_st;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 16;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = KL_MINB_ST;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     static constexpr int kTz = 32;   // z points per block (kl_inputs.ST_TILE)
@@ -260,7 +269,7 @@ __device__ __forceinline__ void sincos_2pi_poly(float t, float& s, float& c) {
 struct BodyMRIQ {
     using Params = kl_args_mriq;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = 8;
+    static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = KL_MINB_MRIQ;
     static constexpr int kG = KL_MRIQ_G, kP = KL_MRIQ_P;
     static_assert(kP >= 0 && kP < kG, "KL_MRIQ_P in [0, KL_MRIQ_G)");
     __device__ static void init(const Params&, State&, char*) {}
@@ -329,7 +338,7 @@ __device__ __forceinline__ void bs_one(float S, float X, float T, float R, float
 struct BodyBS {
     using Params = kl_args_bs;
     using State = Empty;
-    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = 9;
+    static constexpr int kThreads = 128, kChunk = 1, kDynSmem = 0, kMinBlocks = KL_MINB_BS;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {

@@ -11,11 +11,19 @@
 // R4/R5 shared round and latency in the joint chain; R14 w = b * wpb / n_sched; R22 guard L > W.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 #include "kl_internal.h"
 #include "kl_model_common.cuh"
 
 namespace {
 
+#ifdef KL_MODEL_PROFILE
+__device__ __forceinline__ unsigned long long gtimer_m() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 constexpr int kMaxW = 16;                 // virtual-SM warps (64 warps / 4 schedulers)
 constexpr int kMaxS = (kMaxW / 2 + 1) * (kMaxW / 2 + 1);   // 81 joint states at W_v = 16
 constexpr int kThreads = 256;
@@ -89,6 +97,9 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     __shared__ double inv_s[kMaxS];
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
+#ifdef KL_MODEL_PROFILE
+    const unsigned long long tq0 = gtimer_m();
+#endif
     // ---- chain build: one warp per state row
     for (int s = warp; s < S; s += NW) {
         const int p = s / nb, q = s - p * nb;
@@ -110,61 +121,84 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     }
     __syncthreads();
     if (s_bad) return s_bad;
+#ifdef KL_MODEL_PROFILE
+    const unsigned long long tq1 = gtimer_m();
+#endif
     // ---- GTH: for k = S-1 .. 1: s_k = sum_{j<k} P[k][j]; P[i][j] += (P[i][k]/s_k) P[k][j], i,j < k.
-    // 16 x 16 thread tile (rows i = ty + 16m, columns j = tx + 16n); column k is left unscaled
-    // (back substitution applies 1/s_k), and the half-warp owning row k-1 reduces the next pivot
-    // sum from its freshly updated values: one barrier per eliminated state.
+    // The trailing matrix lives in registers: thread (ty, tx) of a 16 x 16 tile holds
+    // a[m][n] = P[ty + 16m][tx + 16n].  Per eliminated state the half-warp owning row k publishes
+    // it (and its pivot sum, reduced by shuffles) to a double-buffered row buffer, the threads
+    // owning column k publish it into P's column k in shared memory (left unscaled: the back
+    // substitution applies 1/s_k and reads exactly these columns), one barrier, then every thread
+    // applies the rank-1 update to its registers.  Shared memory carries 2 S values per state
+    // instead of the whole k x k update.
+    constexpr int kT = kMaxS / 16 + 1;      // 6 x 6 register tile per thread
+    __shared__ double s_row[2][16 * kT];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    if (warp == 0) {
-        double part = 0.0;
-        for (int j = lane; j < S - 1; j += 32) part += P[(S - 1) * S + j];
-        part = warp_sum(part);
-        if (lane == 0) {
-            s_piv[(S - 1) & 1] = part;
-            s_inv[(S - 1) & 1] = 1.0 / part;
+    double a[kT][kT];
+#pragma unroll
+    for (int m = 0; m < kT; ++m)
+#pragma unroll
+        for (int n = 0; n < kT; ++n) {
+            const int i = ty + 16 * m, j = tx + 16 * n;
+            a[m][n] = (i < S && j < S) ? P[i * S + j] : 0.0;
+        }
+    __syncthreads();   // P is now only the column store for the back substitution
+    for (int k = S - 1; k >= 1; --k) {
+        const int mk = k >> 4, buf = k & 1;
+        if ((ty >> 1) == ((k & 15) >> 1)) {   // the warp holding row k (in one of its halves):
+            double part = 0.0;                   // publish the row and its pivot sum
+            const bool own = ty == (k & 15);
+#pragma unroll
+            for (int m = 0; m < kT; ++m)
+                if (own && m == mk) {
+#pragma unroll
+                    for (int n = 0; n < kT; ++n) {
+                        const int j = tx + 16 * n;
+                        const double v = j < k ? a[m][n] : 0.0;
+                        s_row[buf][j] = v;
+                        part += v;
+                    }
+                }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (own && tx == 0) {
+                s_piv[buf] = part;
+                s_inv[buf] = 1.0 / part;
+                inv_s[k] = 1.0 / part;
+            }
+        }
+        if (tx == (k & 15)) {   // threads owning column k: publish it (rows i < k)
+#pragma unroll
+            for (int n = 0; n < kT; ++n)
+                if (n == mk) {
+#pragma unroll
+                    for (int m = 0; m < kT; ++m) {
+                        const int i = ty + 16 * m;
+                        if (i < k) P[i * S + k] = a[m][n];
+                    }
+                }
+        }
+        __syncthreads();
+        if (!(s_piv[buf] > 0.0)) return KL_ENUMERIC;   // uniform across the block
+        const double inv = s_inv[buf];
+        double rk[kT];
+#pragma unroll
+        for (int n = 0; n < kT; ++n) rk[n] = s_row[buf][tx + 16 * n];   // 0 beyond k
+#pragma unroll
+        for (int m = 0; m < kT; ++m) {
+            const int i = ty + 16 * m;
+            if (i < k) {
+                const double c = P[i * S + k] * inv;
+#pragma unroll
+                for (int n = 0; n < kT; ++n) a[m][n] = fma(c, rk[n], a[m][n]);
+            }
         }
     }
     __syncthreads();
-    for (int k = S - 1; k >= 1; --k) {
-        const double sk = s_piv[k & 1];
-        if (!(sk > 0.0)) return KL_ENUMERIC;   // uniform across the block
-        const double inv = s_inv[k & 1];
-        if (threadIdx.x == 0) inv_s[k] = inv;
-        const double* rk = P + k * S;
-        double pk[kMaxS / 16 + 1];
-#pragma unroll
-        for (int n = 0; n < kMaxS / 16 + 1; ++n) {
-            const int j = tx + 16 * n;
-            pk[n] = j < k ? rk[j] : 0.0;
-        }
-        for (int i = ty; i < k; i += 16) {
-            double* ri = P + i * S;
-            const double a = ri[k] * inv;
-#pragma unroll
-            for (int n = 0; n < kMaxS / 16 + 1; ++n) {
-                const int j = tx + 16 * n;
-                if (j < k) ri[j] = fma(a, pk[n], ri[j]);
-            }
-        }
-        if (warp == (((k - 1) & 15) >> 1)) {   // warp-uniform: holds row k-1 in one half
-            double part = 0.0;
-            if (ty == ((k - 1) & 15)) {         // re-read this thread's own updates of row k-1
-                const double* rp = P + (k - 1) * S;
-#pragma unroll
-                for (int n = 0; n < kMaxS / 16 + 1; ++n) {
-                    const int j = tx + 16 * n;
-                    if (j < k - 1) part += rp[j];
-                }
-            }
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            if (tx == 0 && ty == ((k - 1) & 15)) {
-                s_piv[(k - 1) & 1] = part;
-                s_inv[(k - 1) & 1] = 1.0 / part;
-            }
-        }
-        __syncthreads();
-    }
+#ifdef KL_MODEL_PROFILE
+    const unsigned long long tq2 = gtimer_m();
+#endif
     // back substitution by warp 0: pi_0 = 1, pi_j = (1/s_j) sum_{i<j} pi_i P[i][j] (column
     // accumulators m = lane + 32 t held in registers)
     if (warp == 0) {
@@ -186,6 +220,9 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     }
     __syncthreads();
     const double tot = red[8];
+#ifdef KL_MODEL_PROFILE
+    if (threadIdx.x == 0 && S > 60 && blockIdx.x % 20 == 0) printf("MPC S=%d build %.1f gth %.1f back %.1f us\n", S, (tq1 - tq0) / 1e3, (tq2 - tq1) / 1e3, (gtimer_m() - tq2) / 1e3);
+#endif
     double den = 0.0, na = 0.0, nbs = 0.0;
     for (int s = threadIdx.x; s < S; s += kThreads) {
         const int p = s / nb, q = s - p * nb;
@@ -203,7 +240,12 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     return KL_OK;
 }
 
-__global__ void __launch_bounds__(kThreads)
+// Grid: cfg.n_cand candidate CTAs, then KL_NKINDS solo CTAs.  Solo CTA kk solves kind kk's solo
+// chain at its solo occupancy b^max (Eq.4) once for the whole batch -- every candidate of the
+// kind shares it -- into preds[n_cand + kk] (ipc in .solo1); candidate CTAs solve only their
+// joint chain (Eq.5-7).  The CTA that finishes last completes every prediction (solo IPCs, Eq.1
+// CP, Eq.8 dT), publishes them, and runs the selection (a9) if n_pairs > 0.
+__global__ void __launch_bounds__(kThreads, 2)   // 2 CTAs per SM: a 202-candidate batch stays one wave
 k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const KlCand* __restrict__ cands,
               kl_prediction* preds, int n_pairs, const int32_t* __restrict__ pair_off,
               uint32_t* done_counter, KlDecision* dec) {
@@ -213,55 +255,105 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     double* Rs = pi + kMaxS;               // kMaxS
     double* red = Rs + kMaxS;              // 16
     __shared__ double s_binom[kMaxW + 1][kMaxW + 1];
+    __shared__ KlCand s_cd;
+    __shared__ KlModelKind s_k[2];
+    const int n = cfg.n_cand;
+    const bool solo_cta = (int)blockIdx.x >= n;
     for (int x = threadIdx.x; x < (kMaxW + 1) * (kMaxW + 1); x += kThreads)
         s_binom[x / (kMaxW + 1)][x % (kMaxW + 1)] = c_binom[x / (kMaxW + 1)][x % (kMaxW + 1)];
-    __syncthreads();
-
-    const KlCand cd = cands[blockIdx.x];
-    const KlModelKind k1 = kinds[cd.k1], k2 = kinds[cd.k2];
-    kl_prediction out = {};
-    int status = 0;
-    const int t1 = (int)cd.b1 * k1.wpb, t2 = (int)cd.b2 * k2.wpb;
-    const int ts1 = k1.bsolo * k1.wpb, ts2 = k2.bsolo * k2.wpb;
-    if (t1 % cfg.n_sched || t2 % cfg.n_sched || ts1 % cfg.n_sched || ts2 % cfg.n_sched) status = KL_EINFEASIBLE;
-    const int w1 = t1 / cfg.n_sched, w2 = t2 / cfg.n_sched;
-    const int ws1 = ts1 / cfg.n_sched, ws2 = ts2 / cfg.n_sched;
-    const bool solo_query = (cd.b2 == 0);   // prediction of k1 alone at b1 (calibration)
-    if (w1 < 1 || (w2 < 1 && !solo_query) || w1 + w2 > cfg.W || ws1 < 1 || ws1 > cfg.W || ws2 < 1 ||
-        ws2 > cfg.W || (w1 + 1) * (w2 + 1) > kMaxS || cfg.W > kMaxW)
-        status = KL_EINFEASIBLE;
-    ChainOut co;
-    if (status == 0) {   // Eq.4 solo IPCs at b^max
-        status = chain_ipc(&k1, ws1, nullptr, 0, cfg, P, pi, Rs, red, s_binom, &co);
-        out.solo1 = co.ipc_a;
-        if (status == 0) {
-            status = chain_ipc(&k2, ws2, nullptr, 0, cfg, P, pi, Rs, red, s_binom, &co);
-            out.solo2 = co.ipc_a;
+    if (threadIdx.x == 0) {   // one reader of the host-mapped inputs, broadcast through smem
+        if (solo_cta) {
+            s_k[0] = kinds[blockIdx.x - n];
+        } else {
+            const KlCand cd = cands[blockIdx.x];
+            s_cd = cd;
+            s_k[0] = kinds[cd.k1];
+            s_k[1] = kinds[cd.k2];
         }
-        if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
     }
-    if (status == 0) {   // joint chain, Eq.5-7 with R_(i,j) = joint round duration (R4)
-        status = chain_ipc(&k1, w1, solo_query ? nullptr : &k2, solo_query ? 0 : w2, cfg, P, pi, Rs, red, s_binom, &co);
-        if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
+    __syncthreads();
+#ifdef KL_MODEL_PROFILE
+    unsigned long long tp0 = gtimer_m();
+#endif
+    ChainOut co;
+    if (solo_cta) {
+        const KlModelKind k1 = s_k[0];
+        const int ts = k1.bsolo * k1.wpb, ws = ts / cfg.n_sched;
+        int status = (ts % cfg.n_sched || ws < 1 || ws > cfg.W || cfg.W > kMaxW) ? KL_EINFEASIBLE : 0;
         if (status == 0) {
-            out.ipc1 = co.ipc_a;
-            out.ipc2 = co.ipc_b;
-            out.c = out.ipc1 + out.ipc2;
-            if (!solo_query) {
-                out.cp = 1.0 - 1.0 / (out.ipc1 / out.solo1 + out.ipc2 / out.solo2);   // Eq.1
-                out.dT = fabs(k1.ipb * (double)cd.b1 / out.ipc1 - k2.ipb * (double)cd.b2 / out.ipc2);  // Eq.8
+            status = chain_ipc(&k1, ws, nullptr, 0, cfg, P, pi, Rs, red, s_binom, &co);
+            if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
+        }
+        if (threadIdx.x == 0) {
+            kl_prediction o = {};
+            o.solo1 = status == 0 ? co.ipc_a : 0.0;
+            o.status = status;
+            preds[blockIdx.x] = o;
+        }
+    } else {
+        const KlCand cd = s_cd;
+        const KlModelKind k1 = s_k[0], k2 = s_k[1];
+        kl_prediction out = {};
+        int status = 0;
+        const int t1 = (int)cd.b1 * k1.wpb, t2 = (int)cd.b2 * k2.wpb;
+        const int ts1 = k1.bsolo * k1.wpb, ts2 = k2.bsolo * k2.wpb;
+        if (t1 % cfg.n_sched || t2 % cfg.n_sched || ts1 % cfg.n_sched || ts2 % cfg.n_sched) status = KL_EINFEASIBLE;
+        const int w1 = t1 / cfg.n_sched, w2 = t2 / cfg.n_sched;
+        const int ws1 = ts1 / cfg.n_sched, ws2 = ts2 / cfg.n_sched;
+        const bool solo_query = (cd.b2 == 0);   // prediction of k1 alone at b1 (calibration)
+        if (w1 < 1 || (w2 < 1 && !solo_query) || w1 + w2 > cfg.W || ws1 < 1 || ws1 > cfg.W || ws2 < 1 ||
+            ws2 > cfg.W || (w1 + 1) * (w2 + 1) > kMaxS || cfg.W > kMaxW)
+            status = KL_EINFEASIBLE;
+        if (status == 0) {   // joint chain, Eq.5-7 with R_(i,j) = joint round duration (R4)
+            status = chain_ipc(&k1, w1, solo_query ? nullptr : &k2, solo_query ? 0 : w2, cfg, P, pi, Rs, red,
+                               s_binom, &co);
+            if (status == KL_EINFEASIBLE) status = KL_ENUMERIC;
+            if (status == 0) {
+                out.ipc1 = co.ipc_a;
+                out.ipc2 = co.ipc_b;
+                out.c = out.ipc1 + out.ipc2;
             }
         }
+        out.status = status;
+        if (threadIdx.x == 0) {
+            preds[blockIdx.x] = out;
+            if (cfg.cands_dev) cfg.cands_dev[blockIdx.x] = cd;
+        }
     }
-    out.status = status;
-    if (threadIdx.x == 0) {
-        preds[blockIdx.x] = out;
-        if (cfg.preds_host) cfg.preds_host[blockIdx.x] = out;   // the host reads these (mapped)
-        if (cfg.cands_dev) cfg.cands_dev[blockIdx.x] = cd;
+#ifdef KL_MODEL_PROFILE
+    if (threadIdx.x == 0 && blockIdx.x % 20 == 0)
+        printf("MP cta %d %s chain %.1f us\n", blockIdx.x, solo_cta ? "solo" : "joint", (gtimer_m() - tp0) / 1e3);
+#endif
+    if (!last_cta(done_counter)) return;
+    // the last CTA: complete every prediction with the shared solo IPCs (Eq.4), Eq.1 and Eq.8
+    const KlCand* cl = cfg.cands_dev ? cfg.cands_dev : cands;
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+        kl_prediction o = preds[i];
+        const KlCand cd = cl[i];
+        if (o.status != KL_EINFEASIBLE) {
+            const kl_prediction s1 = preds[n + cd.k1], s2 = preds[n + cd.k2];
+            if (s1.status || s2.status) {
+                o.status = KL_ENUMERIC;   // a solo chain failed (range failures are caught above)
+            } else {
+                o.solo1 = s1.solo1;
+                o.solo2 = s2.solo1;
+                if (o.status == 0 && cd.b2 != 0) {
+                    o.cp = 1.0 - 1.0 / (o.ipc1 / o.solo1 + o.ipc2 / o.solo2);   // Eq.1
+                    o.dT = fabs(kinds[cd.k1].ipb * (double)cd.b1 / o.ipc1 -
+                                kinds[cd.k2].ipb * (double)cd.b2 / o.ipc2);      // Eq.8
+                }
+            }
+        }
+        preds[i] = o;
+        if (cfg.preds_host) cfg.preds_host[i] = o;   // the host reads these (mapped)
     }
-    if (n_pairs <= 0) return;
-
-    select_last<kThreads>(cfg, kinds, cfg.cands_dev ? cfg.cands_dev : cands, preds, n_pairs, pair_off, done_counter, dec);
+    __threadfence();
+    __syncthreads();
+    if (n_pairs > 0) {
+        select_body<kThreads>(cfg, kinds, cl, preds, n_pairs, pair_off, done_counter, dec);
+    } else if (threadIdx.x == 0) {
+        *done_counter = 0u;
+    }
 }
 
 }  // namespace
@@ -294,7 +386,7 @@ int kl_dev_model_batch(const KlModelKind* kinds, KlModelCfg cfg, const KlCand* c
         if (e) return e;
         attr = true;
     }
-    k_model_batch<<<cfg.n_cand, kThreads, smem, (cudaStream_t)stream>>>(kinds, cfg, cands, preds, n_pairs,
+    k_model_batch<<<cfg.n_cand + KL_NKINDS, kThreads, smem, (cudaStream_t)stream>>>(kinds, cfg, cands, preds, n_pairs,
                                                                       pair_off, done_counter, dec);
     return (int)cudaGetLastError();
 }

@@ -69,21 +69,29 @@ __device__ bool better_split(const kl_prediction& a, const KlCand& ca, const kl_
     return ca.b1 < cb.b1;
 }
 
-// Fused selection (a9) by the CTA that finishes last: per pair the best split (better_split),
-// then argmax CP over pairs.  Called by every CTA after writing its prediction.
-template <int kThreads>
-__device__ void select_last(const KlModelCfg& cfg, const KlModelKind* kinds, const KlCand* __restrict__ cands,
-                            kl_prediction* preds,
-                            int n_pairs, const int32_t* __restrict__ pair_off, uint32_t* done_counter,
-                            KlDecision* dec) {
+// True in every thread of the CTA that finishes last (the others see false); each CTA calls it
+// once after writing its prediction.  The last CTA resets the counter in select_body (or itself
+// when no selection follows).
+__device__ __forceinline__ bool last_cta(uint32_t* done_counter) {
     __shared__ int s_last;
-    __shared__ int s_best_pair[128];
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(done_counter, 1u) == gridDim.x - 1);
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}
+
+// Fused selection (a9) by the CTA that finishes last: per pair the best split (better_split),
+// then argmax CP over pairs.  Called by every CTA after writing its prediction.
+template <int kThreads>
+__device__ void select_body(const KlModelCfg& cfg, const KlModelKind* kinds_in, const KlCand* __restrict__ cands,
+                            const kl_prediction* preds, int n_pairs, const int32_t* __restrict__ pair_off,
+                            uint32_t* done_counter, KlDecision* dec) {
+    __shared__ int s_best_pair[128];
+    __shared__ KlModelKind kinds[KL_NKINDS];   // staged: the table lives in host-mapped memory
+    for (int k = threadIdx.x; k < KL_NKINDS; k += kThreads) kinds[k] = kinds_in[k];
+    __syncthreads();
     for (int pr = threadIdx.x; pr < n_pairs; pr += kThreads) {
         int best = -1;
         kl_prediction bp;
@@ -114,6 +122,13 @@ __device__ void select_last(const KlModelCfg& cfg, const KlModelKind* kinds, con
         __threadfence_system();
         dec->done = 1;
     }
+}
+
+template <int kThreads>
+__device__ void select_last(const KlModelCfg& cfg, const KlModelKind* kinds, const KlCand* __restrict__ cands,
+                            const kl_prediction* preds, int n_pairs, const int32_t* __restrict__ pair_off,
+                            uint32_t* done_counter, KlDecision* dec) {
+    if (last_cta(done_counter)) select_body<kThreads>(cfg, kinds, cands, preds, n_pairs, pair_off, done_counter, dec);
 }
 
 }  // namespace

@@ -1154,7 +1154,7 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
             KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->off_dev, ctx->off_pinned, 0));
             KL_CUDA(cudaHostAlloc(&ctx->pred_pinned, sizeof(kl_prediction) * kMaxCand, cudaHostAllocMapped));
             KL_CUDA(cudaHostGetDevicePointer((void**)&ctx->pred_host_dev, ctx->pred_pinned, 0));
-            KL_CUDA(cudaMalloc(&ctx->pred_dev, sizeof(kl_prediction) * kMaxCand));   // fused selection
+            KL_CUDA(cudaMalloc(&ctx->pred_dev, sizeof(kl_prediction) * (kMaxCand + KL_NKINDS)));   // + per-kind solo slots
             KL_CUDA(cudaMalloc(&ctx->cand_scratch, sizeof(KlCand) * kMaxCand));
             KL_CUDA(cudaMalloc(&ctx->done_dev, sizeof(uint32_t)));
             KL_CUDA(cudaMemset(ctx->done_dev, 0, sizeof(uint32_t)));
