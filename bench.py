@@ -88,8 +88,8 @@ def algorithmic_work(kind: str, p: dict) -> dict:
     if kind == "MM":
         return {"bound": "tensor", "flops": 2.0 * p["M"] * p["N"] * p["K"],
                 "bytes": 2 * (p["M"] * p["K"] + p["N"] * p["K"]) + 4 * p["M"] * p["N"]}
-    if kind == "MRIQ":    # one (sin, cos) pair per (voxel, k), from MUFU or the FMA pipe
-        return {"bound": "alu", "ops": 1.0 * p["num_x"] * p["num_k"], "bytes": 5 * 4 * p["num_x"]}
+    if kind == "MRIQ":    # sin + cos per (voxel, k): MUFU-bound
+        return {"bound": "alu", "ops": 2.0 * p["num_x"] * p["num_k"], "bytes": 5 * 4 * p["num_x"]}
     if kind == "BS":
         return {"bound": "hbm", "bytes": 5 * 4 * p["n"]}
     if kind == "TEA":     # 32 cycles x ~10 integer ops per 64-bit block
@@ -124,16 +124,13 @@ def ncu_traffic(kind: str):
 
 
 def alu_peak(kind: str, sm_mhz: float, n_sm: int = 148) -> tuple[float, str]:
-    """ALU peaks from unit counts x clock (B300_MICROARCH pipe rates): MRIQ's
-    (sin, cos) pairs come from MUFU (16 ops/clk/SM: a warp's pair holds an SMSP's MUFU for 16
-    cycles while its loop issues 9 instructions) or from FMA-pipe polynomials (22 issue slots, no
-    MUFU); the best mix f = 7/29 of pairs on the FMA pipe costs 16 (1 - f) = 12.14 cycles per warp
-    pair per SMSP, i.e. 128 / 12.14 = 10.54 pairs/clk/SM (MUFU alone: 8); SAD's VABSDIFF4 on the alu pipe, 64 lanes/clk/SM (rt 2 per SMSP);
+    """ALU peaks from unit counts x clock (B300_MICROARCH pipe rates): MUFU 16
+    ops/clk/SM (sin, cos); SAD's VABSDIFF4 on the alu pipe, 64 lanes/clk/SM (rt 2 per SMSP);
     TEA's integer mix spreads over the alu pipe (IADD3/LOP3/SHF) and the fma pipe (IMAD), so its
     ceiling is the issue rate, 128 lanes/clk/SM."""
     f = sm_mhz * 1e6
     if kind == "MRIQ":
-        return 128 * 29 / (16 * 22) * n_sm * f, "(sin,cos) pairs/s (MUFU 16 ops/clk/SM + FMA-pipe polynomials, issue 128/clk/SM)"
+        return 16 * n_sm * f, "MUFU ops/s (16/clk/SM)"
     if kind == "TEA":
         return 128 * n_sm * f, "int ops/s (alu+fma pipes, issue 128/clk/SM)"
     return 64 * n_sm * f, "int ALU ops/s (64/clk/SM)"

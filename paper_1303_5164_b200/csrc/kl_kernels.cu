@@ -226,22 +226,25 @@ struct BodyST {
     }
 };
 
-// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks.
-// A pure __sincosf loop is MUFU-bound: 2 MUFU ops per (voxel, k) take 16 pipe cycles per warp
-// on an SMSP while the loop issues only 9 instructions (ncu: XU 96 %, issue 56 %).  So in every
-// group of KL_MRIQ_G consecutive k-points the last KL_MRIQ_P take sin/cos from FMA-pipe
-// polynomials (sincos_2pi_poly, ~22 issue slots, no MUFU) and the rest from MUFU.  The issue /
-// MUFU balance max(16 (1-f), 9 (1-f) + 22 f) predicts f = P/G = 1/4; measured (variants built by
-// tools/exp_mriq_mix.py, ncu in tools/ncu_mriq_mix.sh) f = 1/8 is the fastest, 1.97 -> 1.82 ms
-// plain grid, 1.98 -> 1.90 ms persistent; at f = 1/4 the XU pipe drops to 71 % but the kernel
-// does not speed up (issue 76 %, MIO-throttle and not-selected stalls).  MUFU terms are staged
-// with 2 pi folded into k (radians for __sincosf), polynomial terms in revolutions (the argument
-// reduction is then t - rint(t)).
+// MRIQ (Parboil ComputeQ): one voxel per thread; k-space staged in 256-entry chunks,
+// 2 pi folded into k at staging time, so the inner loop is 3 FMA for the phase, the two MUFU
+// ops (__sincosf: FMUL.RZ by 1/2pi, MUFU.SIN, MUFU.COS) and 2 FMA accumulates.  MUFU-bound: 2
+// MUFU ops per (voxel, k) take 16 pipe cycles per warp on an SMSP while the loop issues 9
+// instructions (ncu: XU 96 %, issue 56 %).
+// Measured and not adopted (compile-time KL_MRIQ_P > 0; tools/exp_mriq_mix.py, ncu in
+// tools/ncu_mriq_mix.sh): in every group of KL_MRIQ_G k-points the last KL_MRIQ_P take sin/cos
+// from FMA-pipe polynomials (sincos_2pi_poly, ~22 issue slots, no MUFU; staged in revolutions).
+// Solo, P/G = 1/8 is fastest (1.97 -> 1.82 ms plain grid, 1.98 -> 1.90 ms persistent; at 1/4 the
+// XU pipe drops to 71 % but MIO-throttle / not-selected stalls keep the time), but the extra
+// issue slots belong to the co-scheduled partner in a Kernelet phase: the model-guided step did
+// not get faster (device 10.56-10.93 ms vs 10.41-10.68 ms MUFU-only, same profile), and
+// a launch-mode switch (MUFU-only when co-scheduled) would make a co-scheduled MRIQ's result
+// depend on its schedule, breaking sliced == unsliced bit-identity.  So P = 0.
 #ifndef KL_MRIQ_G
 #define KL_MRIQ_G 8
 #endif
 #ifndef KL_MRIQ_P
-#define KL_MRIQ_P 1
+#define KL_MRIQ_P 0
 #endif
 // sin(2 pi t), cos(2 pi t) on the FMA pipe: r = t - rint(t) in [-1/2, 1/2] (rint by the
 // 1.5*2^23 rounding trick, exact for |t| < 2^22), then sin = r P(r^2) (degree 5 in r^2) and

@@ -9,7 +9,7 @@ if [ "${CALIB:-0}" = "1" ]; then
   grep -E " fit |wrote" gpurun_out/calib.log | cut -c1-160
   cp gpurun_out/kl_profile_b200.json profiles/kl_profile_b200.json
 fi
-if [ "${CALIB:-0}" = "1" ]; then
+if [ "${CALIB:-0}" = "1" ] || [ "${OPT:-0}" = "1" ]; then
   echo "== OPT pair table (measured co-runs)"; timeout 1200 python tools/opt_table.py gpurun_out/opt_table.json > gpurun_out/opt_table.log 2>&1
   cp gpurun_out/opt_table.json profiles/r01_opt_table.json
   python tools/pruning_study.py gpurun_out/pruning_b200.json > gpurun_out/pruning_b200.log 2>&1
@@ -40,6 +40,8 @@ done
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_model_batch -c 1 -o gpurun_out/prof_MODEL python tools/model_bench.py 1 > gpurun_out/ncu_full_MODEL.log 2>&1
 python tools/model_bench.py 20 > gpurun_out/model_bench.json
 python tools/ncu_summary.py gpurun_out/ncu_summary.json gpurun_out/prof_*.ncu-rep > /dev/null 2>&1
+# keep the dominant kernel's and the model's reports; the rest are summarised (gpurun_out merge cap)
+for k in MM ST PC BS TEA SAD SPMV; do rm -f gpurun_out/prof_$k.ncu-rep; done
 echo "== MC(1000)"; timeout 900 python tools/mc_cdf.py 1000 gpurun_out/mc_cdf.json 2>&1 | tail -1 | cut -c1-400
 echo "== online"; timeout 900 python tools/online.py 320 gpurun_out/online.json 2>&1 | tail -3 | cut -c1-600
 echo "== f1 study"; timeout 600 python tools/model3_study.py gpurun_out/model3_study.json 2>&1 | tail -3
