@@ -115,13 +115,13 @@ def test_integer_modes_exact(ctx, kind, field):
 
 
 @pytest.mark.parametrize("num_k", [1, 7, 8, 9, 255, 256, 263, 2048])
-def test_mriq_mufu_polynomial_mix(ctx, num_k):
-    """MRIQ takes one sin/cos pair in eight (the last of every whole group of 8 k-points of a
-    256-point chunk) from FMA-pipe polynomials, the rest and the ragged tail from MUFU: every
-    group/tail boundary and the paper's numK against the oracle; the phase range reaches |k.x|
-    of ~48 revolutions (kx, ky, kz ~ U[-32, 32), x ~ U[-0.5, 0.5)).  Below 64 k-points the
-    normwise bound has no averaging to lean on, and the fp32 phase t = k.x itself is off by up to
-    ulp(|t|) (~2e-5 rad at 300 rad) on either path, so those cases draw k from U[-4, 4)."""
+def test_mriq_num_k_edges(ctx, num_k):
+    """MRIQ's k loop: 256-point staging chunks, unrolled groups of KL_MRIQ_G = 8 (of which the last
+    KL_MRIQ_P use the FMA-pipe polynomials in the experimental builds) and ragged tails, against
+    the oracle; the phase range reaches |k.x| of ~48 revolutions (kx, ky, kz ~ U[-32, 32),
+    x ~ U[-0.5, 0.5)).  Below 64 k-points the normwise bound has no averaging to lean on, and the
+    fp32 phase t = k.x itself is off by up to ulp(|t|) (~2e-5 rad at 300 rad), so those cases draw
+    k from U[-4, 4)."""
     d = G.gen("MRIQ", dict(num_x=777, num_k=num_k))
     if num_k < 64:
         for f in ("kx", "ky", "kz"):
@@ -131,8 +131,8 @@ def test_mriq_mufu_polynomial_mix(ctx, num_k):
 
 
 def test_mriq_zero_k_closed_form(ctx):
-    """k = 0 for every k-point: cos = 1 and sin = 0 exactly on both paths, so Qr = sum phiMag
-    and Qi = 0 (the oracle's closed-form pin), bit-exact in fp32 with 16 = 2 groups."""
+    """k = 0 for every k-point: cos = 1 and sin = 0 exactly, so Qr = sum phiMag and Qi = 0 (the
+    oracle's closed-form pin), bit-exact in fp32 (fmaf(phi, 1, q) = phi + q)."""
     d = G.gen("MRIQ", dict(num_x=300, num_k=16))
     for f in ("kx", "ky", "kz"):
         d[f][:] = 0
