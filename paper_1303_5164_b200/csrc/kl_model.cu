@@ -87,6 +87,35 @@ __device__ double block_sum(double v, double* red) {
 // L > W, R22) / KL_ENUMERIC (zero pivot: reducible chain).
 struct ChainOut { double ipc_a, ipc_b; };
 
+constexpr int kT = kMaxS / 16 + 1;      // GTH register tile: 6 x 6 doubles per thread
+
+// Publish row k (held in register row M of the owning half-warp): entries j < k to the row
+// buffer; returns this thread's part of the pivot sum.  Static M: registers, no local memory.
+template <int M>
+__device__ __forceinline__ double publish_row(const double (&a)[kT][kT], double* row, int k, int tx) {
+    double part = 0.0;
+#pragma unroll
+    for (int n = 0; n < kT; ++n) {
+        const int j = tx + 16 * n;
+        const double v = j < k ? a[M][n] : 0.0;
+        row[j] = v;
+        part += v;
+    }
+    return part;
+}
+
+// Publish column k (register column N of the owning threads), rows i < k, into the back-
+// substitution store P[i][k].
+template <int N>
+__device__ __forceinline__ void publish_col(const double (&a)[kT][kT], double* P, int S, int k, int ty) {
+#pragma unroll
+    for (int m = 0; m < kT; ++m) {
+        const int i = ty + 16 * m;
+        if (i < k) P[i * S + k] = a[m][N];
+    }
+}
+
+
 __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, int wb, const KlModelCfg& c,
                          double* P, double* pi, double* Rs, double* red, const double (*binom)[kMaxW + 1],
                          ChainOut* out) {
@@ -132,7 +161,6 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
     // substitution applies 1/s_k and reads exactly these columns), one barrier, then every thread
     // applies the rank-1 update to its registers.  Shared memory carries 2 S values per state
     // instead of the whole k x k update.
-    constexpr int kT = kMaxS / 16 + 1;      // 6 x 6 register tile per thread
     __shared__ double s_row[2][16 * kT];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double a[kT][kT];
@@ -149,35 +177,35 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
         if ((ty >> 1) == ((k & 15) >> 1)) {   // the warp holding row k (in one of its halves):
             double part = 0.0;                   // publish the row and its pivot sum
             const bool own = ty == (k & 15);
-#pragma unroll
-            for (int m = 0; m < kT; ++m)
-                if (own && m == mk) {
-#pragma unroll
-                    for (int n = 0; n < kT; ++n) {
-                        const int j = tx + 16 * n;
-                        const double v = j < k ? a[m][n] : 0.0;
-                        s_row[buf][j] = v;
-                        part += v;
-                    }
+            if (own) {
+                double* row = s_row[buf];
+                switch (mk) {
+                    case 0: part = publish_row<0>(a, row, k, tx); break;
+                    case 1: part = publish_row<1>(a, row, k, tx); break;
+                    case 2: part = publish_row<2>(a, row, k, tx); break;
+                    case 3: part = publish_row<3>(a, row, k, tx); break;
+                    case 4: part = publish_row<4>(a, row, k, tx); break;
+                    default: part = publish_row<5>(a, row, k, tx); break;
                 }
+            }
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
             if (own && tx == 0) {
+                const double inv = 1.0 / part;
                 s_piv[buf] = part;
-                s_inv[buf] = 1.0 / part;
-                inv_s[k] = 1.0 / part;
+                s_inv[buf] = inv;
+                inv_s[k] = inv;
             }
         }
         if (tx == (k & 15)) {   // threads owning column k: publish it (rows i < k)
-#pragma unroll
-            for (int n = 0; n < kT; ++n)
-                if (n == mk) {
-#pragma unroll
-                    for (int m = 0; m < kT; ++m) {
-                        const int i = ty + 16 * m;
-                        if (i < k) P[i * S + k] = a[m][n];
-                    }
-                }
+            switch (mk) {
+                case 0: publish_col<0>(a, P, S, k, ty); break;
+                case 1: publish_col<1>(a, P, S, k, ty); break;
+                case 2: publish_col<2>(a, P, S, k, ty); break;
+                case 3: publish_col<3>(a, P, S, k, ty); break;
+                case 4: publish_col<4>(a, P, S, k, ty); break;
+                default: publish_col<5>(a, P, S, k, ty); break;
+            }
         }
         __syncthreads();
         if (!(s_piv[buf] > 0.0)) return KL_ENUMERIC;   // uniform across the block
@@ -185,13 +213,18 @@ __device__ int chain_ipc(const KlModelKind* ka, int wa, const KlModelKind* kb, i
         double rk[kT];
 #pragma unroll
         for (int n = 0; n < kT; ++n) rk[n] = s_row[buf][tx + 16 * n];   // 0 beyond k
+        // rank-1 update over the 16-blocks that hold indices < k (block-uniform bounds: entries
+        // of eliminated rows / columns in the last block are dead and may take any update; rows
+        // i >= k get c = 0)
+        const int kb = (k - 1) >> 4;
 #pragma unroll
         for (int m = 0; m < kT; ++m) {
-            const int i = ty + 16 * m;
-            if (i < k) {
-                const double c = P[i * S + k] * inv;
+            if (m <= kb) {
+                const int i = ty + 16 * m;
+                const double c = i < k ? P[i * S + k] * inv : 0.0;
 #pragma unroll
-                for (int n = 0; n < kT; ++n) a[m][n] = fma(c, rk[n], a[m][n]);
+                for (int n = 0; n < kT; ++n)
+                    if (n <= kb) a[m][n] = fma(c, rk[n], a[m][n]);
             }
         }
     }
