@@ -85,6 +85,18 @@ def test_mixed_queue_parity(seed):
     for i in insts:
         compare(i.kind, i.result(), refs[i.kind])
     _check_trace(ctx, ids, insts)
+    # slicing and co-scheduling are semantically transparent: every kernel's result
+    # is bit-identical to its unsliced plain-grid run on the GPU, fp32 kinds included
+    for k in kinds:
+        plain = Instance(ds[k], "cuda", inputs=shared[k])
+        ctx.run_plain(k, plain.grid, plain.args, 0)
+        torch.cuda.synchronize()
+        want = plain.result()
+        for i in insts:
+            if i.kind == k:
+                got = i.result()
+                for f in want:
+                    assert np.array_equal(np.asarray(got[f]), np.asarray(want[f])), (k, f)
     ctx.close()
 
 
