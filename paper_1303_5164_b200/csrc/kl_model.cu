@@ -289,28 +289,28 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     double* red = Rs + kMaxS;              // 16
     __shared__ double s_binom[kMaxW + 1][kMaxW + 1];
     __shared__ KlCand s_cd;
-    __shared__ KlModelKind s_k[2];
+    __shared__ KlModelKind s_kall[KL_NKINDS];
     const int n = cfg.n_cand;
     const bool solo_cta = (int)blockIdx.x >= n;
     for (int x = threadIdx.x; x < (kMaxW + 1) * (kMaxW + 1); x += kThreads)
         s_binom[x / (kMaxW + 1)][x % (kMaxW + 1)] = c_binom[x / (kMaxW + 1)][x % (kMaxW + 1)];
-    if (threadIdx.x == 0) {   // one reader of the host-mapped inputs, broadcast through smem
-        if (solo_cta) {
-            s_k[0] = kinds[blockIdx.x - n];
-        } else {
-            const KlCand cd = cands[blockIdx.x];
-            s_cd = cd;
-            s_k[0] = kinds[cd.k1];
-            s_k[1] = kinds[cd.k2];
-        }
-    }
+    // the host-mapped inputs in ONE PCIe round trip: the kind table as 8-byte words, one per
+    // thread, and this CTA's candidate by another warp, in parallel (a dependent cand -> kinds
+    // read by one thread held the whole CTA at this barrier for ~20 % of the batch's warp time)
+    static_assert(sizeof(KlModelKind) % 8 == 0, "kind table copied as 8-byte words");
+    constexpr int kKindWords = KL_NKINDS * (int)sizeof(KlModelKind) / 8;
+    static_assert(kKindWords < kThreads - 32, "kind table fits the first warps");
+    if ((int)threadIdx.x < kKindWords)
+        reinterpret_cast<unsigned long long*>(s_kall)[threadIdx.x] =
+            reinterpret_cast<const unsigned long long*>(kinds)[threadIdx.x];
+    if (threadIdx.x == kThreads - 1 && !solo_cta) s_cd = cands[blockIdx.x];
     __syncthreads();
 #ifdef KL_MODEL_PROFILE
     unsigned long long tp0 = gtimer_m();
 #endif
     ChainOut co;
     if (solo_cta) {
-        const KlModelKind k1 = s_k[0];
+        const KlModelKind k1 = s_kall[blockIdx.x - n];
         const int ts = k1.bsolo * k1.wpb, ws = ts / cfg.n_sched;
         int status = (ts % cfg.n_sched || ws < 1 || ws > cfg.W || cfg.W > kMaxW) ? KL_EINFEASIBLE : 0;
         if (status == 0) {
@@ -325,7 +325,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
         }
     } else {
         const KlCand cd = s_cd;
-        const KlModelKind k1 = s_k[0], k2 = s_k[1];
+        const KlModelKind k1 = s_kall[cd.k1], k2 = s_kall[cd.k2];
         kl_prediction out = {};
         int status = 0;
         const int t1 = (int)cd.b1 * k1.wpb, t2 = (int)cd.b2 * k2.wpb;
@@ -372,8 +372,8 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
                 o.solo2 = s2.solo1;
                 if (o.status == 0 && cd.b2 != 0) {
                     o.cp = 1.0 - 1.0 / (o.ipc1 / o.solo1 + o.ipc2 / o.solo2);   // Eq.1
-                    o.dT = fabs(kinds[cd.k1].ipb * (double)cd.b1 / o.ipc1 -
-                                kinds[cd.k2].ipb * (double)cd.b2 / o.ipc2);      // Eq.8
+                    o.dT = fabs(s_kall[cd.k1].ipb * (double)cd.b1 / o.ipc1 -
+                                s_kall[cd.k2].ipb * (double)cd.b2 / o.ipc2);      // Eq.8
                 }
             }
         }
@@ -383,7 +383,7 @@ k_model_batch(const KlModelKind* __restrict__ kinds, const KlModelCfg cfg, const
     __threadfence();
     __syncthreads();
     if (n_pairs > 0) {
-        select_body<kThreads>(cfg, kinds, cl, preds, n_pairs, pair_off, done_counter, dec);
+        select_body<kThreads>(cfg, s_kall, cl, preds, n_pairs, pair_off, done_counter, dec);
     } else if (threadIdx.x == 0) {
         *done_counter = 0u;
     }
