@@ -346,7 +346,7 @@ def run_kernelet(args, rank, world, local_rank):
         with open(args.trace_out, "w") as f:
             for t in sorted(last, key=lambda t: t.t0_ns):
                 f.write(json.dumps({"kind": K.KINDS[t.kind], "cap": t.cap, "cap_max": t.cap_max, "grids": t.grids,
-                                    "start": t.start, "end": t.end, "exh": t.exhausted, "adm": t.admitted,
+                                    "start": t.start, "end": t.end, "exh": t.exhausted, "adm": t.admitted, "mx": t.max_per_sm,
                                     "t0_us": round((t.t0_ns - z) / 1e3, 1), "t1_us": round((t.t1_ns - z) / 1e3, 1),
                                     "partner": K.KINDS[t.partner_kind] if t.partner_kind >= 0 else None,
                                     "cp": round(t.cp, 3), "dec": t.phase}) + "\n")

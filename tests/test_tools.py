@@ -19,3 +19,26 @@ def test_progress_rate_of_uniform_stream():
     tl = np.stack([s, s + 10], axis=1)
     for t0, t1 in ((1000, 3000), (1234, 8765)):
         assert abs(progress(tl, t0, t1) / (t1 - t0) - 0.1) < 1e-9
+
+
+def test_slice_report_rates_and_residency(tmp_path):
+    """tools/slice_report.py: per-slice algorithmic rate = work per virtual block x executed
+    blocks / resident interval; residency checked against the admission cap; aggregate HBM
+    timeline sums concurrent slices."""
+    import json
+    import kl_inputs as G
+    from tools import slice_report as SR
+    p = dict(G.PAPER["PC"])
+    g = G.grid_blocks("PC", p)
+    recs = [{"kind": "PC", "cap": 4, "cap_max": 4, "start": 0, "end": g, "exh": 1, "adm": 592, "mx": 4,
+             "t0_us": 0.0, "t1_us": 500.0, "partner": "MRIQ", "cp": 0.2, "dec": 1},
+            {"kind": "MRIQ", "cap": 4, "cap_max": 4, "start": 0, "end": 100, "exh": 0, "adm": 592, "mx": 5,
+             "t0_us": 0.0, "t1_us": 500.0, "partner": "PC", "cp": 0.2, "dec": 1}]
+    f = tmp_path / "t.jsonl"
+    f.write_text("\n".join(json.dumps(r) for r in recs) + "\n")
+    r = SR.main(str(f), None, 1965.0)
+    pc = next(s for s in r["slices"] if s["kind"] == "PC")
+    want = p["n_threads"] * (p["hops"] * 64 + 8) / 500e-6 / 1e9      # whole PC in 500 us
+    assert abs(pc["hbm_GBps"] - want) < 1e-6 * want
+    assert r["residency_checked"] == 2 and r["residency_reaches_cap"] == 1 and r["residency_above_cap"] == 1
+    assert r["aggregate"]["peak_bin_hbm_GBps"] >= pc["hbm_GBps"]
