@@ -137,22 +137,33 @@ struct BodySAD {
     }
 };
 
-// SPMV (CUSP CSR-vector): one warp per row, 8 rows per block, butterfly reduction.
+// SPMV (CUSP CSR-vector): 8 rows per block, the paper's unit of work.
+#ifndef KL_SPMV_LANES
+#define KL_SPMV_LANES 32
+#endif
+// KL_SPMV_LANES lanes per row (rows hold 8-24 nonzeros), lane-strided products, butterfly
+// reduction inside the row's lane group.  At this size the kernel is latency-bound (row pointer
+// -> column -> x gather -> reduce per row), so rows in flight is what counts for a plain grid:
+// 8 lanes per row (2-warp blocks, 32 blocks = 256 rows per SM) take it 28.4 -> 22.7 us, but
+// through the persistent launcher 38 -> 43 us -- twice the blocks means twice the epoch joins
+// and fetches on the kernel's control words -- so the product keeps a warp per row.
 struct BodySPMV {
     using Params = kl_args_spmv;
     using State = Empty;
-    static constexpr int kThreads = 256, kChunk = 8, kDynSmem = 0, kMinBlocks = 8;
+    static constexpr int kLanes = KL_SPMV_LANES;
+    static_assert(kLanes == 8 || kLanes == 16 || kLanes == 32, "lanes per row");
+    static constexpr int kThreads = 8 * kLanes, kChunk = 8, kDynSmem = 0, kMinBlocks = 2048 / kThreads > 32 ? 32 : 2048 / kThreads;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        const int row = (int)vb * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-        if (row >= a.n_rows) return;
-        const int s = __ldg(a.rowptr + row), e = __ldg(a.rowptr + row + 1);
+        const int row = (int)vb * 8 + (int)(threadIdx.x / kLanes), lane = threadIdx.x % kLanes;
+        const bool live = row < a.n_rows;   // no early return: the whole warp takes the shuffles
+        const int s = live ? __ldg(a.rowptr + row) : 0, e = live ? __ldg(a.rowptr + row + 1) : 0;
         float sum = 0.f;
-        for (int j = s + lane; j < e; j += 32) sum = fmaf(__ldg(a.vals + j), __ldg(a.x + __ldg(a.cols + j)), sum);
+        for (int j = s + lane; j < e; j += kLanes) sum = fmaf(__ldg(a.vals + j), __ldg(a.x + __ldg(a.cols + j)), sum);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (lane == 0) a.y[row] = sum;
+        for (int o = kLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (live && lane == 0) a.y[row] = sum;
     }
 };
 
