@@ -4,6 +4,8 @@ C1 (BASELINE.json configs[0]): PC + BS, 64 blocks each, exhaustive model search;
 queues of every kind; the stop-at-slice-boundary protocol under stress.  Checks: outputs vs the
 oracle, coverage audit (every block exactly once), contiguous slice ranges per kernel,
 per-SM residency never above the admission cap, device counters."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -222,3 +224,21 @@ def test_block_timeline():
         assert min(t.t0_ns for t in recs) <= tl[:, 0].min()
         assert max(t.t1_ns for t in recs) >= tl[:, 1].max()
     ctx.close()
+
+
+def test_compute_sanitizer_memcheck_clean():
+    """Race / memory checking: compute-sanitizer memcheck over the slice launcher,
+    explicit slicing, a co-scheduled queue and a model batch finds no error (the full
+    memcheck + racecheck + synccheck sweep over every kind is tools/sanitize.sh)."""
+    import shutil
+    import subprocess
+    import sys
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([exe, "--tool", "memcheck", sys.executable, os.path.join(root, "tools", "sanitize_target.py"),
+                        "PC,SPMV,MM,BS"], capture_output=True, text=True, timeout=600, cwd=root)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-2000:]
+    assert "ERROR SUMMARY: 0 errors" in out and "audit ok" in out, out[-2000:]
