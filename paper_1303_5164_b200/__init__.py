@@ -328,12 +328,21 @@ class Context:
         -> ids (one ABI call)."""
         n = len(items)
         arr = (KernelDesc * max(n, 1))()
+        addressof, sizeof = C.addressof, C.sizeof
+        # field-wise fill (addressof, no pointer objects): ~0.5 us per descriptor instead of ~5 us,
+        # which at 32 kernels per bench step was 1.5 % of the step in Python marshalling
         for i, it in enumerate(items):
             kind, grid, args, tag, ev = it[:5]
-            flag = it[5] if len(it) > 5 else None
-            kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
-            e = getattr(ev, "cuda_event", ev) if ev is not None else None
-            arr[i] = KernelDesc(kid, grid, C.cast(C.pointer(args), _vp), C.sizeof(args), None, tag, e, flag)
+            d = arr[i]
+            d.kind = KIND_ID[kind] if isinstance(kind, str) else int(kind)
+            d.grid_blocks = grid
+            d.args = addressof(args)
+            d.args_bytes = sizeof(args)
+            d.tag = tag
+            if ev is not None:
+                d.ready_event = getattr(ev, "cuda_event", ev)
+            if len(it) > 5 and it[5] is not None:
+                d.ready_flag = it[5]
         ids = (C.c_uint64 * max(n, 1))()
         self._check(self._L.kl_submit_batch(self._h, arr, n, ids))
         out = list(ids)[:n]
