@@ -275,12 +275,13 @@ def run_kernelet(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126.5 MiB)
     gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev)
 
+    counters[5] = rank      # kl_counters.rank / .world: the per-step reset clears fields 0-4 only
+    counters[6] = world
+
     def one_step():
         if not args.opt:
             ctx.reset_model_cache()
         ctx.reset_counters()
-        counters[5] = rank
-        counters[6] = world
         ids = ctx.submit_many([(i.kind, i.grid, i.args, n + 1, None) for n, i in enumerate(insts)])
         c = ctx.sync()
         if world > 1:
