@@ -705,8 +705,12 @@ def main():
             units = w.get("ops") if solo["bound"] == "alu" else (w.get("flops") if solo["bound"] == "tensor" else w.get("bytes"))
             scale = {"alu": 1e12, "tensor": 1e12, "hbm": 1e9}[solo["bound"]]
             ach = units * tk["blocks"] / w["grid"] / (tk["busy_ms"] / 1e3) / scale
+            tr = ncu_traffic(dom)
             roof = {"bound": solo["bound"], "achieved": ach, "peak": solo["peak"], "unit": solo["unit"],
-                    "frac": ach / solo["peak"], "traffic": ncu_traffic(dom), "kernel": dom,
+                    "frac": ach / solo["peak"], "traffic": tr["bytes_per_instance"] if tr else None,
+                    "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture "
+                                       f"of the kind's whole-instance persistent launch ({tr['source']})") if tr else None,
+                    "kernel": dom,
                     "measured": "timed region: algorithmic units of the kind's executed blocks / union of its "
                                 "launches' resident intervals (device %globaltimer records)",
                     "solo": {"achieved": solo["achieved"], "frac": solo["frac"], "ms": solo["ms"]},
