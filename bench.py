@@ -62,6 +62,9 @@ def parse():
                     help="pruning thresholds alpha_p alpha_m (default: the profile JSON's, else the paper's 0.4 0.1)")
     ap.add_argument("--age-limit-us", type=int, default=None,
                     help="starvation guard (kl_config.age_limit_us; default 0 = the paper's greedy)")
+    ap.add_argument("--levels", default="four", choices=["all", "four"],
+                    help="occupancy levels per kernel (kl_config.level_mode): every b with whole warps per virtual "
+                         "SM, or the four levels {1/4, 1/2, 3/4, 1} x b_max of config C2")
     ap.add_argument("--speculative", action="store_true", help="enable the speculative start (kl_config.speculative)")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
@@ -258,6 +261,7 @@ def run_kernelet(args, rank, world, local_rank):
     lane_b = torch.cuda.Stream(device=dev)
     cfg = dict(kcfg)
     cfg["split_rule"] = args.split_rule
+    cfg["level_mode"] = 1 if args.levels == "four" else 0
     if args.alpha:
         cfg["alpha_p"], cfg["alpha_m"] = args.alpha
     if args.speculative:
@@ -643,7 +647,9 @@ def main():
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
-              "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model"}
+              "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
+              "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
+              else "every b with whole warps per virtual SM"}
 
     if args.impl == "reference":
         if rank != 0:
