@@ -26,7 +26,11 @@
 namespace {
 
 constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int kStages = 4;
+#ifndef KL_MM_STAGES
+#define KL_MM_STAGES 4   // the stage count is a build knob: 2-4 (48 KiB of shared memory each)
+#endif
+constexpr int kStages = KL_MM_STAGES;
+static_assert(kStages >= 2 && kStages <= 4, "KL_MM_STAGES in [2, 4] (227 KB of shared memory per block)");
 constexpr int kStageBytes = (BM + BN) * BK * 2;          // 48 KiB
 constexpr int kBarOffset = kStages * kStageBytes;
 constexpr int kDynSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
