@@ -498,6 +498,15 @@ def per_kernel(ctx, insts, data, dev, flush, barrier) -> dict:
     return out
 
 
+def johnson_order(jobs, a, b):
+    """Johnson's rule for a two-machine flow shop (machine 1 = the H2D copy stream, machine 2 = the
+    GPU's kernels): jobs with a < b first by increasing a, then the rest by decreasing b; minimises
+    the makespan of the two-stage pipeline."""
+    first = sorted((j for j in jobs if a[j] < b[j]), key=lambda j: a[j])
+    rest = sorted((j for j in jobs if a[j] >= b[j]), key=lambda j: -b[j])
+    return first + rest
+
+
 def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b, pk=None) -> dict:
     """Same metric through the public API with HOST buffers: every step copies the step's inputs
     (one set per kind, shared by its instances) from pinned host memory and reads the completion
@@ -517,11 +526,8 @@ def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b, pk=None
         nk = {k: sum(1 for i in insts if i.kind == k) for k in kinds_in_order}
         nbytes = {k: sum(t.numel() * t.element_size() for t in next(i for i in insts if i.kind == k).inputs.values())
                   for k in kinds_in_order}
-        a = {k: nbytes[k] / 55e9 * 1e3 for k in kinds_in_order}          # copy ms
-        b = {k: pk[k]["ms"] * nk[k] for k in kinds_in_order}              # kernel ms
-        first = sorted((k for k in kinds_in_order if a[k] < b[k]), key=lambda k: a[k])
-        rest = sorted((k for k in kinds_in_order if a[k] >= b[k]), key=lambda k: -b[k])
-        kinds_in_order = first + rest
+        kinds_in_order = johnson_order(kinds_in_order, {k: nbytes[k] / 55e9 * 1e3 for k in kinds_in_order},
+                                       {k: pk[k]["ms"] * nk[k] for k in kinds_in_order})
     host = {}
     for k in kinds_in_order:
         src = next(i for i in insts if i.kind == k)

@@ -42,3 +42,26 @@ def test_slice_report_rates_and_residency(tmp_path):
     assert abs(pc["hbm_GBps"] - want) < 1e-6 * want
     assert r["residency_checked"] == 2 and r["residency_reaches_cap"] == 1 and r["residency_above_cap"] == 1
     assert r["aggregate"]["peak_bin_hbm_GBps"] >= pc["hbm_GBps"]
+
+
+def test_johnson_order_minimises_two_stage_makespan():
+    """bench.johnson_order (e2e copy order): on random two-machine flow shops its makespan equals
+    the brute-force minimum over all job orders (Johnson 1954)."""
+    import itertools
+    import random
+    import bench
+
+    def makespan(order, a, b):
+        t1 = t2 = 0.0
+        for j in order:
+            t1 += a[j]
+            t2 = max(t2, t1) + b[j]
+        return t2
+
+    rng = random.Random(7)
+    for _ in range(200):
+        jobs = list(range(6))
+        a = {j: rng.uniform(0.1, 10) for j in jobs}
+        b = {j: rng.uniform(0.1, 10) for j in jobs}
+        best = min(makespan(p, a, b) for p in itertools.permutations(jobs))
+        assert abs(makespan(bench.johnson_order(jobs, a, b), a, b) - best) < 1e-9
