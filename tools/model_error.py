@@ -11,6 +11,8 @@ and measured CP = 1 - 1/(sum cIPC_k / IPC_k^solo) with the solo IPC measured at 
 progress is counted inside the window where both are resident (tools/corun.py, per-block device
 timestamps), so neither the ramp-up nor the survivor's solo tail enters the co-run rates.  Reports the paper's metric, the average absolute IPC error per virtual SM
 (0.08 on C2050), and the CP error.
+KL_C3_SYNTH=1 adds the synthetic streaming kernel (4 FMAs per element), i.e. config C3's
+tensor-core MM vs streaming pair among 8 more.
 usage: python tools/model_error.py [out.json]"""
 import itertools
 import json
@@ -28,7 +30,7 @@ import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
 from tools.corun import corun, solo_rate  # noqa: E402
 
-KINDS = G.MIXES["ALL"]
+KINDS = G.MIXES["ALL"] + (["SYNTH"] if os.environ.get("KL_C3_SYNTH") else [])   # C3: + the streaming kernel
 
 
 def fits(p1, b1, p2, b2, sm):
