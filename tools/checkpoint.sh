@@ -1,6 +1,9 @@
 #!/bin/bash
 # Refresh every measured artefact on the GPU box (run under gpurun from the repo root).
 # Outputs land in gpurun_out/ (copied into profiles/ by hand after review).
+# CALIB=1: recalibrate the profile and re-measure the OPT pair table; OPT=1: the OPT table only;
+# EXTRA=1: also the slice report, C5 on one GPU, C3 with the streaming kernel, ncu range replay,
+# compute-sanitizer.
 set -u
 mkdir -p gpurun_out
 echo "== gpu tests"; timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
@@ -47,4 +50,13 @@ echo "== online"; timeout 900 python tools/online.py 320 gpurun_out/online.json 
 echo "== f1 study"; timeout 600 python tools/model3_study.py gpurun_out/model3_study.json 2>&1 | tail -3
 echo "== model bench"; python tools/model_bench.py 20
 echo "== launcher overhead"; python tools/launcher_overhead.py > gpurun_out/launcher_overhead.txt 2>&1; cat gpurun_out/launcher_overhead.txt
+if [ "${EXTRA:-0}" = "1" ]; then
+  echo "== slice report"; timeout 600 python bench.py --no-cpu --no-baselines --steps 5 --trace-out gpurun_out/step_trace.jsonl --json-out gpurun_out/bench_trace.json > /dev/null 2>&1
+  python tools/slice_report.py gpurun_out/step_trace.jsonl gpurun_out/slices.json > gpurun_out/slices.txt 2>&1; head -20 gpurun_out/slices.txt
+  echo "== C5 on one GPU"; timeout 1200 python bench.py --workload c5 --steps 2 --warmup 1 --no-cpu --json-out gpurun_out/bench_c5.json > gpurun_out/bench_c5.log 2>&1
+  python -c "import json;d=json.load(open('gpurun_out/bench_c5.json'));print(d['value'], d['ms_per_step'], d['speedup_vs_sequential'])"
+  echo "== C3 with the streaming kernel"; KL_C3_SYNTH=1 timeout 1200 python tools/model_error.py gpurun_out/model_error_synth.json > gpurun_out/model_error_synth.log 2>&1
+  echo "== ncu range replay"; bash tools/ncu_range.sh
+  echo "== sanitizers"; bash tools/sanitize.sh
+fi
 echo "== done"; ls gpurun_out
