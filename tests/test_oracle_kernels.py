@@ -161,6 +161,33 @@ def test_bs_cnd_and_parity():
     assert np.allclose(r2["call"], 30.0 - math.exp(-0.02 * 0.25), rtol=1e-6)
 
 
+def test_bs_textbook_value():
+    """Pins d1 = (ln(S/X) + (R + V^2/2) T) / (V sqrt T) and d2 = d1 - V sqrt T through a printed
+    textbook example (tests/golden/bs_textbook.txt): put-call parity holds for any d1/d2 and the
+    deep-in-the-money case saturates CND, so only printed prices catch a wrong drift or V sqrt T.
+    The A&S CND error (< 7.5e-8) is far below the printed rounding (0.005)."""
+    f = open(__file__.replace("test_oracle_kernels.py", "golden/bs_textbook.txt")).read().split("\n")
+    rows = [list(map(float, l.split())) for l in f if l.strip() and not l.startswith("#")]
+    for S, X, R, V, T, d1, d2, call, put in rows:
+        d = G.gen("BS", {"n": 2})
+        d["S"] = np.full(2, S, np.float32); d["X"] = np.full(2, X, np.float32); d["T"] = np.full(2, T, np.float32)
+        d["params"].update(R=R, V=V)
+        r = O.run_kernel(d)
+        assert np.all(np.abs(r["call"] - call) < 0.005), (r["call"], call)
+        assert np.all(np.abs(r["put"] - put) < 0.005), (r["put"], put)
+        # d1 and d2 separately: N(d1) = dC/dS and N(d2) = -e^{RT} dC/dX, by central differences
+        # of the oracle's own prices (fp32 inputs: steps large enough to be exactly representable)
+        h = 0.25
+        dd = G.gen("BS", {"n": 4})
+        dd["S"] = np.array([S + h, S - h, S, S], np.float32); dd["X"] = np.array([X, X, X + h, X - h], np.float32)
+        dd["T"] = np.full(4, T, np.float32); dd["params"].update(R=R, V=V)
+        c = O.run_kernel(dd)["call"].astype(np.float64)
+        n_d1 = (c[0] - c[1]) / (2 * h)
+        n_d2 = -(c[2] - c[3]) / (2 * h) * math.exp(R * T)
+        assert abs(n_d1 - 0.5 * math.erfc(-d1 / math.sqrt(2))) < 2e-3, n_d1
+        assert abs(n_d2 - 0.5 * math.erfc(-d2 / math.sqrt(2))) < 2e-3, n_d2
+
+
 def test_tea_known_answer_and_roundtrip():
     f = open(__file__.replace("test_oracle_kernels.py", "golden/tea_kat.txt")).read().split("\n")
     line = [l for l in f if l and not l.startswith("#")][0].split()

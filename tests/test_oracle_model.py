@@ -290,6 +290,63 @@ def test_pipe_ceiling_monte_carlo():
     assert abs(mc - model) <= 3.5 * sig + 1e-4, (mc, model, sig)
 
 
+def _simulate_pipes(ws, rms, rs, pis, pipes, cfg, rounds, seed):
+    """Per-warp Monte Carlo of the R26 round for two kernels written from the reading's prose
+    (R26), not from model.c: every ready warp issues once, so the round lasts at least
+    #ready cycles; a kernel on a pipe of ceiling pi needs ready_k/pi_k cycles of that pipe; pipes
+    are separate resources, so kernels on the same pipe queue behind each other (their pipe times
+    add) and kernels on different pipes overlap.  Returns per-kernel instructions/cycle and
+    batch-means sigmas."""
+    rng = np.random.default_rng(seed)
+    idle = [np.zeros(w, bool) for w in ws]
+    nb = 50
+    per = rounds // nb
+    inst_b, cyc_b = np.zeros((nb, len(ws))), np.zeros(nb)
+    for b in range(nb):
+        for _ in range(per):
+            nidle = [int(x.sum()) for x in idle]
+            ready = [w - n for w, n in zip(ws, nidle)]
+            busy = {}
+            for rk, pk, pp in zip(ready, pis, pipes):
+                busy[pp] = busy.get(pp, 0.0) + rk / pk      # cycles each pipe is busy this round
+            R = max([float(sum(ready)), 1.0] + list(busy.values()))
+            L = O.latency(cfg, sum(n * r for n, r in zip(nidle, rs)), sum(nidle))
+            pir = min(1.0, R / L)
+            for k in range(len(ws)):
+                u = rng.random(ws[k])
+                inst_b[b, k] += ready[k]
+                idle[k] = np.where(idle[k], u >= pir, u < rms[k])
+            cyc_b[b] += R
+    ipc = inst_b.sum(0) / cyc_b.sum()
+    sig = np.std(inst_b / cyc_b[:, None], axis=0, ddof=1) / math.sqrt(nb)
+    return ipc, sig
+
+
+@pytest.mark.parametrize("same_pipe", [False, True])
+def test_pipe_ceiling_two_kernels_monte_carlo(same_pipe):
+    """R26's joint round for two kernels with different ceilings, on different pipes (rounds
+    max(r1 + r2, r1/p1, r2/p2)) and on one shared pipe (max(r1 + r2, r1/p1 + r2/p2)): per-kernel
+    joint IPCs (Eq.5-6) against the simulated round process.  The ceilings are chosen so the pipe
+    term binds most rounds and the two rules differ by ~40 %, so confusing them, dropping a term
+    or swapping the kernels' ceilings fails."""
+    cfg = O.smcfg(L0=90.0, B=1.0, a0=1.0, W=16)
+    p1, p2 = 0.3, 0.5
+    k1 = O.kmodel(0.06, r=2.0, pi=p1, pipe=1)
+    k2 = O.kmodel(0.12, r=1.0, pi=p2, pipe=1 if same_pipe else 2)
+    w1, w2 = 6, 7
+    P, R = O.build_joint(k1, w1, k2, w2, cfg)
+    a, b, _ = O.ipc_joint(w1, w2, O.stationary(P), R)
+    mc, sig = _simulate_pipes([w1, w2], [0.06, 0.12], [2.0, 1.0], [p1, p2], [1, 1 if same_pipe else 2],
+                              cfg, 60000, seed=21 + same_pipe)
+    assert abs(mc[0] - a) <= 3.5 * sig[0] + 1e-4, (mc, a, b, sig)
+    assert abs(mc[1] - b) <= 3.5 * sig[1] + 1e-4, (mc, a, b, sig)
+    # the two readings are far apart at these parameters (the test can tell them apart)
+    k2o = O.kmodel(0.12, r=1.0, pi=p2, pipe=2 if same_pipe else 1)
+    Po, Ro = O.build_joint(k1, w1, k2o, w2, cfg)
+    ao, bo, _ = O.ipc_joint(w1, w2, O.stationary(Po), Ro)
+    assert abs(ao + bo - a - b) > 20 * (sig[0] + sig[1])
+
+
 def test_reducible_chain_rejected():
     """R22: Rm=1 with P_ir clamped to 1 makes the chain an involution; the guard L > W rejects."""
     with pytest.raises(ValueError):
