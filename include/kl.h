@@ -231,7 +231,11 @@ kl_status kl_create(int device, const kl_config* cfg, kl_ctx** out);
 kl_status kl_destroy(kl_ctx* ctx);
 const char* kl_last_error(const kl_ctx* ctx);
 
-/* Alg.1 lines 2-3: add kernel K to the pending set R; returns its id (>= 1). */
+/* Alg.1 lines 2-3: add kernel K to the pending set R; returns its id (>= 1).
+ * Errors: KL_EINVAL for an unknown kind, grid_blocks = 0 or >= 2^27, args_bytes != the kind's
+ * kl_args size, Rm outside [0,1] in an attached profile, args the kind cannot use (ST: nx not a
+ * multiple of 4; MM: M, N, K not multiples of the 128 x 256 x 64 tile, or grid_blocks larger
+ * than the (M/128)(N/256) output tiles -- every other body range-checks its virtual block). */
 kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* desc, uint64_t* out_id);
 /* kl_submit for n descriptors in order (one ABI crossing for a whole queue); out_ids[n] (may be
  * NULL).  Errors as kl_submit: the first failing descriptor's status is returned, the ones before

@@ -123,7 +123,10 @@ struct KlKindInfo {
 int kl_dev_kind_info(int kind, KlKindInfo* out);
 // Prepare per-instance device state (e.g. TMA descriptors for MM); `blob` receives up to
 // 512 bytes of launch-time parameter data stored with the instance.
-int kl_dev_prepare(int kind, const void* args, uint32_t args_bytes, void* blob, uint32_t blob_cap);
+// Validate and pack a kernel's args into its launch blob.  `grid` is the descriptor's grid_blocks:
+// kinds whose body indexes by the virtual block without a range guard (MM: one output tile per
+// block) reject a grid larger than their arguments imply.
+int kl_dev_prepare(int kind, const void* args, uint32_t args_bytes, uint32_t grid, void* blob, uint32_t blob_cap);
 // Launch the persistent slice launcher for `kind` with `grid` blocks.
 int kl_dev_launch_persistent(int kind, const void* blob, const KlLaunch& L, uint32_t grid,
                              void* stream);

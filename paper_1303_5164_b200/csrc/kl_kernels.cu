@@ -192,6 +192,7 @@ struct BodyST {
         if (y >= ny) return;                      // whole warp (one row per warp)
         const bool act = x0 < nx;
         const int z0 = bz * kTz, z1 = min(z0 + kTz, nz);
+        if (z0 >= nz) return;                     // a grid larger than the field: nothing to do
         const size_t sz = (size_t)nx * ny;
         const bool iy = y > 0 && y < ny - 1;
         const float* in = a.in;
@@ -418,6 +419,7 @@ struct BodyMATADD {
     __device__ static void fini(const Params&, State&, char*) {}
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
         const int g = a.n / 16, bx = vb % g, by = vb / g;
+        if (by >= g) return;                      // a grid larger than the matrix
         const int i = (by * 16 + (threadIdx.x >> 4)) * a.n + bx * 16 + (threadIdx.x & 15);
         a.C[i] = a.A[i] + a.B[i];
     }
@@ -459,7 +461,7 @@ struct BodySYNTH {
 
 // MM lives in kl_mm.cu (tcgen05); these are its entry points.
 int kl_mm_info(KlKindInfo* o);
-int kl_mm_prepare(const void* args, uint32_t bytes, void* blob, uint32_t cap);
+int kl_mm_prepare(const void* args, uint32_t bytes, uint32_t grid, void* blob, uint32_t cap);
 int kl_mm_launch_persistent(const void* blob, const KlLaunch& L, uint32_t grid, void* stream);
 int kl_mm_launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream);
 
@@ -497,9 +499,9 @@ int kl_dev_kind_info(int kind, KlKindInfo* out) {
     KL_DISPATCH(kind, info_of, out);
 }
 
-int kl_dev_prepare(int kind, const void* args, uint32_t bytes, void* blob, uint32_t cap) {
+int kl_dev_prepare(int kind, const void* args, uint32_t bytes, uint32_t grid, void* blob, uint32_t cap) {
     if (kind < 0 || kind >= KL_NKINDS || bytes != kArgBytes[kind]) return -1;
-    if (kind == KL_MM) return kl_mm_prepare(args, bytes, blob, cap);
+    if (kind == KL_MM) return kl_mm_prepare(args, bytes, grid, blob, cap);
     if (bytes > cap) return -1;
     if (kind == KL_ST && (reinterpret_cast<const kl_args_st*>(args)->nx % 4)) return -1;   // float4 rows
     std::memcpy(blob, args, bytes);

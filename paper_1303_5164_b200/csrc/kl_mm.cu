@@ -267,10 +267,11 @@ int kl_mm_info(KlKindInfo* o) {
     return 0;
 }
 
-int kl_mm_prepare(const void* args, uint32_t bytes, void* blob, uint32_t cap) {
+int kl_mm_prepare(const void* args, uint32_t bytes, uint32_t grid, void* blob, uint32_t cap) {
     if (bytes != sizeof(kl_args_mm) || cap < sizeof(MMParams)) return -1;
     const kl_args_mm& a = *reinterpret_cast<const kl_args_mm*>(args);
     if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.M % BM || a.N % BN || a.K % BK) return -1;
+    if ((uint64_t)grid > (uint64_t)(a.M / BM) * (uint64_t)(a.N / BN)) return -1;   // one tile per block
     MMParams p;
     std::memset(&p, 0, sizeof p);
     if (!encode_kmajor(&p.ta, a.A, (uint64_t)a.M, (uint64_t)a.K, BM)) return -1;

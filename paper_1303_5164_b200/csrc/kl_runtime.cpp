@@ -1236,7 +1236,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     k->ready = d->ready_event;
     k->ready_flag = d->ready_flag;
     if (!ctx->host_only) {
-        if (kl_dev_prepare(d->kind, d->args, d->args_bytes, k->blob, kBlob))
+        if (kl_dev_prepare(d->kind, d->args, d->args_bytes, d->grid_blocks, k->blob, kBlob))
             return ctx->fail(KL_EINVAL, "cannot prepare args of kind %d", d->kind);
         k->slot = ctx->free_slots.back();
         ctx->free_slots.pop_back();
@@ -1397,7 +1397,7 @@ kl_status kl_run_plain(kl_ctx* ctx, const kl_kernel_desc* d, void* stream, uint3
         return ctx->fail(KL_EINVAL, "bad descriptor");
     if ((uint64_t)off + n > d->grid_blocks) return ctx->fail(KL_EINVAL, "slice beyond grid");
     alignas(128) unsigned char blob[kBlob];
-    if (kl_dev_prepare(d->kind, d->args, d->args_bytes, blob, kBlob)) return ctx->fail(KL_EINVAL, "cannot prepare args");
+    if (kl_dev_prepare(d->kind, d->args, d->args_bytes, d->grid_blocks, blob, kBlob)) return ctx->fail(KL_EINVAL, "cannot prepare args");
     int rc = kl_dev_launch_plain(d->kind, blob, off, n, stream);
     if (rc) return ctx->fail(KL_ECUDA, "plain launch: %s", cudaGetErrorString((cudaError_t)rc));
     return KL_OK;

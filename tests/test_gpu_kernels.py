@@ -143,3 +143,102 @@ def test_mriq_zero_k_closed_form(ctx):
         acc = np.float32(acc + v)
     assert np.all(np.asarray(res["qi"]) == 0)
     assert np.all(np.asarray(res["qr"]) == acc)
+
+
+# ---- paths the SMALL sizes never reach -------------------------------------------------------
+# MM at SMALL is 3 output tiles with K/64 = 3 k-blocks: no CTA processes a second tile, the TMA
+# ring never wraps and the second TMEM accumulator is never used.  These sizes (P:1143's kernel,
+# shrunk so the plain-C oracle finishes in seconds) give 160 output tiles (> 148 SMs) and
+# K/64 = 8 k-blocks (> every ring depth), and the capped launches on a context restricted to a
+# few SMs make each persistent CTA loop over ~10 tiles (both accumulators, ring phase flips, the
+# overlapped epilogue of tile i-1 during tile i).
+MM_BIG = dict(M=2560, N=2048, K=512)
+
+
+@pytest.fixture(scope="module")
+def mm_big():
+    out = {}
+    for mode in ("int", "random"):
+        d = G.gen("MM", MM_BIG, mode=mode)
+        out[mode] = (d, O.run_kernel(d))
+    return out
+
+
+@pytest.mark.parametrize("mode", ["int", "random"])
+def test_mm_multi_tile_plain(ctx, mm_big, mode):
+    d, ref = mm_big[mode]
+    inst = Instance(d, "cuda")
+    res = _run_plain(ctx, inst)
+    if mode == "int":
+        assert np.array_equal(res["C"], ref["C"])           # every partial sum exact in fp32
+    else:
+        compare("MM", res, ref)
+
+
+@pytest.mark.parametrize("n_sms,cap", [(8, 1), (148, 1), (0, 0)])
+@pytest.mark.parametrize("mode", ["int", "random"])
+def test_mm_multi_tile_persistent(mm_big, mode, n_sms, cap):
+    """Persistent MM CTAs that each run many tiles: bit-exact (int) / normwise (random) against
+    the oracle on every element, and bit-identical to the one-tile-per-CTA plain grid."""
+    d, ref = mm_big[mode]
+    with K.Context(device=0, audit=1, **({"n_sms": n_sms} if n_sms else {})) as c:
+        inst = Instance(d, "cuda")
+        plain = _run_plain(c, inst)
+        for o in inst.outputs.values():
+            o.fill_(0)
+        torch.cuda.synchronize()
+        if cap:
+            c.run_capped("MM", inst.grid, inst.args, cap)
+        else:
+            kid = c.submit("MM", inst.grid, inst.args, tag=3)
+            c.sync()
+            assert np.all(c.audit(kid, inst.grid) == 1)
+        res = inst.result()
+    assert np.array_equal(res["C"], plain["C"])
+    if mode == "int":
+        assert np.array_equal(res["C"], ref["C"])
+    else:
+        compare("MM", res, ref)
+
+
+@pytest.mark.parametrize("nx", [260, 300, 388])
+def test_st_multi_x_tile(ctx, nx):
+    """ST with several 128-wide x tiles (SMALL has one): the tile-edge lanes load their x
+    neighbour from the adjacent tile (lane 0's x-1, lane 31's x+4), and the last tile is ragged
+    (260: one active lane; 300: 11; 388: 1 lane + a 3-tile row).  Integer Laplacian mode is
+    bit-exact; the Parboil constants within the normwise bound; sliced == unsliced."""
+    size = dict(nx=nx, ny=10, nz=40)
+    d = G.gen("ST", size, mode="int")
+    inst = Instance(d, "cuda", c0=6.0, c1=1.0)
+    res = _run_plain(ctx, inst)
+    assert np.array_equal(res["out"], O.run_kernel(d, c0=6.0, c1=1.0)["out"])
+    d = G.gen("ST", size)
+    inst = Instance(d, "cuda")
+    base = _run_plain(ctx, inst)
+    compare("ST", base, O.run_kernel(d))
+    sl = [(o, min(3, inst.grid - o)) for o in range(0, inst.grid, 3)][::-1]
+    assert np.array_equal(_run_plain(ctx, inst, sl)["out"], base["out"])
+
+
+def test_oversized_grid_rejected_or_guarded(ctx):
+    """A descriptor whose grid exceeds what its arguments imply must not touch memory outside
+    the buffers: MM (no per-block range guard) is rejected at submit; ST and MatrixAdd guard the
+    surplus blocks (outputs unchanged, nothing written past the end -- compute-sanitizer covers
+    the bodies in tools/sanitize.sh)."""
+    d = G.gen("MM", "small")
+    inst = Instance(d, "cuda")
+    with pytest.raises(K.KlError):
+        ctx.submit("MM", inst.grid + 1, inst.args)
+    for kind in ("ST", "MATADD"):
+        d = G.gen(kind, "small")
+        inst = Instance(d, "cuda")
+        base = _run_plain(ctx, inst)
+        guard = torch.full((1 << 20,), 7.0, device="cuda")     # the next allocation
+        for o in inst.outputs.values():
+            o.fill_(0)
+        ctx.run_plain(kind, inst.grid * 3, inst.args, 0)
+        torch.cuda.synchronize()
+        res = inst.result()
+        for f in base:
+            assert np.array_equal(res[f], base[f]), (kind, f)
+        assert bool((guard == 7.0).all())

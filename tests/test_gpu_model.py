@@ -116,3 +116,120 @@ def test_decisions_match_oracle():
         n_cmp += 1
         ctx.close()
     assert n_cmp == 12
+
+
+def _args_of(kind, keep={}):
+    """Descriptor args for decide-only submissions: zero structs, except MM, whose prepare step
+    encodes TMA descriptors and so needs a real (small) operand set."""
+    if kind != "MM":
+        return 1000, K.ARGS[K.KIND_ID[kind]]()
+    if "MM" not in keep:
+        import kl_inputs as G
+        from paper_1303_5164_b200.workload import Instance
+        keep["MM"] = Instance(G.gen("MM", "small"), "cuda")
+    return keep["MM"].grid, keep["MM"].args
+
+
+def _bench_profiles():
+    """The calibrated B200 profile and scheduler config the bench runs (bench.load_profiles)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kl_profile_b200.json")
+    d = json.load(open(path))
+    fields = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
+    profs = {k: {f: v[f] for f in fields if f in v} for k, v in d["profiles"].items()}
+    return profs, d.get("config", {})
+
+
+@pytest.mark.parametrize("split_rule", [1, 0])
+def test_decisions_match_oracle_bench_config(split_rule):
+    """The bench's decision configuration: calibrated profiles with the resource fields the
+    runtime reads from the compiled kernels (MM: TMEM- and shared-memory-bound, one block per SM),
+    the four C2 occupancy levels (level_mode = 1 <-> oracle mode "4"), alpha = 0 and both split
+    rules; queues drawn from the ALL mix always holding MM.  The oracle gets the runtime-resolved
+    profiles (kl_get_profile), so this compares the decision logic, not the profile plumbing."""
+    K.build()
+    profs, kcfg = _bench_profiles()
+    cfg = dict(kcfg)
+    cfg.update(split_rule=split_rule, level_mode=1)
+    rng = np.random.default_rng(23 + split_rule)
+    all_mix = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA"]
+    for rep in range(16):
+        ctx = K.Context(device=0, profiles=profs, **cfg)
+        resolved = {k: K.profile_dict(ctx.get_profile(k)) for k in all_mix}
+        assert resolved["MM"]["bmax"] == 1 and resolved["MM"]["tmem"] > 0
+        n = int(rng.integers(1, 9))
+        kinds = ["MM"] + [str(k) for k in rng.choice(all_mix, n)]
+        rng.shuffle(kinds)
+        pend = []
+        for k in kinds:
+            kid = ctx.submit(k, *_args_of(k))
+            pend.append({"kind": k, "blocks": 1000, "id": kid})
+        d1, d2 = _decide_both(ctx)
+        ocfg = O.smcfg(W=16, L0=kcfg["L0"], B=kcfg["B"], a0=kcfg.get("a0", 1.0), b0=kcfg.get("b0", 0.0))
+        ref = O.find_co_schedule(pend, resolved, ocfg, ap=ctx.config.alpha_p, am=ctx.config.alpha_m,
+                                 mode="4", cp_min=ctx.config.cp_min, split_rule=split_rule)
+        for d in (d1, d2):
+            assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref["solo"])
+            assert d.id1 == pend[ref["ia"]]["id"], (kinds, d.id1, ref)
+            if not ref["solo"]:
+                assert d.id2 == pend[ref["ib"]]["id"]
+                assert (d.b1, d.b2) == (ref["b1"], ref["b2"]), (kinds, d.b1, d.b2, ref["b1"], ref["b2"])
+                assert abs(d.cp - ref["cp"]) < 1e-9
+            else:
+                assert d.b1 == ref["b1"]
+        ctx.close()
+
+
+def test_opt_frozen_table_decisions():
+    """f2 OPT path: a prediction table installed with kl_cache_put and
+    model_frozen = 1 drives the decisions without the device model; they equal the oracle's
+    FindCoSchedule run on the same table (its `cache` argument), and a candidate without an
+    installed entry is never chosen (infeasible)."""
+    K.build()
+    profs, kcfg = _bench_profiles()
+    rng = np.random.default_rng(31)
+    all_mix = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA"]
+    for rep in range(8):
+        ctx = K.Context(device=0, profiles=profs, **dict(kcfg, model_frozen=1, split_rule=rep % 2, level_mode=1))
+        resolved = {k: K.profile_dict(ctx.get_profile(k)) for k in all_mix}
+        # a synthetic "measured" table: random CPs over every maximal split of every kind pair,
+        # with about a quarter of the candidates left out
+        table, items = {}, []
+        for i, a in enumerate(all_mix):
+            for b in all_mix[i:]:
+                for (b1, b2) in O.maximal_splits(O.B200_SM, resolved[a], resolved[b], 4, "4"):
+                    if rng.random() < 0.25:
+                        continue
+                    i1, i2 = float(rng.uniform(0.05, 0.9)), float(rng.uniform(0.05, 0.9))
+                    s1, s2 = float(rng.uniform(0.3, 1.0)), float(rng.uniform(0.3, 1.0))
+                    pr = dict(ipc1=i1, ipc2=i2, c=i1 + i2, solo1=s1, solo2=s2,
+                              cp=1.0 - 1.0 / (i1 / s1 + i2 / s2), dT=float(rng.uniform(0, 1e6)), status=0)
+                    table[(a, b, b1, b2)] = pr
+                    items.append(((a, b, b1, b2), pr))
+                    if a != b:   # the runtime looks the pair up in either order
+                        sw = dict(ipc1=i2, ipc2=i1, c=i1 + i2, solo1=s2, solo2=s1, cp=pr["cp"], dT=pr["dT"], status=0)
+                        table[(b, a, b2, b1)] = sw
+                        items.append(((b, a, b2, b1), sw))
+        ctx.cache_put(items)
+        kinds = [str(k) for k in rng.choice(all_mix, int(rng.integers(2, 9)))]
+        pend = []
+        for k in kinds:
+            pend.append({"kind": k, "blocks": 1000, "id": ctx.submit(k, *_args_of(k))})
+        d = ctx.decide()
+        # entries the table lacks are infeasible to both sides
+        cache = {key: table.get(key, dict(status=2, ipc1=0, ipc2=0, c=0, solo1=0, solo2=0, cp=0, dT=0))
+                 for a in all_mix for b in all_mix
+                 for (b1, b2) in O.maximal_splits(O.B200_SM, resolved[a], resolved[b], 4, "4")
+                 for key in [(a, b, b1, b2)]}
+        ocfg = O.smcfg(W=16, L0=kcfg["L0"], B=kcfg["B"], a0=kcfg.get("a0", 1.0), b0=kcfg.get("b0", 0.0))
+        ref = O.find_co_schedule(pend, resolved, ocfg, ap=ctx.config.alpha_p, am=ctx.config.alpha_m, mode="4",
+                                 cp_min=ctx.config.cp_min, split_rule=rep % 2, cache=cache)
+        assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref)
+        assert d.id1 == pend[ref["ia"]]["id"]
+        if not ref["solo"]:
+            assert d.id2 == pend[ref["ib"]]["id"]
+            assert (d.b1, d.b2) == (ref["b1"], ref["b2"])
+            assert abs(d.cp - table[(pend[ref["ia"]]["kind"], pend[ref["ib"]]["kind"], d.b1, d.b2)]["cp"]) < 1e-12
+        assert ctx.stats().model_batches == 0          # the device model never ran
+        ctx.close()
