@@ -39,16 +39,27 @@ ALL = G.MIXES["ALL"]
 METRIC = "kernel-queue throughput (kernels/s) & speedup vs sequential, 1/2/4/8 B200"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of this node; without WORLD_SIZE in the environment and N > 1, bench.py "
+                         "re-launches itself under torch.distributed.run with N ranks (default: WORLD_SIZE, else 1)")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="kernelet", choices=["kernelet", "reference"])
     ap.add_argument("--instances", type=int, default=4, help="instances of each ALL-mix kernel per GPU (c2)")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
-                    help="c2: ALL mix x4 per GPU (configs[1], default); c4: 1000 random kernels per GPU; "
-                         "c5: 10,000-kernel multi-user queue over all GPUs")
+    ap.add_argument("--workload", default="c5", choices=["c2", "c4", "c5"],
+                    help="c5: the 10,000-kernel multi-user queue shared by all GPUs (configs[4], the metric's "
+                         "1/2/4/8-GPU workload, strong scaling; default); c4: 1000 random kernels per GPU from "
+                         "--mix (configs[3]); c2: the ALL mix x --instances per GPU (configs[1])")
+    ap.add_argument("--mix", default="ALL", choices=["ALL", "CI", "MI", "MIX"],
+                    help="c4 only: the tb:workloads mix the 1000 kernels are drawn from (P:1193-1196)")
+    ap.add_argument("--pool", type=int, default=4,
+                    help="input/output sets per kind: instance j of a kind reads input set j %% pool and writes "
+                         "output set j %% pool (distinct device buffers)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional check of the multi-rank path, "
+                         "counters gathered through host memory)")
     ap.add_argument("--size", default="paper", choices=["paper", "small"])
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -69,7 +80,26 @@ def parse():
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_cmd(args, argv: list[str]) -> list[str] | None:
+    """The torch.distributed.run command that re-launches this script with args.gpus ranks, or None
+    when no spawn is needed (already under a launcher, N = 1, or the reference arm, which runs on
+    rank 0 only)."""
+    if "WORLD_SIZE" in os.environ or args.impl == "reference" or (args.gpus or 1) <= 1:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -79,7 +109,10 @@ def parse():
 def algorithmic_work(kind: str, p: dict) -> dict:
     if kind == "PC":      # one 64-B HBM3e access per random dependent load (nodes are visited
         # once: no reuse for L2) + 8 B of output per thread; ncu: 64 B DRAM read per hop
-        return {"bound": "hbm", "bytes": p["n_threads"] * (p["hops"] * 64 + 8)}
+        # (DESIGN reading R27: the HBM3e access atom is 64 B; SURVEY §8(d)'s 32-B-sector figure
+        # is reported beside it as bytes_32B)
+        return {"bound": "hbm", "bytes": p["n_threads"] * (p["hops"] * 64 + 8),
+                "bytes_32B": p["n_threads"] * (p["hops"] * 32 + 8)}
     if kind == "SAD":     # 4 pixel |diff|-accumulates per vabsdiff4; ALU-bound
         n_mb = (p["width"] // 16) * (p["height"] // 16)
         return {"bound": "alu", "ops": n_mb * 1089 * 256 / 4, "bytes": 2 * p["width"] * p["height"] + n_mb * 1089 * 2}
@@ -100,11 +133,21 @@ def algorithmic_work(kind: str, p: dict) -> dict:
     return {"bound": "hbm", "bytes": 0}
 
 
-def ncu_traffic(kind: str):
+_UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def _metric_bytes(m: dict) -> float:
+    """One ncu raw-page metric {"value": "1,234.5", "unit": "Mbyte"} in bytes (each metric carries
+    its own unit: ncu scales read and write bytes independently)."""
+    return float(str(m["value"]).replace(",", "")) * _UNIT[m.get("unit", "byte")]
+
+
+def ncu_traffic(kind: str, profiles_dir: str | None = None):
     """DRAM bytes (read + write) of one launch of `kind` from the committed `ncu --set full`
     summary (profiles/*ncu_summary.json, latest round), or None."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")), reverse=True):
+    pdir = profiles_dir or os.path.join(ROOT, "profiles")
+    for path in sorted(glob.glob(os.path.join(pdir, "r*_ncu_summary.json")), reverse=True):
         try:
             d = json.load(open(path))
         except Exception:
@@ -116,27 +159,45 @@ def ncu_traffic(kind: str):
                 if f"Body{kind}>" in r.get("kernel", "") or f"Body{kind}E" in r.get("kernel", "") or \
                         f"::Body{kind}" in r.get("kernel", ""):
                     try:
-                        rd = float(str(r["dram__bytes_read.sum"]["value"]).replace(",", ""))
-                        wr = float(str(r["dram__bytes_write.sum"]["value"]).replace(",", ""))
-                        unit = r["dram__bytes_read.sum"]["unit"]
-                        mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-                        return {"bytes_per_instance": (rd + wr) * mul, "source": os.path.basename(path)}
+                        rd = _metric_bytes(r["dram__bytes_read.sum"])
+                        wr = _metric_bytes(r["dram__bytes_write.sum"])
+                        return {"bytes_per_instance": rd + wr, "read": rd, "write": wr,
+                                "source": os.path.basename(path)}
                     except (KeyError, ValueError):
                         continue
     return None
 
 
+def pipe_peaks() -> dict:
+    """Builder-measured lane ops per SM clock (tools/pipe_peaks.cu -> profiles/r*_pipe_peaks.json,
+    latest round); the guide's nominal unit counts where a pipe was not measured."""
+    import glob
+    out = {"mufu_sincos": (16.0, "nominal"), "vabsdiff4": (64.0, "nominal"), "issue": (128.0, "nominal")}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_pipe_peaks.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        for k in ("mufu_sincos", "vabsdiff4"):
+            if k in d:
+                out[k] = (float(d[k]["lane_ops_per_clk_per_sm"]), f"builder-measured ({os.path.basename(path)})")
+        if "ffma" in d and "imad" in d:       # TEA issues on the alu and fma pipes together
+            out["issue"] = (float(d["imad"]["lane_ops_per_clk_per_sm"]) + float(d["lop3"]["lane_ops_per_clk_per_sm"]),
+                            f"builder-measured IMAD + LOP3 pipes ({os.path.basename(path)})")
+        break
+    return out
+
+
 def alu_peak(kind: str, sm_mhz: float, n_sm: int = 148) -> tuple[float, str]:
-    """ALU peaks from unit counts x clock (B300_MICROARCH pipe rates): MUFU 16
-    ops/clk/SM (sin, cos); SAD's VABSDIFF4 on the alu pipe, 64 lanes/clk/SM (rt 2 per SMSP);
-    TEA's integer mix spreads over the alu pipe (IADD3/LOP3/SHF) and the fma pipe (IMAD), so its
-    ceiling is the issue rate, 128 lanes/clk/SM."""
+    """ALU peaks from lane ops per SM clock x SMs x clock: MRIQ's sin + cos on
+    MUFU; SAD's VABSDIFF4 on the alu pipe; TEA's integer mix spread over the alu pipe (IADD3/LOP3/
+    SHF) and the fma pipe (IMAD), so its ceiling is the two pipes together."""
     f = sm_mhz * 1e6
-    if kind == "MRIQ":
-        return 16 * n_sm * f, "MUFU ops/s (16/clk/SM)"
-    if kind == "TEA":
-        return 128 * n_sm * f, "int ops/s (alu+fma pipes, issue 128/clk/SM)"
-    return 64 * n_sm * f, "int ALU ops/s (64/clk/SM)"
+    pp = pipe_peaks()
+    key = {"MRIQ": "mufu_sincos", "TEA": "issue"}.get(kind, "vabsdiff4")
+    per, src = pp[key]
+    label = {"MRIQ": "MUFU ops/s", "TEA": "int ops/s (alu+fma pipes)"}.get(kind, "int ALU ops/s")
+    return per * n_sm * f, f"{label} ({per:.2f}/clk/SM, {src})"
 
 
 # ---------------------------------------------------------------------------------------------
@@ -192,24 +253,25 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------------------------
-def global_queue(workload: str, instances: int, world: int) -> list[str]:
+def global_queue(workload: str, instances: int, world: int, mix: str = "ALL") -> list[str]:
     """c2 (configs[1]): ALL mix, `instances` of each kernel per GPU, round-robin arrivals.
-    c4 (configs[3]): 1000 kernels per GPU drawn uniformly from ALL (seed 42).
+    c4 (configs[3]): 1000 kernels per GPU drawn uniformly from `mix` (ALL, or the CI/MI/MIX
+    variants of tb:workloads; seed 42).
     c5 (configs[4]): 10,000-kernel multi-user queue (16 Poisson users on CI/MI/MIX/ALL), the
     whole queue shared by all GPUs (strong scaling)."""
     if workload == "c2":
         return [e["kind"] for e in G.queue("ALL", len(ALL) * instances * world, order="round_robin")]
     if workload == "c4":
-        return [e["kind"] for e in G.queue("ALL", 1000 * world, seed=42, order="uniform")]
+        return [e["kind"] for e in G.queue(mix, 1000 * world, seed=42, order="uniform")]
     if workload == "c5":
         return [e["kind"] for e in G.multi_user_queue(10000, 16, seed=7)]
     raise ValueError(workload)
 
 
-def build_queue(rank: int, world: int, instances: int, workload: str = "c2") -> list[str]:
+def build_queue(rank: int, world: int, instances: int, workload: str = "c5", mix: str = "ALL") -> list[str]:
     """This GPU's shard of the global queue, mix-preserving round robin."""
     from paper_1303_5164_b200.dist import shard
-    return shard(global_queue(workload, instances, world), rank, world)
+    return shard(global_queue(workload, instances, world, mix), rank, world)
 
 
 MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
@@ -226,6 +288,17 @@ def load_profiles(path: str):
     return None, {}
 
 
+def max_over_ranks(x: float, dev, world: int, backend: str = "nccl") -> float:
+    """The slowest rank's value (whole-job time is set by the last GPU to finish)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_kernelet(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -236,25 +309,31 @@ def run_kernelet(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     K.lib()
-    kinds = build_queue(rank, world, args.instances, args.workload)
+    kinds = build_queue(rank, world, args.instances, args.workload, args.mix)
     profiles, kcfg = load_profiles(args.profile)
     t_gen = time.time()
     data = {k: G.gen(k, args.size) for k in sorted(set(kinds))}
-    inputs = {k: inputs_to_device(data[k], dev) for k in data}
-    # output leases: a pool of POOL output sets per kind, instance j of a kind writes set j % POOL
-    # (inputs are shared read-only); the trace check below proves no two launches that were
-    # resident at the same time wrote the same set
+    # leases: POOL input sets and POOL output sets per kind (distinct device buffers; input set j
+    # is a device copy of the generated set, so every set has the oracle's values); instance j of
+    # a kind reads input set j % POOL and writes output set j % POOL.  The trace check below
+    # proves no two launches that were resident at the same time wrote the same output set.
     from paper_1303_5164_b200.workload import alloc_outputs
-    POOL = 4
-    pools, seen, lease = {}, {}, []
+    POOL = max(1, args.pool)
+    in_pools, pools, seen, lease = {}, {}, {}, []
     insts = []
     for k in kinds:
         j = seen.get(k, 0)
         seen[k] = j + 1
         if j < POOL:
+            if j == 0:
+                in_pools[k] = [inputs_to_device(data[k], dev)]
+            else:
+                in_pools[k].append({n: t.clone() for n, t in in_pools[k][0].items()})
             pools.setdefault(k, []).append(alloc_outputs(k, data[k]["params"], dev))
-        insts.append(Instance(data[k], dev, inputs=inputs[k], outputs=pools[k][j % POOL]))
+        insts.append(Instance(data[k], dev, inputs=in_pools[k][j % POOL], outputs=pools[k][j % POOL]))
+        insts[-1].lease = j % POOL
         lease.append((k, j % POOL))
+    torch.cuda.synchronize(dev)
     t_gen = time.time() - t_gen
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
     lane_a = torch.cuda.Stream(device=dev)
@@ -277,7 +356,8 @@ def run_kernelet(args, rank, world, local_rank):
         tab = json.load(open(args.opt))["table"]
         ctx.cache_put([((t["k1"], t["k2"], t["b1"], t["b2"]), t) for t in tab])
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > L2 (126.5 MiB)
-    gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev)
+    nccl = world > 1 and args.backend == "nccl"
+    gathered = torch.zeros(world * 8, dtype=torch.int64, device=dev if nccl else "cpu")
 
     counters[5] = rank      # kl_counters.rank / .world: the per-step reset clears fields 0-4 only
     counters[6] = world
@@ -288,9 +368,11 @@ def run_kernelet(args, rank, world, local_rank):
         ctx.reset_counters()
         ids = ctx.submit_many([(i.kind, i.grid, i.args, n + 1, None) for n, i in enumerate(insts)])
         c = ctx.sync()
-        if world > 1:
+        if nccl:        # the one collective: per-GPU counters, read by NCCL from device memory
             with torch.cuda.stream(lane_a):
                 dist.all_gather_into_tensor(gathered, counters)
+        elif world > 1:
+            dist.all_gather_into_tensor(gathered, counters.cpu())
         return ids, c
 
     def barrier():
@@ -356,18 +438,18 @@ def run_kernelet(args, rank, world, local_rank):
                                     "partner": K.KINDS[t.partner_kind] if t.partner_kind >= 0 else None,
                                     "cp": round(t.cp, 3), "dec": t.phase}) + "\n")
     lease_conflicts = check_leases(trace, ids, lease)
-    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), dev, world, args.backend)
     c_last = cnts[-1]
     assert c_last.kernels_done == len(insts), (c_last.kernels_done, len(insts))
-    if world > 1:
+    n_done = len(insts)
+    if world > 1:       # whole-job completion from the all-gathered counters of the last step
         g = gathered.view(world, 8).cpu()
-        assert int(g[:, 0].sum()) == len(insts) * world      # NCCL-gathered completion counters
-
+        n_done = int(g[:, 0].sum())
+        assert [int(x) for x in g[:, 6]] == [world] * world and sorted(int(x) for x in g[:, 5]) == list(range(world))
+        assert n_done == args.n_global, (n_done, args.n_global)
     res = {
-        "value": len(insts) * world * args.steps / (total_ms / 1e3),
+        "value": n_done * args.steps / (total_ms / 1e3),
+        "kernels_per_rank": len(insts),
         "ms_per_step": total_ms / args.steps,
         "device_ms_per_step": statistics.median(dev_ms),
         "phases_per_step": (ctx.stats().decisions - dec0) / args.steps,
@@ -388,7 +470,7 @@ def run_kernelet(args, rank, world, local_rank):
     res["schedule_first_step"] = phase_kinds
 
     if not args.no_baselines:
-        res["baselines"] = baselines(ctx, insts, dev, flush, barrier, args)
+        res["baselines"] = baselines(ctx, insts, dev, flush, barrier, args, world)
         res["per_kernel"] = per_kernel(ctx, insts, data, dev, flush, barrier)
         res["e2e"] = e2e(ctx, insts, data, dev, barrier, args, world, rank, lane_a, lane_b, res["per_kernel"])
     ctx.close()
@@ -453,34 +535,35 @@ def _time_streams(fn, dev, flush, barrier, reps=3):
     return statistics.median(ts)
 
 
-def baselines(ctx, insts, dev, flush, barrier, args) -> dict:
+def baselines(ctx, insts, dev, flush, barrier, args, world=1) -> dict:
     """Sequential (one stream, full grids at max occupancy, back to back) and plain multi-stream
-    (round robin over S streams, full grids, no slicing) executions of the same kernels."""
+    (round robin over S streams, full grids, no slicing) executions of the same kernels, on every
+    rank's shard; whole-job time = the slowest rank."""
     import torch
     out = {}
+    n = args.n_global
 
     def seq(s, e0):
         for i in insts:
             ctx.run_plain(i.kind, i.grid, i.args, s)
 
-    ms = _time_streams(seq, dev, flush, barrier)
-    out["sequential"] = {"ms_per_step": ms, "kernels_per_s": len(insts) / (ms / 1e3)}
+    ms = max_over_ranks(_time_streams(seq, dev, flush, barrier), dev, world, args.backend)
+    out["sequential"] = {"ms_per_step": ms, "kernels_per_s": n / (ms / 1e3)}
     for S in (2, 4, 8):
         streams = [torch.cuda.Stream(device=dev) for _ in range(S)]
 
         def ms_fn(s, e0, streams=streams):
-            evs = []
             for st in streams:
                 st.wait_event(e0)
-            for n, i in enumerate(insts):
-                ctx.run_plain(i.kind, i.grid, i.args, streams[n % len(streams)])
+            for j, i in enumerate(insts):
+                ctx.run_plain(i.kind, i.grid, i.args, streams[j % len(streams)])
             for st in streams:
                 ev = torch.cuda.Event()
                 ev.record(st)
                 s.wait_event(ev)
 
-        ms = _time_streams(ms_fn, dev, flush, barrier)
-        out[f"multistream{S}"] = {"ms_per_step": ms, "kernels_per_s": len(insts) / (ms / 1e3)}
+        ms = max_over_ranks(_time_streams(ms_fn, dev, flush, barrier), dev, world, args.backend)
+        out[f"multistream{S}"] = {"ms_per_step": ms, "kernels_per_s": n / (ms / 1e3)}
     return out
 
 
@@ -508,31 +591,32 @@ def johnson_order(jobs, a, b):
 
 
 def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b, pk=None) -> dict:
-    """Same metric through the public API with HOST buffers: every step copies the step's inputs
-    (one set per kind, shared by its instances) from pinned host memory and reads the completion
-    counters back.  Each kind's copy is its kernels' arrival: the kernels are submitted with the
-    copy's event as `ready_event`, so the scheduler overlaps the PCIe transfer of later kinds with
-    the execution of earlier ones (arrivals trigger re-planning)."""
+    """Same metric through the public API with HOST buffers.  Every step copies every input set
+    of the step (the --pool sets per kind; instance j of a kind reads set j % pool) from pinned
+    host memory and reads every output set back (the last instance written to each set), inside
+    the timed region.  Each input set's copy is the arrival of the kernels that read it: they are
+    submitted with the copy's event as `ready_event`, so the scheduler overlaps the PCIe transfer
+    of later sets with the execution of earlier ones (arrivals trigger re-planning)."""
     import torch
-    kinds_in_order = []
+    sets = []               # (kind, lease) in first-use order
     for i in insts:
-        if i.kind not in kinds_in_order:
-            kinds_in_order.append(i.kind)
+        if (i.kind, i.lease) not in sets:
+            sets.append((i.kind, i.lease))
+    rep = {s: next(i for i in insts if (i.kind, i.lease) == s) for s in sets}
     # copy order: a two-stage flow shop (one copy stream, then the kernels), ordered by Johnson's
-    # rule -- kinds whose copy is shorter than their kernel time first, by increasing copy time;
+    # rule -- sets whose copy is shorter than their kernel time first, by increasing copy time;
     # then the rest by decreasing kernel time -- so the last copy has the least kernel time behind
     # it (copy time from the bytes at the measured ~55 GB/s pinned H2D rate)
     if pk:
-        nk = {k: sum(1 for i in insts if i.kind == k) for k in kinds_in_order}
-        nbytes = {k: sum(t.numel() * t.element_size() for t in next(i for i in insts if i.kind == k).inputs.values())
-                  for k in kinds_in_order}
-        kinds_in_order = johnson_order(kinds_in_order, {k: nbytes[k] / 55e9 * 1e3 for k in kinds_in_order},
-                                       {k: pk[k]["ms"] * nk[k] for k in kinds_in_order})
-    host = {}
-    for k in kinds_in_order:
-        src = next(i for i in insts if i.kind == k)
-        host[k] = {n: t.cpu().pin_memory() for n, t in src.inputs.items()}
-    h2d = sum(t.numel() * t.element_size() for d in host.values() for t in d.values())
+        nk = {s: sum(1 for i in insts if (i.kind, i.lease) == s) for s in sets}
+        a = {s: rep[s].input_bytes() / 55e9 * 1e3 for s in sets}
+        b = {s: pk[s[0]]["ms"] * nk[s] for s in sets}
+        sets = johnson_order(sets, a, b)
+    host_in = {s: {n: t.cpu().pin_memory() for n, t in rep[s].inputs.items()} for s in sets}
+    host_out = {s: {n: torch.empty_like(t, device="cpu").pin_memory() for n, t in rep[s].outputs.items()}
+                for s in sets}
+    h2d = sum(t.numel() * t.element_size() for d in host_in.values() for t in d.values())
+    d2h = sum(t.numel() * t.element_size() for d in host_out.values() for t in d.values()) + 64
     copy_stream = torch.cuda.Stream(device=dev)
     ts = []
     for _ in range(max(2, min(args.steps, 3))):
@@ -542,40 +626,43 @@ def e2e(ctx, insts, data, dev, barrier, args, world, rank, lane, lane_b, pk=None
         copy_stream.wait_event(e0)
         ready = {}
         with torch.cuda.stream(copy_stream):
-            for k in kinds_in_order:
-                src = next(i for i in insts if i.kind == k)
-                for n, t in src.inputs.items():
-                    t.copy_(host[k][n], non_blocking=True)
+            for s in sets:
+                for n, t in rep[s].inputs.items():
+                    t.copy_(host_in[s][n], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
-                ready[k] = ev
+                ready[s] = ev
         ctx.reset_model_cache()
         ctx.reset_counters()
-        ctx.submit_many([(i.kind, i.grid, i.args, n + 1, ready[i.kind]) for n, i in enumerate(insts)])
+        ctx.submit_many([(i.kind, i.grid, i.args, n + 1, ready[(i.kind, i.lease)]) for n, i in enumerate(insts)])
         c = ctx.sync()
-        res = ctx.counters.cpu()        # D2H read of the step's result
+        with torch.cuda.stream(lane):   # D2H of the step's results: every output set + counters
+            for s in sets:
+                for n, t in rep[s].outputs.items():
+                    host_out[s][n].copy_(t, non_blocking=True)
+            res = ctx.counters.to("cpu", non_blocking=True)
         e1.record(lane)
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
         assert int(res[0]) == len(insts)
-    ms = statistics.median(ts)
-    if world > 1:                       # whole-job time: the slowest rank
-        import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"value": len(insts) * world / (ms / 1e3), "unit": "kernels/s", "h2d_bytes_per_step": int(h2d),
-            "copy_order": kinds_in_order,
-            "d2h_bytes_per_step": 64, "ms_per_step": ms, "h2d_GBps": h2d / (ms / 1e3) / 1e9}
+    ms = max_over_ranks(statistics.median(ts), dev, world, args.backend)
+    return {"value": args.n_global / (ms / 1e3), "unit": "kernels/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": ms, "h2d_GBps": h2d / (ms / 1e3) / 1e9,
+            "copy_order": [f"{k}#{j}" for k, j in sets],
+            "what": f"every step: H2D of all {len(sets)} input sets ({args.pool} per kind, pinned host -> device), "
+                    f"the queue, D2H of all {len(sets)} output sets + the counters"}
 
 
 # ---------------------------------------------------------------------------------------------
 class OracleLeg:
     """The oracle as it stands, on the host cores: every kind's outputs on a fixed strided sample
-    (fraction f of the elements) plus the oracle's full Alg.1 decision sequence (model + search)
-    for the queue; throughput = kernels-equivalent of work done / wall time."""
+    (fraction f of the elements) plus the oracle's Alg.1 decision sequence for the queue, run in
+    the GPU run's configuration (the calibrated profile's L0/B/a0/b0 latency, alpha_p/alpha_m, the
+    occupancy-level mode and the split rule); throughput = kernels-equivalent of work done / wall
+    time."""
 
-    def __init__(self, kinds: list[str], size: str):
+    def __init__(self, kinds: list[str], size: str, profile_path: str | None = None, split_rule: int = 1,
+                 levels: str = "four", alpha=None, max_decisions: int = 200):
         import oracle as O
         O.build()
         self.O = O
@@ -589,79 +676,113 @@ class OracleLeg:
                              "BS": lambda: p["n"], "TEA": lambda: p["n"],
                              "SAD": lambda: (p["width"] // 16) * (p["height"] // 16) * 1089,
                              "ST": lambda: p["nx"] * p["ny"] * p["nz"], "MM": lambda: p["M"] * p["N"]}[k]()
-        self.profs = _oracle_profiles()
+        self.profs, pcfg = _oracle_profiles(profile_path)
+        self.cfg = O.smcfg(L0=pcfg.get("L0", 800.0), B=pcfg.get("B", 1.0), a0=pcfg.get("a0", 0.0),
+                           b0=pcfg.get("b0", 0.0), W=16)
+        ap, am = alpha if alpha else (pcfg.get("alpha_p", 0.4), pcfg.get("alpha_m", 0.1))
+        self.sched_kw = dict(ap=ap, am=am, mode="4" if levels == "four" else "all", split_rule=split_rule)
+        self.max_decisions = max_decisions
+        self.config = {"L0": self.cfg.L0, "B": self.cfg.B, "a0": self.cfg.a0, "b0": self.cfg.b0, "W_v": 16,
+                       **self.sched_kw}
 
     def run(self, target_s: float) -> dict:
-        frac = 1e-4
+        frac = 1e-4          # grow the sample until it takes about target_s (bounded CPU work)
+        while True:
+            t_kind = _oracle_sample(self.O, self.data, self.sizes, frac, self.cores)
+            t_k = sum(t_kind.values())
+            if t_k >= 0.5 * target_s or frac >= 1.0:
+                break
+            frac = min(1.0, frac * min(20.0, target_s / max(t_k, 1e-3)))
         t0 = time.time()
-        _oracle_sample(self.O, self.data, self.sizes, frac, self.cores)
-        probe = max(time.time() - t0, 1e-3)
-        frac = min(1.0, frac * target_s / probe)
-        t0 = time.time()
-        _oracle_sample(self.O, self.data, self.sizes, frac, self.cores)
-        t_k = time.time() - t0
-        t0 = time.time()
+        n_dec = 0
         if self.profs:
-            q = [{"kind": k, "blocks": 1000} for k in self.kinds]
-            self.O.alg1_makespan(q, self.profs, self.O.smcfg(W=16))
+            # the decision sequence for the first max_decisions queue entries (each decision
+            # searches every pending kind pair, so its cost does not depend on the queue length
+            # once all kinds are pending)
+            q = [{"kind": k, "blocks": 1000} for k in self.kinds[: self.max_decisions]]
+            _, tr = self.O.alg1_makespan(q, self.profs, self.cfg, **self.sched_kw)
+            n_dec = len(tr)
         t_s = time.time() - t0
-        n_equiv = frac * len(self.kinds)
-        return {"value": n_equiv / (t_k + t_s), "unit": "kernels/s", "cores": self.cores, "kind": "oracle",
-                "sample": f"{frac:.2e} of every output element of the {len(self.kinds)}-kernel queue (strided, "
-                          f"{self.cores} threads) + the oracle's Alg.1/FindCoSchedule decision sequence; "
-                          f"{t_k + t_s:.1f} s wall"}
+        # whole-queue oracle time: each kind's sampled time scaled to one full instance, times the
+        # kind's count in the queue, plus the decisions scaled to one per kernel
+        count = {k: self.kinds.count(k) for k in t_kind}
+        t_queue = sum(count[k] * t_kind[k] / frac for k in t_kind) + t_s * len(self.kinds) / max(1, n_dec)
+        return {"value": len(self.kinds) / t_queue, "unit": "kernels/s", "cores": self.cores, "kind": "oracle",
+                "sample": f"{frac:.2e} of the output elements of one instance of each of the {len(t_kind)} kinds "
+                          f"(strided, {self.cores} threads, {t_k:.1f} s), scaled to the {len(self.kinds)}-kernel "
+                          f"queue's kind counts, + the oracle's Alg.1/FindCoSchedule decisions for the first "
+                          f"{min(len(self.kinds), self.max_decisions) if self.profs else 0} kernels ({n_dec} decisions, "
+                          f"{t_s:.1f} s; charged per kernel) in the GPU run's model configuration {self.config}"}
 
 
-def cpu_oracle_leg(kinds: list[str], size: str, target_s: float = 15.0) -> dict:
-    return OracleLeg(kinds, size).run(target_s)
+def cpu_oracle_leg(kinds: list[str], size: str, target_s: float = 15.0, **kw) -> dict:
+    return OracleLeg(kinds, size, **kw).run(target_s)
 
 
-def _oracle_sample(O, data, sizes, frac, cores):
+def _oracle_sample(O, data, sizes, frac, cores) -> dict:
+    """Run the oracle on a strided `frac` of every kind's output elements, the kind's elements
+    split over `cores` threads; returns wall seconds per kind."""
     from concurrent.futures import ThreadPoolExecutor
-    jobs = []
-    for k, d in data.items():
-        n = sizes[k]
-        m = max(1, int(n * frac))
-        idx = np.linspace(0, n - 1, m).astype(np.int64)
-        for chunk in np.array_split(idx, cores):
-            if chunk.size:
-                jobs.append((d, chunk))
+    out = {}
     with ThreadPoolExecutor(cores) as ex:
-        list(ex.map(lambda j: O.run_kernel(j[0], j[1]), jobs))
+        for k, d in data.items():
+            n = sizes[k]
+            m = max(1, int(n * frac))
+            idx = np.linspace(0, n - 1, m).astype(np.int64)
+            t0 = time.time()
+            list(ex.map(lambda c, d=d: O.run_kernel(d, c), [c for c in np.array_split(idx, cores) if c.size]))
+            out[k] = time.time() - t0
+    return out
 
 
-def _oracle_profiles():
-    path = os.path.join(ROOT, "profiles", "kl_profile_b200.json")
+def _oracle_profiles(path: str | None = None):
+    path = path or os.path.join(ROOT, "profiles", "kl_profile_b200.json")
     if not os.path.exists(path):
-        return None
-    d = json.load(open(path))["profiles"]
-    return {k: v for k, v in d.items() if k in ALL}
+        return None, {}
+    d = json.load(open(path))
+    return {k: v for k, v in d["profiles"].items() if k in ALL}, d.get("config", {})
 
 
 # ---------------------------------------------------------------------------------------------
-def main():
-    args = parse()
+def workload_name(args) -> str:
+    return {"c2": f"C2: ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels per GPU, {args.size} "
+                  "sizes, all pending at t=0)",
+            "c4": f"C4: 1000 kernels per GPU uniform over {args.mix} (seed 42), {args.size} sizes",
+            "c5": f"C5: 10,000-kernel multi-user queue (16 Poisson users on CI/MI/MIX/ALL, seed 7) shared by all "
+                  f"GPUs, {args.size} sizes"}[args.workload]
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    cmd = spawn_cmd(args, argv)
+    if cmd:                 # --gpus N without a launcher: one process per GPU via torch.distributed.run
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    n_global = len(global_queue(args.workload, args.instances, world))
-    wl_name = {"c2": f"ALL mix x{args.instances} per GPU ({len(ALL) * args.instances} kernels, {args.size} sizes, "
-                     "all pending at t=0)",
-               "c4": f"1000 kernels per GPU uniform over ALL (seed 42), {args.size} sizes",
-               "c5": f"10,000-kernel multi-user queue (16 Poisson users, CI/MI/MIX/ALL), {args.size} sizes"}[args.workload]
-    config = {"workload": wl_name, "global_kernels": n_global,
+    if args.gpus is None:
+        args.gpus = world
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    args.n_global = len(global_queue(args.workload, args.instances, world, args.mix))
+    config = {"workload": workload_name(args), "global_kernels": args.n_global,
               "sizes": "tb:description (million = 2^20), MRIQ numK = 2048", "parallelism": f"queue shard x{world}",
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
+              "leases": f"{args.pool} input sets + {args.pool} output sets per kind (distinct device buffers)",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
               "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
               "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
               else "every b with whole warps per virtual SM"}
+    scaling = "strong" if args.workload == "c5" else "weak"
+    leg_kw = dict(profile_path=args.profile, split_rule=args.split_rule, levels=args.levels, alpha=args.alpha)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        kinds = build_queue(0, 1, args.instances, args.workload)
-        leg = OracleLeg(kinds, args.size)
+        kinds = build_queue(0, 1, args.instances, args.workload, args.mix)
+        leg = OracleLeg(kinds, args.size, **leg_kw)
         vals = []
         for s in range(args.warmup + args.steps):
             r = leg.run(target_s=max(2.0, 60.0 / (args.warmup + args.steps)))
@@ -669,7 +790,7 @@ def main():
                 vals.append(r["value"])
         v = statistics.median(vals)
         line = {"metric": METRIC, "value": v, "unit": "kernels/s", "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32/f64/u32 (per kernel)", "data": "synthetic", "config": config,
                 "cpu_baseline": {**r, "value": v}, "e2e": {"value": v, "unit": "kernels/s", "h2d_bytes_per_step": 0,
                                                           "d2h_bytes_per_step": 0}}
@@ -677,10 +798,15 @@ def main():
         return
 
     import torch
+    if os.environ.get("KL_BENCH_ONE_DEVICE"):   # functional multi-rank check on a one-GPU box
+        local_rank = 0
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     res = run_kernelet(args, rank, world, local_rank)
     if rank == 0:
         bl = res.get("baselines", {})
@@ -705,7 +831,7 @@ def main():
                 a = v["ops"] / (v["ms"] / 1e3)
                 roof_all[k] = {"bound": "alu", "achieved": a / 1e12, "peak": pk_ / 1e12, "unit": f"T{what}",
                                "frac": a / pk_, "ms": v["ms"]}
-        qk = build_queue(0, 1, args.instances, args.workload)
+        qk = build_queue(0, 1, args.instances, args.workload, args.mix)
         dom = max(pk, key=lambda k: pk[k]["ms"] * sum(1 for x in qk if x == k)) if pk else None
         roof = None
         if dom:
@@ -729,11 +855,11 @@ def main():
                     "units_per_instance": units}
         line = {"metric": METRIC, "value": res["value"], "unit": "kernels/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
-                "scaling": "strong" if args.workload == "c5" else "weak", "vs_baseline": None, "dtype": "f32/bf16->f32/u32/u8 (per kernel); model f64",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f32/bf16->f32/u32/u8 (per kernel); model f64",
                 "data": "synthetic", "config": config, "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
                 "e2e": res.get("e2e"), "roofline": roof,
-                "speedup_vs_sequential": res["value"] / world / seq if seq else None,
-                "speedup_vs_multistream": res["value"] / world / ms4 if ms4 else None,
+                "speedup_vs_sequential": res["value"] / seq if seq else None,
+                "speedup_vs_multistream": res["value"] / ms4 if ms4 else None,
                 "baselines": bl, "roofline_all": roof_all, "device_ms_per_step": res["device_ms_per_step"],
                 "phases_per_step": res["phases_per_step"], "parity": res["parity"],
                 "engine_per_step": {k: res.get(k) for k in ("retunes_per_step", "stops_per_step", "memops_per_step")},
@@ -742,7 +868,7 @@ def main():
                 "schedule_first_step": res["schedule_first_step"]}
         if not args.no_cpu and world == 1:
             try:
-                line["cpu_baseline"] = cpu_oracle_leg(build_queue(0, 1, args.instances, args.workload), args.size)
+                line["cpu_baseline"] = cpu_oracle_leg(qk, args.size, **leg_kw)
             except Exception as e:      # never lose the GPU line to the CPU leg
                 line["cpu_baseline"] = {"error": repr(e)[:300]}
         print(json.dumps(line))

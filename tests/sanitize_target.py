@@ -3,7 +3,7 @@
 size unsliced, explicitly sliced (index rectification, 3 slices, permuted order), through the
 persistent slice launcher (scheduler: the whole mixed queue co-scheduled), and one model batch
 (kl_predict over candidate pairs).  Checks parity so a sanitizer run is also a correctness run.
-usage: compute-sanitizer --tool {memcheck,racecheck,synccheck} python tools/sanitize_target.py [KINDS]"""
+usage: compute-sanitizer --tool {memcheck,racecheck,synccheck} python tests/sanitize_target.py [KINDS]"""
 import os
 import sys
 

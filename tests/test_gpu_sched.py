@@ -237,7 +237,7 @@ def test_compute_sanitizer_memcheck_clean():
     if not os.path.exists(exe):
         pytest.skip("compute-sanitizer not installed")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([exe, "--tool", "memcheck", sys.executable, os.path.join(root, "tools", "sanitize_target.py"),
+    r = subprocess.run([exe, "--tool", "memcheck", sys.executable, os.path.join(root, "tests", "sanitize_target.py"),
                         "PC,SPMV,MM,BS"], capture_output=True, text=True, timeout=600, cwd=root)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-2000:]

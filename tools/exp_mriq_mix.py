@@ -1,6 +1,7 @@
 """A/B of the MRIQ MUFU/polynomial mix (KL_MRIQ_G, KL_MRIQ_P): build one libkl.so per variant
 (`build`, CPU) and time each on the GPU (`run`): solo plain-grid device time at paper size (L2
-flushed, median of 7) and normwise parity against the oracle on a small seeded case."""
+flushed, median of 7); parity of a variant build is tests/test_gpu_kernels.py (tools/ never
+imports oracle/)."""
 import json
 import os
 import subprocess
@@ -31,16 +32,10 @@ def one():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch
     import kl_inputs as G
-    import oracle as O
     import paper_1303_5164_b200 as K
     from paper_1303_5164_b200.workload import Instance
-    from kl_check import compare
     ctx = K.Context(device=0)
-    d = G.gen("MRIQ", "small")
-    i = Instance(d, "cuda")
-    ctx.run_plain("MRIQ", i.grid, i.args, 0)
-    torch.cuda.synchronize()
-    err = compare("MRIQ", i.result(), O.run_kernel(d))
+    err = None      # parity of the variant: tests/test_gpu_kernels.py on the variant build
     i = Instance(G.gen("MRIQ", "paper"), "cuda")
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     ts = []
