@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define KL_ABI_VERSION 1
+#define KL_ABI_VERSION 2
 #define KL_MAX_SMS 256
 
 typedef struct kl_ctx kl_ctx;
@@ -77,10 +77,11 @@ typedef struct {   /* ST: 7-point stencil, in[z][y][x]; block = 128x4 (x,y) tile
     int32_t nx, ny, nz;
     float c0, c1;          /* interior out = c1*(6 neighbours) - c0*in; boundary out = in */
 } kl_args_st;
-typedef struct {   /* MM: C[M][N] (fp32) = A[M][K] (bf16) * B, B given K-major as Bt[N][K] (bf16)*/
+typedef struct {   /* MM: C[M][N] (fp32) = A[M][K] (bf16) * B, B given K-major as Bt[N][K] (bf16);
+                      one thread block = one 256x256 output tile on a CTA pair (tcgen05 2-SM)   */
     const uint16_t* A; const uint16_t* Bt;
     float* C;
-    int32_t M, N, K;       /* M multiple of 128, N multiple of 256, K multiple of 64 */
+    int32_t M, N, K;       /* M multiple of 256, N multiple of 256, K multiple of 64 */
 } kl_args_mm;
 typedef struct {   /* MRIQ: Q[i] = sum_k phiMag_k exp(i 2 pi k.x_i); one voxel per thread       */
     const float *x, *y, *z, *kx, *ky, *kz, *phimag;
@@ -163,6 +164,11 @@ typedef struct {
                                   re-tunes or stops it (needs retune = 1); 0 (default): measured
                                   no gain on B200 (the batch then shares the SMs with it) */
     int32_t max_regs_per_sm, max_smem_per_sm, max_warps_per_sm, max_blocks_per_sm; /* 0 = device */
+    int32_t mm_stages;         /* MM's occupancy level: TMA ring stages of its CTA
+                                  pairs, one of 2 3 4 6 (32 KiB of shared memory each); 0
+                                  (default): per co-schedule the deepest ring whose shared memory
+                                  fits beside the partner's blocks (6 when MM runs solo) */
+    int32_t pad_cfg;
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
     void* stream_b;            /* optional cudaStream_t: second stream of the launch pool      */
@@ -221,6 +227,8 @@ typedef struct {               /* one launch of a kernel (trace / residency evid
     double cp;                 /* predicted CP of that decision */
     uint32_t cap_max;          /* largest cap in force during the launch (re-tunes) */
     uint32_t grids;            /* device grids that served it (1 + top-ups) */
+    uint32_t variant;          /* kind-specific instantiation (MM: TMA ring stages), 0 = none */
+    uint32_t pad;
 } kl_trace_rec;
 
 /* ---- calls -------------------------------------------------------------------------------- */
@@ -234,8 +242,8 @@ const char* kl_last_error(const kl_ctx* ctx);
 /* Alg.1 lines 2-3: add kernel K to the pending set R; returns its id (>= 1).
  * Errors: KL_EINVAL for an unknown kind, grid_blocks = 0 or >= 2^27, args_bytes != the kind's
  * kl_args size, Rm outside [0,1] in an attached profile, args the kind cannot use (ST: nx not a
- * multiple of 4; MM: M, N, K not multiples of the 128 x 256 x 64 tile, or grid_blocks larger
- * than the (M/128)(N/256) output tiles -- every other body range-checks its virtual block). */
+ * multiple of 4; MM: M, N, K not multiples of the 256 x 256 x 64 pair tile, or grid_blocks
+ * larger than the (M/256)(N/256) output tiles -- every other body range-checks its virtual block). */
 kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* desc, uint64_t* out_id);
 /* kl_submit for n descriptors in order (one ABI crossing for a whole queue); out_ids[n] (may be
  * NULL).  Errors as kl_submit: the first failing descriptor's status is returned, the ones before

@@ -54,7 +54,7 @@ SMALL = {
     "SAD": dict(width=176, height=112),                                   # 11x7 = 77 macroblocks
     "SPMV": dict(n_rows=1003, n_cols=800, nnz_min=8, nnz_max=24),       # ragged last block
     "ST": dict(nx=96, ny=20, nz=136),                                     # partial tiles in y and z
-    "MM": dict(M=384, N=256, K=192),
+    "MM": dict(M=512, N=256, K=192),
     "MRIQ": dict(num_x=10007, num_k=300),
     "BS": dict(n=128 * 20 * 64),                                          # config C1: 163840
     "TEA": dict(n=128 * 10 * 37 + 6),
@@ -75,7 +75,7 @@ SAD_MB = 16            # macroblock edge
 SAD_RANGE = 16         # search offsets in [-16, 16]
 SPMV_ROWS_PER_BLOCK = 8
 ST_TILE = (128, 4, 32)  # x, y, z points per block (32 threads x float4 in x, 4 rows)
-MM_TILE = (128, 256)   # output tile (M, N) per block
+MM_TILE = (256, 256)   # output tile (M, N) per block (a CTA pair)
 BS_PER_BLOCK = 128 * 20
 TEA_PER_BLOCK = 128 * 10
 MRIQ_PER_BLOCK = 256

@@ -114,6 +114,7 @@ class Config(C.Structure):
                 ("retune", C.c_int32), ("model_states", C.c_int32), ("granularity", C.c_int32),
                 ("age_limit_us", C.c_int32), ("mc_seed", C.c_int32), ("speculative", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
+                ("mm_stages", C.c_int32), ("pad_cfg", C.c_int32),
                 ("profiles", C.POINTER(Profile)), ("stream_a", _vp), ("stream_b", _vp),
                 ("counters_dev", _vp)]
 
@@ -159,7 +160,8 @@ class TraceRec(C.Structure):
                 ("slice", C.c_uint32), ("start", C.c_uint32), ("end", C.c_uint32), ("executed", C.c_uint32),
                 ("admitted", C.c_uint32), ("max_per_sm", C.c_uint32), ("exhausted", C.c_uint32),
                 ("t0_ns", C.c_int64), ("t1_ns", C.c_int64), ("phase", C.c_int32),
-                ("partner_kind", C.c_int32), ("cp", C.c_double), ("cap_max", C.c_uint32), ("grids", C.c_uint32)]
+                ("partner_kind", C.c_int32), ("cp", C.c_double), ("cap_max", C.c_uint32), ("grids", C.c_uint32),
+                ("variant", C.c_uint32), ("pad", C.c_uint32)]
 
 
 ABI_SYMBOLS = ["kl_abi_version", "kl_config_default", "kl_create", "kl_destroy", "kl_last_error",

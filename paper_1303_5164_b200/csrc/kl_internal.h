@@ -106,6 +106,8 @@ struct KlLaunch {
     uint32_t* audit;                // per-virtual-block execution counts (may be null)
     unsigned long long* stamps;     // per-virtual-block end time, %globaltimer (may be null)
     unsigned long long tag;
+    uint32_t variant;               // kind-specific instantiation (MM: TMA ring stages; 0 = default)
+    uint32_t pad;
 };
 
 // ---- kernel-side entry points exported by kl_kernels.cu / kl_mm.cu ---------------------------

@@ -15,6 +15,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include <type_traits>
 #include "kl_internal.h"
 
@@ -25,6 +26,7 @@ __device__ __forceinline__ uint32_t smid_u32() {
     asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
     return r;
 }
+__device__ __forceinline__ uint32_t smem_u32_of(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -342,6 +344,169 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
     }
 }
 
+// ---- CTA pairs (thread-block clusters of 2 on one TPC) ------------------------------------
+// A body with kPair = true runs one virtual block on a CTA pair (tcgen05 cta_group::2: the two
+// SMs' tensor cores compute one tile from operands split across their shared memories).  The
+// pair joins, is admitted and fetches as ONE unit: each CTA passes its own SM's admission cap,
+// the leader (cluster rank 0) fetches and hands the range to its peer through distributed shared
+// memory, and both run Body::block on the same virtual block.  Statistics (executed blocks,
+// audit, stamps) are the leader's.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `local` (a shared::cta address) in the CTA of cluster rank `rank`
+__device__ __forceinline__ uint32_t map_rank(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+template <class Body>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(64)
+k_persistent_pair(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
+    extern __shared__ __align__(1024) char dsmem[];
+    __shared__ uint32_t s_vb[2], s_end[2], s_adm, s_peer_adm;
+    KlCtl* ctl = L.ctl;
+    const uint32_t len = ctl->len;
+    const uint32_t rank = cluster_rank();
+    uint32_t sm = 0;
+    bool joined = false;
+    if (threadIdx.x == 0) {
+        uint32_t adm = 0;
+        joined = join_epoch(L);
+        if (joined) {
+            sm = smid_u32();
+            const uint32_t cap = cap_now(L, ctl);
+            const uint32_t c = atomicAdd(&ctl->sm_count[sm], 1u);
+            if (cap && c >= cap) atomicSub(&ctl->sm_count[sm], 1u);
+            else adm = 1;
+        }
+        s_adm = adm;
+        st_cluster_u32(map_rank(smem_u32_of(&s_peer_adm), rank ^ 1u), adm);
+    }
+    cluster_sync_all();
+    const bool pair_ok = s_adm && s_peer_adm;
+    if (threadIdx.x == 0 && s_adm) {
+        if (!pair_ok) {
+            atomicSub(&ctl->sm_count[sm], 1u);     // the peer was refused: release this SM's slot
+        } else {
+            const uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+            atomicMax(&ctl->sm_hwm[sm], c);
+            atomicAdd(&ctl->sm_adm[sm], 1u);
+            const unsigned long long now = gtimer();
+            if (atomicCAS(&ctl->sm_t0[sm], 0ull, now) != 0ull) atomicMin(&ctl->sm_t0[sm], now);
+        }
+    }
+    if (pair_ok) {
+        typename Body::State st;
+        Body::init(P, st, dsmem);
+        uint32_t nexec = 0;
+        bool counted = true;
+        for (uint32_t it = 0;; ++it) {
+            if (threadIdx.x == 0 && rank == 0) {
+                uint32_t vb = 0, end = 0;
+                const uint32_t cap = cap_now(L, ctl);
+                bool leave = false;
+                if (cap) {
+                    uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                    while (c > cap) {
+                        const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                        if (prev == c) { leave = true; counted = false; break; }
+                        c = prev;
+                    }
+                }
+                if (!leave) {
+                    const unsigned long long req = ctl->stop_req;
+                    unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L.chunk);
+                    if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
+                        stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
+                        old = (atomicAdd(&ctl->word, 0ull) & ~KL_W_MASK28) | (old & KL_W_MASK28);
+                    }
+                    vb = kl_w_next(old);
+                    const uint32_t lim = word_limit(old, len);
+                    end = vb < lim ? min(vb + L.chunk, lim) : vb;
+                    if (vb >= len && lim == len && L.rec) {
+                        if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
+                            L.rec->drained = 1u;
+                            __threadfence_system();
+                        }
+                    }
+                }
+                s_vb[it & 1] = vb;
+                s_end[it & 1] = end;
+                st_cluster_u32(map_rank(smem_u32_of(&s_vb[it & 1]), 1u), vb);
+                st_cluster_u32(map_rank(smem_u32_of(&s_end[it & 1]), 1u), end);
+            }
+            Body::before_pair_sync(st);
+            cluster_sync_all();   // the range is visible to the peer; both finished the previous tile
+            Body::after_pair_sync(st);
+            const uint32_t vb = s_vb[it & 1], end = s_end[it & 1];
+            if (vb >= end) break;
+            for (uint32_t v = vb; v < end; ++v) {
+                if (rank == 0 && L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v] = gtimer();
+                Body::block(P, st, dsmem, v);
+                if (rank == 0 && L.audit && threadIdx.x == 0) atomicAdd(L.audit + v, 1u);
+                if (rank == 0 && L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v + 1] = gtimer();
+            }
+            nexec += end - vb;
+        }
+        Body::fini(P, st, dsmem);
+        if (threadIdx.x == 0) {
+            if (rank == 0) atomicAdd(&ctl->sm_exec[sm], nexec);
+            // the peer's slot: released unless the leader's cap check released the pair's (the
+            // leader's decision to leave is the pair's; its peer's SM keeps the cap too)
+            if (counted) atomicSub(&ctl->sm_count[sm], 1u);
+        }
+    }
+    __shared__ int s_close;
+    __shared__ unsigned long long s_j;
+    if (threadIdx.x == 0) {
+        unsigned long long j = 0ull;
+        s_close = (joined && leave_epoch_try(ctl, &j)) ? 1 : 0;
+        s_j = j;
+    }
+    __syncthreads();
+    if (s_close) {
+        const EpochStats S = gather_stats_block<Body::kThreads>(ctl, L.n_sms);
+        if (threadIdx.x == 0) finalize_epoch(ctl, len, s_j, S);
+    }
+}
+
+// Plain grid of CTA pairs: one resident pair per TPC, cluster c runs virtual blocks offset + c,
+// offset + c + n_clusters, ... (a static tile loop: the pair's setup -- barriers, TMEM
+// allocation -- and its epilogue overlap across its tiles instead of being paid per tile).
+template <class Body>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Body::kThreads, 1)
+k_plain_pair(const __grid_constant__ typename Body::Params P, uint32_t offset, uint32_t n) {
+    extern __shared__ __align__(1024) char dsmem[];
+    uint32_t ncl;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+    typename Body::State st;
+    Body::init(P, st, dsmem);
+    for (uint32_t v = cluster_id_x(); v < n; v += ncl) {
+        if (v != cluster_id_x()) {       // the previous tile's hand-off, as in the pair launcher
+            Body::before_pair_sync(st);
+            cluster_sync_all();
+            Body::after_pair_sync(st);
+        }
+        Body::block(P, st, dsmem, offset + v);
+    }
+    Body::fini(P, st, dsmem);
+}
+
 // Plain grid: blockIdx rectified by the slice offset.
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads)
@@ -382,6 +547,54 @@ template <class Body>
 int launch_persistent(const void* blob, const KlLaunch& L, uint32_t grid, void* stream) {
     const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
     k_persistent<Body><<<grid, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, L);
+    return (int)cudaGetLastError();
+}
+
+// CTA-pair bodies: one resident pair per TPC (one CTA per SM: the body's shared memory and the
+// whole TMEM), attributes from the pair kernels.
+template <class Body>
+int info_of_pair(KlKindInfo* o) {
+    cudaFuncAttributes fa;
+    cudaError_t e;
+    e = cudaFuncSetAttribute(k_persistent_pair<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncSetAttribute(k_plain_pair<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kDynSmem);
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncGetAttributes(&fa, k_persistent_pair<Body>);
+    if (e != cudaSuccess) return (int)e;
+    o->threads = Body::kThreads;
+    o->dyn_smem = Body::kDynSmem;
+    o->regs = fa.numRegs;
+    o->static_smem = (int)fa.sharedSizeBytes;
+    o->tmem_cols = 0;
+    o->bmax = 1;
+    o->default_chunk = Body::kChunk;
+    return 0;
+}
+
+// `grid` CTAs, rounded up to whole pairs.
+template <class Body>
+int launch_persistent_pair(const void* blob, const KlLaunch& L, uint32_t grid, void* stream) {
+    const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
+    grid = (grid + 1u) & ~1u;
+    k_persistent_pair<Body><<<grid, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, L);
+    return (int)cudaGetLastError();
+}
+
+// n virtual blocks on min(n, n_sms / 2) pairs.
+template <class Body>
+int launch_plain_pair(const void* blob, uint32_t offset, uint32_t n, void* stream) {
+    const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
+    if (n == 0) return 0;
+    static int n_sms = 0;
+    if (!n_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (n_sms < 2) n_sms = 2;
+    }
+    const uint32_t pairs = std::min(n, (uint32_t)(n_sms / 2));
+    k_plain_pair<Body><<<2 * pairs, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, offset, n);
     return (int)cudaGetLastError();
 }
 

@@ -1,47 +1,55 @@
 // kl_mm.cu -- MM ("Multiplying two dense matrices", 8192x2048 . 2048x2048) on the
-// 5th-generation tensor cores (product path).
+// 5th-generation tensor cores, one CTA PAIR per output tile (product path).
 //
-// One virtual thread block = one 128x256 fp32 output tile.  A persistent block (8 warps) pulls
-// tiles from the slice launcher and runs, per tile,
-//   warp 0 lane 0 : TMA producer  -- 128x64 (A) and 256x64 (B) bf16 tiles, 128B swizzle, into a
-//                   ring of kStages shared-memory stages, completion on mbarriers (expect_tx);
-//   warp 1 lane 0 : MMA issuer    -- tcgen05.mma.cta_group::1.kind::f16 (M=128, N=256, K=16) x4
-//                   per stage into one of two 256-column fp32 TMEM accumulators; tcgen05.commit
-//                   frees the stage; the last commit signals the epilogue;
-//   warps 4..7    : epilogue      -- drains the PREVIOUS tile's accumulator (tcgen05.ld
-//                   32x32b.x32, each warp its 32 TMEM lanes) while warps 0-1 run this tile's
-//                   mainloop; the last tile is drained in fini().  Warps 2-3 idle (8 warps keep
-//                   b*wpb divisible by the 4 schedulers: whole virtual-SM warps, R14).
-// The stage count is the kernel's occupancy knob (shared memory per block).
+// One virtual thread block = one 256x256 fp32 output tile computed by a CTA pair (a cluster of 2
+// on one TPC; kl_launcher.cuh k_persistent_pair): tcgen05.mma.cta_group::2 (M=256, N=256, K=16)
+// reads A's 256 rows as 128 rows from each CTA's shared memory and B's 256 columns as 128 rows
+// of Bt from each, and accumulates CTA r's 128 rows in CTA r's TMEM.  Per tile, in both CTAs,
+//   warp 0 lane 0 : TMA producer  -- its CTA's 128x64 (A) and 128x64 (B) bf16 tiles, 128B swizzle,
+//                   into a ring of S shared-memory stages; completion (.cta_group::2) on the
+//                   LEADER's full barrier, which expects both CTAs' bytes;
+//   warp 1 lane 0 : MMA issuer (leader only) -- 4 MMAs per stage into one of two 256-column fp32
+//                   accumulators; tcgen05.commit multicast frees the stage in both CTAs and, after
+//                   the last k-block, signals both CTAs' epilogues;
+//   warps 4..7    : epilogue -- drain the PREVIOUS tile's accumulator (tcgen05.ld 32x32b.x32, each
+//                   warp its 32 TMEM lanes) while warps 0-1 run this tile's mainloop.
+// Against one-CTA 128x256 tiles this halves the operand bytes each SM pulls from L2 per MMA
+// (the one-CTA kernel is L2-feed-bound at 48 % of the bf16 peak).  The per-tile cluster barrier of
+// the pair launcher orders accumulator reuse across the two CTAs.
+// The stage count S in {2, 3, 4, 6} (32 KiB of shared memory each) is the kernel's occupancy
+// knob: MM's occupancy levels; one instantiation per level.
 // Numerics: bf16 products are exact in fp32; only the fp32 accumulation order differs from the
 // oracle's fp64 sum (normwise tolerance).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include "kl_internal.h"
 #include "kl_launcher.cuh"
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64;
-#ifndef KL_MM_STAGES
-#define KL_MM_STAGES 4   // the stage count is a build knob: 2-4 (48 KiB of shared memory each)
-#endif
-constexpr int kStages = KL_MM_STAGES;
-static_assert(kStages >= 2 && kStages <= 4, "KL_MM_STAGES in [2, 4] (227 KB of shared memory per block)");
-constexpr int kStageBytes = (BM + BN) * BK * 2;          // 48 KiB
-constexpr int kBarOffset = kStages * kStageBytes;
-constexpr int kDynSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int kThreads = 256;   // 8 warps: whole warps per virtual SM (R14)
-constexpr uint32_t kTmemCols = 2 * BN;   // two fp32 accumulators: tile i's MMAs overlap tile i-1's epilogue
-// instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 256, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr int BM = 128;            // A rows per CTA (the pair's tile is 2*BM = 256 rows)
+constexpr int BN = 256;            // tile columns (the pair's N)
+constexpr int BNH = BN / 2;        // Bt rows per CTA
+constexpr int BK = 64;             // k per stage (one 128-byte swizzle atom of bf16)
+constexpr int kStageBytes = (BM + BNH) * BK * 2;   // 32 KiB per CTA
+constexpr int kThreads = 256;      // 8 warps: whole warps per virtual SM (R14)
+constexpr uint32_t kTmemCols = 2 * BN;             // two fp32 accumulators (tile i / epilogue of i-1)
+// instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 256, M = 256 (pair)
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+constexpr int kStageLevels[4] = {2, 3, 4, 6};
+
+constexpr int kEpiBox = 32;                        // C store box: 32 rows x 32 fp32 (128 B rows)
+constexpr int kEpiBufBytes = kEpiBox * kEpiBox * 4;  // 4 KiB
+constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;      // 4 epilogue warps x 2 buffers
 
 struct MMParams {
     CUtensorMap ta;   // A  [M][K] bf16, box 64 x 128
-    CUtensorMap tb;   // Bt [N][K] bf16, box 64 x 256
+    CUtensorMap tb;   // Bt [N][K] bf16, box 64 x 128
+    CUtensorMap tc;   // C  [M][N] fp32, box 32 x 32, 128B swizzle (TMA store epilogue)
     float* C;
     int32_t M, N, K;
 };
@@ -64,10 +72,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+// TMA 2-D load into this CTA's shared memory; completion bytes land on `bar_cluster` (a
+// shared::cluster address: the leader CTA's full barrier).
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"((uint64_t)map), "r"(bar_cluster), "r"(c0), "r"(c1)
         : "memory");
 }
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row core groups 1024 B apart.
@@ -80,15 +91,20 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
     d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
     return d;
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+// Arrive on the barrier at shared offset `bar` in both CTAs of the pair once the MMAs issued so
+// far complete.
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(bar)
+        : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -104,27 +120,34 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
                    "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])             \
                  : "r"(taddr))
 
+template <int S>
 struct BodyMM {
+    static_assert(S >= 2 && S <= 6, "stages");
     using Params = MMParams;
-    static constexpr int kThreads = ::kThreads, kChunk = 1, kDynSmem = ::kDynSmem;
+    static constexpr int kThreads = ::kThreads, kChunk = 1;
+    static constexpr int kDynSmem = S * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kEpiOffset = S * kStageBytes;
+    static constexpr int kBarOffset = S * kStageBytes + kEpiBytes;
     struct State {
         uint32_t base;      // 1024-aligned shared address of stage 0
         uint32_t bars;      // full[s] bars+8s, empty[s] bars+64+8s, tfull[b] bars+128+8b, tmem ptr bars+192
         uint32_t tmem;
+        uint32_t rank;      // rank in the CTA pair (0: leader, issues the MMAs)
         uint32_t stage, phase;
         uint32_t tph;       // per-accumulator wait parity bits
-        uint32_t ntile;     // tiles issued by this persistent block
+        uint32_t ntile;     // tiles issued by this persistent pair
         int prev_m, prev_n; // tile whose accumulator is still to be drained (-1: none)
     };
     __device__ static void init(const Params&, State& st, char* dsmem) {
         const uint32_t raw = smem_u32(dsmem);
         st.base = (raw + 1023u) & ~1023u;
         st.bars = st.base + kBarOffset;
+        st.rank = cluster_rank();
         st.stage = st.phase = st.tph = st.ntile = 0;
         st.prev_m = st.prev_n = -1;
         const int warp = threadIdx.x >> 5;
         if (threadIdx.x == 0) {
-            for (int s = 0; s < kStages; ++s) {
+            for (int s = 0; s < S; ++s) {
                 mbar_init(st.bars + 8 * s, 1);
                 mbar_init(st.bars + 64 + 8 * s, 1);
             }
@@ -133,45 +156,69 @@ struct BodyMM {
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        if (warp == 1) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(st.bars + 192),
+        if (warp == 1) {   // the same warp in both CTAs allocates the pair's columns
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(st.bars + 192),
                          "r"(kTmemCols));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
         }
         tc_fence_before();
-        __syncthreads();
+        cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
         tc_fence_after();
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(st.tmem) : "r"(st.bars + 192));
     }
-    // Epilogue warps: wait for tile (m, n)'s accumulator b, move it TMEM -> registers -> C.
+    __device__ static void before_pair_sync(State&) { tc_fence_before(); }
+    __device__ static void after_pair_sync(State&) { tc_fence_after(); }
+    // Epilogue warps: wait for tile (m, n)'s accumulator b and move this CTA's 128 rows TMEM ->
+    // registers -> shared memory (128B-swizzled 32x32 boxes, two buffers per warp) -> C by TMA
+    // bulk-tensor stores (whole 128-byte lines; a thread-per-row STG epilogue issues 32 partial
+    // sectors per instruction and was the launch's tail).
     __device__ static void drain(const Params& P, State& st, int m, int n, uint32_t b) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         mbar_wait(st.bars + 128 + 8 * b, (st.tph >> b) & 1u);
         tc_fence_after();
         const int q = warp & 3;                              // TMEM lane quarter of this warp
-        const int row = m * BM + q * 32 + lane;
-        float* crow = P.C + (size_t)row * P.N + (size_t)n * BN;
+        const int row0 = m * (2 * BM) + (int)st.rank * BM + q * 32;
         const uint32_t tbase = st.tmem + ((uint32_t)(q * 32) << 16) + b * BN;
+        const uint32_t ebuf = st.base + kEpiOffset + (uint32_t)q * 2u * kEpiBufBytes;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
             uint32_t r[32];
             TMEM_LD_X32(tbase + (uint32_t)c, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            float4* dst = reinterpret_cast<float4*>(crow + c);
+            const uint32_t buf = ebuf + (uint32_t)((c >> 5) & 1) * kEpiBufBytes;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // buf's last store read it
+            __syncwarp();
+#ifdef KL_MM_DBG_NOEPI      // A/B probe: no C stores
+            if (r[0] == 0x7fffffffu && r[1] == 0x7fffffffu)
+#endif
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-                dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t a = buf + (uint32_t)lane * 128u + (uint32_t)((j ^ (lane & 7)) * 16);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r[4 * j]), "r"(r[4 * j + 1]),
+                             "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                             : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)&P.tc),
+                    "r"(buf), "r"(n * BN + c), "r"(row0)
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
         }
         tc_fence_before();
     }
     __device__ static void fini(const Params& P, State& st, char*) {
         if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_n, (st.ntile - 1) & 1u);
+        if ((threadIdx.x >> 5) >= 4 && (threadIdx.x & 31) == 0)
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // C written before the kernel's end
         tc_fence_before();
-        __syncthreads();
+        cluster_sync_all();   // both CTAs drained: the pair's columns can go
         tc_fence_after();
         if ((threadIdx.x >> 5) == 1)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols));
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols));
     }
     __device__ static void block(const Params& P, State& st, char*, uint32_t vb) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,48 +229,61 @@ struct BodyMM {
         if (warp == 0) {
             if (lane == 0) {
                 uint32_t s = st.stage, ph = st.phase;
+                const int arow = tm * (2 * BM) + (int)st.rank * BM, brow = tn * BN + (int)st.rank * BNH;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(st.bars + 64 + 8 * s, ph ^ 1u);
                     const uint32_t full = st.bars + 8 * s;
                     const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
-                    mbar_expect_tx(full, kStageBytes);
-                    tma_load_2d(sa, &P.ta, full, kb * BK, tm * BM);
-                    tma_load_2d(sb, &P.tb, full, kb * BK, tn * BN);
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
+#ifdef KL_MM_DBG_NOTMA   // A/B probe: the MMAs on stale shared memory, no operand traffic
+                    if (st.rank == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+                    (void)sa; (void)sb; (void)arow; (void)brow;
+#else
+                    if (st.rank == 0) mbar_expect_tx(full, 2 * kStageBytes);   // both CTAs' bytes
+                    const uint32_t full_lead = map_rank(full, 0u);
+                    tma_load_2d_pair(sa, &P.ta, full_lead, kb * BK, arow);
+                    tma_load_2d_pair(sb, &P.tb, full_lead, kb * BK, brow);
+#endif
+                    if (++s == S) { s = 0; ph ^= 1u; }
                 }
             }
             __syncwarp();
         } else if (warp == 1) {
-            tc_fence_after();
-            if (lane == 0) {
-                uint32_t s = st.stage, ph = st.phase;
-                const uint32_t tacc = st.tmem + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
-                    mbar_wait(st.bars + 8 * s, ph);
-                    tc_fence_after();
-                    const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
+            if (st.rank == 0) {
+                tc_fence_after();
+                if (lane == 0) {
+                    uint32_t s = st.stage, ph = st.phase;
+                    const uint32_t tacc = st.tmem + acc * BN;
+                    for (int kb = 0; kb < nk; ++kb) {
+                        mbar_wait(st.bars + 8 * s, ph);
+                        tc_fence_after();
+                        const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
+#ifndef KL_MM_DBG_NOMMA   // A/B probe: operand traffic only
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), kIdesc,
-                                  (kb | k) != 0 ? 1u : 0u);
-                    umma_commit(st.bars + 64 + 8 * s);       // stage free once these MMAs finish
-                    if (++s == kStages) { s = 0; ph ^= 1u; }
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_bf16_pair(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), kIdesc,
+                                           (kb | k) != 0 ? 1u : 0u);
+#else
+                        (void)sa; (void)sb; (void)tacc;
+#endif
+                        umma_commit_pair(st.bars + 64 + 8 * s);   // stage free in both CTAs
+                        if (++s == S) { s = 0; ph ^= 1u; }
+                    }
+                    umma_commit_pair(st.bars + 128 + 8 * acc);    // accumulator `acc` complete
                 }
-                umma_commit(st.bars + 128 + 8 * acc);        // accumulator `acc` complete
+                __syncwarp();
             }
-            __syncwarp();
         } else if (warp >= 4 && st.prev_m >= 0) {
             drain(P, st, st.prev_m, st.prev_n, acc ^ 1u);    // previous tile, other accumulator
         }
         // every role advances the shared pipeline state identically
         for (int kb = 0; kb < nk; ++kb)
-            if (++st.stage == kStages) { st.stage = 0; st.phase ^= 1u; }
+            if (++st.stage == S) { st.stage = 0; st.phase ^= 1u; }
         if (st.prev_m >= 0) st.tph ^= 1u << (acc ^ 1u);    // that accumulator's wait was consumed
         st.prev_m = tm;
         st.prev_n = tn;
         st.ntile++;
         tc_fence_before();
-        __syncthreads();   // the drained accumulator is free before the next tile's first MMA
+        __syncthreads();
         tc_fence_after();
     }
 };
@@ -257,25 +317,58 @@ bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t k, 
     return r == CUDA_SUCCESS;
 }
 
+// C [rows][cols] fp32, box 32 x 32, 128B swizzle (the epilogue's staging layout).
+bool encode_c(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols) {
+    auto fn = get_encode();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kEpiBox, (cuuint32_t)kEpiBox};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Stage count of a launch: L.variant names it (0 = the default, the deepest ring).
+int stages_of(uint32_t variant) {
+    for (int v : kStageLevels)
+        if ((int)variant == v) return v;
+    return 6;
+}
+
 }  // namespace
+
+int kl_mm_stage_smem(int stages) {     // dynamic shared memory of one CTA at `stages`
+    return stages * kStageBytes + kEpiBytes + 1024 + 256;
+}
 
 int kl_mm_info(KlKindInfo* o) {
     if (!get_encode()) return -3;
-    int rc = info_of<BodyMM>(o);
+    int rc = 0;
+    KlKindInfo tmp;
+    // every instantiation's attributes are set (dynamic shared memory opt-in) at load time
+    if ((rc = info_of_pair<BodyMM<2>>(&tmp)) || (rc = info_of_pair<BodyMM<3>>(&tmp)) ||
+        (rc = info_of_pair<BodyMM<4>>(&tmp)))
+        return rc;
+    rc = info_of_pair<BodyMM<6>>(o);
     if (rc) return rc;
     o->tmem_cols = (int)kTmemCols;
+    o->dyn_smem = kl_mm_stage_smem(2);   // the kind's profile: its shallowest ring (the runtime
+                                         // picks each launch's depth, kl_runtime.cpp variant_of)
     return 0;
 }
 
 int kl_mm_prepare(const void* args, uint32_t bytes, uint32_t grid, void* blob, uint32_t cap) {
     if (bytes != sizeof(kl_args_mm) || cap < sizeof(MMParams)) return -1;
     const kl_args_mm& a = *reinterpret_cast<const kl_args_mm*>(args);
-    if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.M % BM || a.N % BN || a.K % BK) return -1;
-    if ((uint64_t)grid > (uint64_t)(a.M / BM) * (uint64_t)(a.N / BN)) return -1;   // one tile per block
+    if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.M % (2 * BM) || a.N % BN || a.K % BK) return -1;
+    if ((uint64_t)grid > (uint64_t)(a.M / (2 * BM)) * (uint64_t)(a.N / BN)) return -1;   // one tile per block
     MMParams p;
     std::memset(&p, 0, sizeof p);
     if (!encode_kmajor(&p.ta, a.A, (uint64_t)a.M, (uint64_t)a.K, BM)) return -1;
-    if (!encode_kmajor(&p.tb, a.Bt, (uint64_t)a.N, (uint64_t)a.K, BN)) return -1;
+    if (!encode_kmajor(&p.tb, a.Bt, (uint64_t)a.N, (uint64_t)a.K, BNH)) return -1;
+    if (!encode_c(&p.tc, a.C, (uint64_t)a.M, (uint64_t)a.N)) return -1;
     p.C = a.C;
     p.M = a.M;
     p.N = a.N;
@@ -285,9 +378,16 @@ int kl_mm_prepare(const void* args, uint32_t bytes, uint32_t grid, void* blob, u
 }
 
 int kl_mm_launch_persistent(const void* blob, const KlLaunch& L, uint32_t grid, void* stream) {
-    return launch_persistent<BodyMM>(blob, L, grid, stream);
+    // a short remainder (uncapped launch sized to the remaining tiles) still gets two CTAs per tile
+    if (grid < L.n_sms) grid = std::min(2u * grid, L.n_sms);
+    switch (stages_of(L.variant)) {
+        case 2: return launch_persistent_pair<BodyMM<2>>(blob, L, grid, stream);
+        case 3: return launch_persistent_pair<BodyMM<3>>(blob, L, grid, stream);
+        case 4: return launch_persistent_pair<BodyMM<4>>(blob, L, grid, stream);
+        default: return launch_persistent_pair<BodyMM<6>>(blob, L, grid, stream);
+    }
 }
 
 int kl_mm_launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream) {
-    return launch_plain<BodyMM>(blob, offset, n, stream);
+    return launch_plain_pair<BodyMM<6>>(blob, offset, n, stream);
 }

@@ -30,6 +30,7 @@
 
 uint32_t kl_args_size(int kind);
 int kl_dev_ctl_init(KlCtl* pool, const uint32_t* slots_lens, int n, unsigned long long* counters, void* stream);
+int kl_mm_stage_smem(int stages);
 
 namespace {
 
@@ -89,6 +90,7 @@ struct Launch {
     std::vector<int> topup_streams;   // streams of top-up grids of this epoch
     uint32_t cap = 0, slice = 0, epoch = 0;
     uint32_t cap_max = 0;             // 0 = uncapped at some point
+    uint32_t variant = 0;             // MM: TMA ring stages of this launch
     bool stop_requested = false;
     KlLaunch params{};
     int32_t decision = 0, partner_kind = -1;
@@ -294,6 +296,29 @@ std::vector<std::pair<uint32_t, uint32_t>> maximal_splits(const kl_ctx* c, const
     return out;
 }
 
+// MM's occupancy level (reading R28): the TMA ring depth of its CTA pairs.  The
+// model sees MM at one block per SM whatever the depth (its warps do not change); the engine
+// gives each launch the deepest ring whose shared memory fits beside the partner's blocks (the
+// feasibility of the pair itself is decided at the shallowest ring, the kind's profile smem).
+uint32_t variant_of(const kl_ctx* c, int kind, int partner_kind, uint32_t partner_b) {
+    if (kind != KL_MM) return 0;
+    if (c->cfg.mm_stages) return (uint32_t)c->cfg.mm_stages;
+    static const int kLevels[4] = {6, 4, 3, 2};
+    kl_profile pm = c->prof[KL_MM];
+    const KlKindInfo& in = c->info[KL_MM];
+    for (int s : kLevels) {
+        pm.smem = in.static_smem + kl_mm_stage_smem(s);
+        if (partner_kind < 0) {
+            if (fits(c, pm, 1, nullptr, 0) == 0) return (uint32_t)s;
+            continue;
+        }
+        const kl_profile& pp = c->prof[partner_kind];
+        const uint32_t pb = partner_b ? partner_b : (uint32_t)std::max(1, pp.bmax);
+        if (fits(c, pm, 1, &pp, pb) == 0) return (uint32_t)s;
+    }
+    return 2;
+}
+
 bool pruned(const kl_profile& a, const kl_profile& b, double ap, double am) {
     return std::fabs(a.pur - b.pur) < ap && std::fabs(a.mur - b.mur) < am;   // R9: AND, strict
 }
@@ -366,7 +391,8 @@ const std::vector<std::pair<uint32_t, uint32_t>>& splits_of(kl_ctx* c, int k1, i
     return c->splits[k1][k2];
 }
 
-kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp);
+kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp,
+                        uint32_t variant = 0);
 uint32_t slice_of(const kl_ctx* c, uint32_t b, int m);
 
 // The general model kernel (kl_model3.cu) serves three-state kinds and block granularity.
@@ -438,7 +464,8 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* 
         for (uint32_t b = 1; b <= (uint32_t)std::max(1, p0.bmax); ++b)
             if (fits(ctx, p0, b, &model_cta, 1) == 0) cap = b;
         if (cap) {
-            kl_status st = launch_kernel(ctx, spec, cap, slice_of(ctx, cap, 1), -1, 0.0);
+            kl_status st = launch_kernel(ctx, spec, cap, slice_of(ctx, cap, 1), -1, 0.0,
+                                         variant_of(ctx, spec->kind, -1, 0) ? 2u : 0u);
             if (st) return st;
             ctx->st.speculative++;
         }
@@ -676,7 +703,8 @@ int pick_stream(kl_ctx* ctx) {
     return best;
 }
 
-kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp) {
+kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int partner_kind, double cp,
+                        uint32_t variant) {
     if (ctx->free_recs.empty()) return ctx->fail(KL_ENOMEM, "launch record ring exhausted");
     const KlKindInfo& inf = ctx->info[k->kind];
     auto L = std::make_unique<Launch>();
@@ -691,6 +719,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     L->decision = (int32_t)ctx->st.decisions;
     L->partner_kind = partner_kind;
     L->cp = cp;
+    L->variant = variant;
     KlLaunchRec* rec = ctx->recs + L->rec;
     std::memset(rec, 0, sizeof(*rec));
     KlLaunch P{};
@@ -704,6 +733,7 @@ kl_status launch_kernel(kl_ctx* ctx, Inst* k, uint32_t cap, uint32_t slice, int 
     P.audit = k->audit;
     P.stamps = k->stamps;
     P.tag = k->tag;
+    P.variant = variant;
     // grid: cap blocks per SM plus slack, so SMs whose slots free up late (the predecessor's tail
     // blocks) still receive their share; surplus blocks fail admission and exit at once
     const uint32_t per_sm = cap ? cap : (uint32_t)std::max(1, inf.bmax);
@@ -818,14 +848,14 @@ kl_status reconcile(kl_ctx* ctx) {
     if (!ctx->have_desired) return KL_OK;
     const Decision& d = ctx->desired;
     const int m = waves_of(ctx, d);
-    struct Want { Inst* k; uint32_t cap, slice; int partner; };
+    struct Want { Inst* k; uint32_t cap, slice; int partner; uint32_t variant; };
     Want w[2];
     int nw = 0;
     if (d.solo) {
-        w[nw++] = {d.k1, 0u, slice_of(ctx, d.b1, m), -1};
+        w[nw++] = {d.k1, 0u, slice_of(ctx, d.b1, m), -1, variant_of(ctx, d.k1->kind, -1, 0)};
     } else {
-        w[nw++] = {d.k1, d.b1, slice_of(ctx, d.b1, m), d.k2->kind};
-        w[nw++] = {d.k2, d.b2, slice_of(ctx, d.b2, m), d.k1->kind};
+        w[nw++] = {d.k1, d.b1, slice_of(ctx, d.b1, m), d.k2->kind, variant_of(ctx, d.k1->kind, d.k2->kind, d.b2)};
+        w[nw++] = {d.k2, d.b2, slice_of(ctx, d.b2, m), d.k1->kind, variant_of(ctx, d.k2->kind, d.k1->kind, d.b1)};
     }
     for (auto& Lp : ctx->inflight) {
         Launch* L = Lp.get();
@@ -833,7 +863,9 @@ kl_status reconcile(kl_ctx* ctx) {
         int want = -1;
         for (int i = 0; i < nw; ++i)
             if (w[i].k == L->k) want = i;
-        if (want < 0) {
+        if (want < 0 || L->variant > w[want].variant) {
+            // not wanted, or its shared memory (MM's ring) does not fit beside the new partner:
+            // stop at the next fetch and relaunch at the wanted level
             kl_status st = request_stop(ctx, L);
             if (st) return st;
         } else if (w[want].cap != L->cap) {
@@ -844,7 +876,7 @@ kl_status reconcile(kl_ctx* ctx) {
     for (int i = 0; i < nw; ++i) {
         Inst* k = w[i].k;
         if (k->drained || k->inflight) continue;   // running as wanted, or stopping: relaunch later
-        kl_status st = launch_kernel(ctx, k, w[i].cap, w[i].slice, w[i].partner, d.cp);
+        kl_status st = launch_kernel(ctx, k, w[i].cap, w[i].slice, w[i].partner, d.cp, w[i].variant);
         if (st) return st;
     }
     return KL_OK;
@@ -926,6 +958,7 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
         t.cp = L->cp;
         t.cap_max = L->cap_max;
         t.grids = 1u + (uint32_t)L->topup_streams.size();
+        t.variant = L->variant;
         ctx->trace.push_back(t);
         k->next = r->end;
         k->inflight = nullptr;
@@ -1076,6 +1109,8 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
     else kl_config_default(&ctx->cfg);
     kl_config& cfg = ctx->cfg;
     if (cfg.n_sched <= 0 || 64 % cfg.n_sched) return KL_EINVAL;
+    if (cfg.mm_stages && cfg.mm_stages != 2 && cfg.mm_stages != 3 && cfg.mm_stages != 4 && cfg.mm_stages != 6)
+        return KL_EINVAL;
     for (int k = 0; k < KL_NKINDS; ++k) ctx->prof[k] = cfg.profiles ? cfg.profiles[k] : kDefaultProfiles[k];
     cfg.profiles = nullptr;
     ctx->device = device;
@@ -1420,7 +1455,7 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     int si = pick_stream(ctx);
     KL_CUDA(cudaEventRecord(e0, ctx->pool[si]));
     ctx->pool_busy[si] -= 1000;            // launch_kernel picks the least busy stream: this one
-    st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0);
+    st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0, variant_of(ctx, k->kind, -1, 0));
     ctx->pool_busy[si] += 1000;
     if (st) return st;
     KL_CUDA(cudaEventRecord(e1, ctx->pool[k->inflight->stream]));
@@ -1453,8 +1488,10 @@ kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, cons
     st = flush_ctl_init(ctx);
     if (st) return st;
     const size_t t0 = ctx->trace.size();
-    st = launch_kernel(ctx, k1, cap1, slice_of(ctx, cap1 ? cap1 : 1, 1), k2->kind, 0.0);
-    if (!st) st = launch_kernel(ctx, k2, cap2, slice_of(ctx, cap2 ? cap2 : 1, 1), k1->kind, 0.0);
+    st = launch_kernel(ctx, k1, cap1, slice_of(ctx, cap1 ? cap1 : 1, 1), k2->kind, 0.0,
+                       variant_of(ctx, k1->kind, k2->kind, cap2));
+    if (!st) st = launch_kernel(ctx, k2, cap2, slice_of(ctx, cap2 ? cap2 : 1, 1), k1->kind, 0.0,
+                                variant_of(ctx, k2->kind, k1->kind, cap1));
     if (st) return st;
     bool stopped = false;
     uint64_t spins = 0;

@@ -146,12 +146,12 @@ def test_mriq_zero_k_closed_form(ctx):
 
 
 # ---- paths the SMALL sizes never reach -------------------------------------------------------
-# MM at SMALL is 3 output tiles with K/64 = 3 k-blocks: no CTA processes a second tile, the TMA
-# ring never wraps and the second TMEM accumulator is never used.  These sizes (P:1143's kernel,
-# shrunk so the plain-C oracle finishes in seconds) give 160 output tiles (> 148 SMs) and
-# K/64 = 8 k-blocks (> every ring depth), and the capped launches on a context restricted to a
-# few SMs make each persistent CTA loop over ~10 tiles (both accumulators, ring phase flips, the
-# overlapped epilogue of tile i-1 during tile i).
+# MM at SMALL is 2 pair tiles with K/64 = 3 k-blocks: no CTA pair processes a second tile, the
+# TMA ring never wraps and the second TMEM accumulator is never used.  These sizes (P:1143's
+# kernel, shrunk so the plain-C oracle finishes in seconds) give 80 256x256 pair tiles (> 74 CTA
+# pairs on 148 SMs) and K/64 = 8 k-blocks (> every ring depth), and the capped launches on a
+# context restricted to a few SMs make each persistent pair loop over ~20 tiles (both
+# accumulators, ring phase flips, the overlapped epilogue of tile i-1 during tile i).
 MM_BIG = dict(M=2560, N=2048, K=512)
 
 
@@ -199,6 +199,49 @@ def test_mm_multi_tile_persistent(mm_big, mode, n_sms, cap):
         assert np.array_equal(res["C"], ref["C"])
     else:
         compare("MM", res, ref)
+
+
+@pytest.mark.parametrize("stages", [2, 3, 4, 6])
+def test_mm_stage_levels(mm_big, stages):
+    """MM's occupancy levels are its TMA ring depths (separate instantiations, kl_config.mm_stages):
+    every level is bit-exact in integer mode against the oracle on every element, through the
+    persistent pair launcher on a restricted context (many tiles per pair: K/64 = 8 k-blocks wrap
+    the 2- to 6-stage rings), and the launch record names the level."""
+    d, ref = mm_big["int"]
+    with K.Context(device=0, audit=1, n_sms=16, mm_stages=stages) as c:
+        inst = Instance(d, "cuda")
+        for o in inst.outputs.values():
+            o.fill_(0)
+        torch.cuda.synchronize()
+        c.run_capped("MM", inst.grid, inst.args, 1)
+        res = inst.result()
+        assert c.trace()[-1].variant == stages
+    assert np.array_equal(res["C"], ref["C"])
+
+
+def test_mm_ring_fits_beside_the_partner():
+    """Beside a partner the engine gives MM the deepest ring whose shared memory fits next to the
+    partner's blocks (reading R28): the chosen level fits the SM's shared memory with the
+    partner's cap, the next deeper one does not, and MM's output is exact."""
+    dm = G.gen("MM", "small", mode="int")
+    refm = O.run_kernel(dm)
+    smem_sm = torch.cuda.get_device_properties(0).shared_memory_per_multiprocessor
+    for partner, cap in (("ST", 8), ("SAD", 8), ("PC", 2), ("ST", 1)):   # feasible in warps and registers
+        dp = G.gen(partner, "small")
+        with K.Context(device=0, audit=1) as c:
+            pm, pp = c.get_profile("MM"), c.get_profile(partner)
+            im, ip = Instance(dm, "cuda"), Instance(dp, "cuda")
+            torch.cuda.synchronize()
+            recs = c.run_pair("MM", im.grid, im.args, 1, partner, ip.grid, ip.args, cap)
+            var = recs[0].variant
+            res = im.result()
+        assert var in (2, 3, 4, 6)
+        mm_smem = lambda s: pm.smem + (s - 2) * 32768 + 1024     # profile smem = the 2-stage ring
+        other = cap * (pp.smem + 1024)
+        assert mm_smem(var) + other <= smem_sm, (partner, cap, var)
+        if var < 6:
+            assert mm_smem({2: 3, 3: 4, 4: 6}[var]) + other > smem_sm, (partner, cap, var)
+        assert np.array_equal(res["C"], refm["C"])
 
 
 @pytest.mark.parametrize("nx", [260, 300, 388])

@@ -116,7 +116,7 @@ def test_stencil_parboil_constant_field():
 
 def test_mm_integer_exact():
     d = G.gen("MM", "small", mode="int")
-    C = O.run_kernel(d)["C"].reshape(384, 256)
+    C = O.run_kernel(d)["C"].reshape(512, 256)
     A = (d["A"].astype(np.uint32) << 16).view(np.float32).astype(np.int64)
     Bt = (d["Bt"].astype(np.uint32) << 16).view(np.float32).astype(np.int64)
     assert np.array_equal(C.astype(np.int64), A @ Bt.T)
