@@ -65,15 +65,94 @@ __device__ __forceinline__ uint32_t vsad4(uint32_t a, uint32_t b, uint32_t c) {
 struct BodySAD {
     using Params = kl_args_sad;
     using State = Empty;
-    static constexpr int kThreads = 32, kChunk = 1, kDynSmem = 0;
+    // 32 one-warp blocks per SM (the block limit) at <= 64 registers.  The round-1 body kept the
+    // whole 16x16 current macroblock (64 words) and 33 accumulators in registers: 128 registers,
+    // 16 resident warps, too few to cover the window loads (ncu: alu pipe 53 %, long-scoreboard
+    // stalls).  Here each of two passes holds half the macroblock's rows (32 words) and a ring of
+    // 8 accumulators; pass 0 parks its partial sums in shared memory, pass 1 adds them.
+    // Four warps per block, each on its own macroblock: a fetched chunk of 4 virtual blocks runs
+    // together (block_range), so the launcher's per-block join / fetch / leave atomics are paid
+    // once per 4 macroblocks (with one-warp blocks they cost +50 % against the plain grid).
+    static constexpr int kThreads = 128, kChunk = 4, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
-    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        __shared__ uint32_t win[48 * 12];
-        __shared__ uint32_t curs[64];
+    // One pass over macroblock rows r in [8H, 8H + 8) (cur: their 32 words).  Lane l =
+    // displacement column dx = l; SAD(dx, dy) gets the row term S(y, r) of window row y = dy + r.
+    // Window row y feeds dy = y - r for the pass's 8 rows, so 8 accumulators in a ring indexed by
+    // dy mod 8 suffice; the one for dy = y - (8H + 7) is complete after row y.  The 40 window rows
+    // come in 5 phases of 8 (only the first and last phase have invalid (y, r) pairs), so every
+    // ring index and validity test is a compile-time constant.
+    template <int H, int P>
+    __device__ static void phase(const uint32_t* win, const uint32_t (&cur)[32], int lane, uint32_t (&ring)[8],
+                                 uint16_t* part, uint16_t* o) {
+        const int wo = lane >> 2, sh = (lane & 3) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int y = 8 * H + 8 * P + j;
+            const uint32_t* row = win + y * 12 + wo;
+            const uint32_t w0 = row[0], w1 = row[1], w2 = row[2], w3 = row[3], w4 = row[4];
+            const uint32_t q0 = __funnelshift_r(w0, w1, sh), q1 = __funnelshift_r(w1, w2, sh);
+            const uint32_t q2 = __funnelshift_r(w2, w3, sh), q3 = __funnelshift_r(w3, w4, sh);
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+                const bool valid = (P == 0) ? (rr <= j) : (P == 4) ? (rr >= j) : true;   // 0 <= dy <= 32
+                if (valid) {
+                    uint32_t& acc = ring[(j - rr + 8) & 7];
+                    uint32_t s = vsad4(q0, cur[rr * 4 + 0], acc);
+                    s = vsad4(q1, cur[rr * 4 + 1], s);
+                    s = vsad4(q2, cur[rr * 4 + 2], s);
+                    acc = vsad4(q3, cur[rr * 4 + 3], s);
+                }
+            }
+            const int dy = 8 * P + j - 7;                  // complete: all 8 rows of the pass added
+            if (dy >= 0) {
+                uint32_t& acc = ring[(j + 1) & 7];         // dy mod 8
+                if (H == 0) part[dy * 32 + lane] = (uint16_t)acc;                 // <= 8*16*255
+                else o[dy * 33 + lane] = (uint16_t)(acc + part[dy * 32 + lane]);  // <= 65280
+                acc = 0;
+            }
+        }
+    }
+    template <int H>
+    __device__ static uint32_t half(const uint32_t* win, const uint32_t* curw, int lane, uint16_t* part, uint16_t* o,
+                                    uint32_t col) {
+        uint32_t cur[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) cur[i] = curw[H * 32 + i];
+        uint32_t ring[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ring[i] = 0;
+        phase<H, 0>(win, cur, lane, ring, part, o);
+        phase<H, 1>(win, cur, lane, ring, part, o);
+        phase<H, 2>(win, cur, lane, ring, part, o);
+        phase<H, 3>(win, cur, lane, ring, part, o);
+        phase<H, 4>(win, cur, lane, ring, part, o);
+        // displacement column dx = 32 (lane l: dy = l; lane 0 also dy = 32 in the high half)
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+            const uint32_t* row = win + (lane + 8 * H + rr) * 12 + 8;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) col = vsad4(row[i], cur[rr * 4 + i], col);
+        }
+        return col;
+    }
+    __device__ static void block_range(const Params& a, State& st, char* d, uint32_t v0, uint32_t v1) {
+        const uint32_t v = v0 + (threadIdx.x >> 5);
+        if (v < v1) macroblock(a, v);
+    }
+    __device__ static void block(const Params& a, State& st, char* d, uint32_t vb) { block_range(a, st, d, vb, vb + 1); }
+    // One warp: macroblock vb (its own slice of the block's shared memory).
+    __device__ static void macroblock(const Params& a, uint32_t vb) {
+        __shared__ uint32_t win_all[4][48 * 12];
+        __shared__ uint32_t curw_all[4][64];
+        __shared__ uint16_t part_all[4][33 * 32];
+        const int wid = threadIdx.x >> 5;
+        uint32_t* win = win_all[wid];
+        uint32_t* curw = curw_all[wid];
+        uint16_t* part = part_all[wid];
         const int W = a.width, H = a.height, mbw = W / 16, n_mb = mbw * (H / 16);
         if ((int)vb >= n_mb) return;   // padding blocks of the paper's 8048-block grid
-        const int lane = threadIdx.x;
+        const int lane = threadIdx.x & 31;
         const int mx = vb % mbw, my = vb / mbw;
         const int x0 = mx * 16 - 16, y0 = my * 16 - 16;
         const bool inner = (x0 >= 0) && (x0 + 48 <= W) && (y0 >= 0) && (y0 + 48 <= H);
@@ -93,78 +172,52 @@ struct BodySAD {
             }
         }
         for (int i = lane; i < 64; i += 32)
-            curs[i] = *reinterpret_cast<const uint32_t*>(a.cur + (size_t)(my * 16 + i / 4) * W + mx * 16 + (i % 4) * 4);
+            curw[i] = *reinterpret_cast<const uint32_t*>(a.cur + (size_t)(my * 16 + i / 4) * W + mx * 16 + (i % 4) * 4);
         __syncwarp();
-        uint32_t cur[64];
-#pragma unroll
-        for (int i = 0; i < 64; ++i) cur[i] = curs[i];
-        uint32_t acc[33];
-#pragma unroll
-        for (int i = 0; i < 33; ++i) acc[i] = 0;
-        const int wo = lane >> 2, sh = (lane & 3) * 8;
-#pragma unroll
-        for (int y = 0; y < 48; ++y) {
-            const uint32_t* row = win + y * 12 + wo;
-            uint32_t w0 = row[0], w1 = row[1], w2 = row[2], w3 = row[3], w4 = row[4];
-            uint32_t q0 = __funnelshift_r(w0, w1, sh), q1 = __funnelshift_r(w1, w2, sh);
-            uint32_t q2 = __funnelshift_r(w2, w3, sh), q3 = __funnelshift_r(w3, w4, sh);
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const int dy = y - r;
-                if (dy >= 0 && dy <= 32) {
-                    uint32_t s = vsad4(q0, cur[r * 4 + 0], acc[dy]);
-                    s = vsad4(q1, cur[r * 4 + 1], s);
-                    s = vsad4(q2, cur[r * 4 + 2], s);
-                    acc[dy] = vsad4(q3, cur[r * 4 + 3], s);
-                }
-            }
-        }
         uint16_t* o = a.out + (size_t)vb * 1089;
-#pragma unroll
-        for (int dy = 0; dy < 33; ++dy) o[dy * 33 + lane] = (uint16_t)acc[dy];
-        // displacement column dx = 32: lane l computes dy = l, lane 0 also dy = 32
-        for (int dy = lane; dy < 33; dy += 32) {
+        uint32_t col = half<0>(win, curw, lane, part, o, 0u);
+        __syncwarp();
+        col = half<1>(win, curw, lane, part, o, col);
+        o[lane * 33 + 32] = (uint16_t)col;
+        if (lane == 0) {               // dy = 32 of column dx = 32
             uint32_t s = 0;
+#pragma unroll 4
+            for (int r = 0; r < 16; ++r)
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const uint32_t* row = win + (dy + r) * 12 + 8;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) s = vsad4(row[i], cur[r * 4 + i], s);
-            }
-            o[dy * 33 + 32] = (uint16_t)s;
+                for (int i = 0; i < 4; ++i) s = vsad4(win[(32 + r) * 12 + 8 + i], curw[r * 4 + i], s);
+            o[32 * 33 + 32] = (uint16_t)s;
         }
         __syncwarp();
     }
 };
 
-// SPMV (CUSP CSR-vector): 8 rows per block, the paper's unit of work.
-#ifndef KL_SPMV_LANES
-#define KL_SPMV_LANES 32
-#endif
-// KL_SPMV_LANES lanes per row (rows hold 8-24 nonzeros), lane-strided products, butterfly
-// reduction inside the row's lane group.  At this size the kernel is latency-bound (row pointer
-// -> column -> x gather -> reduce per row), so rows in flight is what counts for a plain grid:
-// 8 lanes per row (2-warp blocks, 32 blocks = 256 rows per SM) take it 28.4 -> 22.7 us, but
-// through the persistent launcher 38 -> 43 us -- twice the blocks means twice the epoch joins
-// and fetches on the kernel's control words -- so the product keeps a warp per row.
+// SPMV (CUSP CSR-vector): 8 rows per virtual block, the paper's unit of work.  At this
+// size the kernel is latency-bound (row pointer -> column -> x gather -> reduce per row), so rows
+// in flight is what counts.  A block runs a whole fetched chunk of 8 virtual blocks (64 rows)
+// together, 4 lanes per row (rows hold 8-24 nonzeros: 2-6 per lane), lane-strided products and a
+// butterfly inside the row's lane group -- 8x the rows in flight of a warp per row, with the same
+// number of blocks, joins and fetches (round 1: more, smaller blocks lost their gain to the
+// launcher's per-block costs).  A row's arithmetic never depends on the grouping.
 struct BodySPMV {
     using Params = kl_args_spmv;
     using State = Empty;
-    static constexpr int kLanes = KL_SPMV_LANES;
-    static_assert(kLanes == 8 || kLanes == 16 || kLanes == 32, "lanes per row");
-    static constexpr int kThreads = 8 * kLanes, kChunk = 8, kDynSmem = 0, kMinBlocks = 2048 / kThreads > 32 ? 32 : 2048 / kThreads;
+    static constexpr int kLanes = 4;
+    static constexpr int kThreads = 256, kChunk = 8, kDynSmem = 0, kMinBlocks = 8;
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
-    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
-        const int row = (int)vb * 8 + (int)(threadIdx.x / kLanes), lane = threadIdx.x % kLanes;
-        const bool live = row < a.n_rows;   // no early return: the whole warp takes the shuffles
+    __device__ static void block_range(const Params& a, State&, char*, uint32_t v0, uint32_t v1) {
+        const int r_local = (int)(threadIdx.x / kLanes), lane = (int)(threadIdx.x % kLanes);
+        const int row = (int)v0 * 8 + r_local;
+        const bool live = r_local < (int)(v1 - v0) * 8 && row < a.n_rows;   // the warp takes the shuffles
         const int s = live ? __ldg(a.rowptr + row) : 0, e = live ? __ldg(a.rowptr + row + 1) : 0;
         float sum = 0.f;
+#pragma unroll 2
         for (int j = s + lane; j < e; j += kLanes) sum = fmaf(__ldg(a.vals + j), __ldg(a.x + __ldg(a.cols + j)), sum);
-#pragma unroll
-        for (int o = kLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (live && lane == 0) a.y[row] = sum;
     }
+    __device__ static void block(const Params& a, State& st, char* d, uint32_t vb) { block_range(a, st, d, vb, vb + 1); }
 };
 
 // ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z

@@ -241,6 +241,14 @@ struct min_blocks { static constexpr int value = 0; };   // 0 = unspecified
 template <class B>
 struct min_blocks<B, std::void_t<decltype(B::kMinBlocks)>> { static constexpr int value = B::kMinBlocks; };
 
+// Optional Body::block_range(P, st, dsmem, v0, v1): the body runs a fetched chunk of virtual
+// blocks [v0, v1) together (more independent work in flight per block: SPMV's rows); the
+// per-block result must not depend on how the range is grouped (sliced == unsliced).
+template <class B, class = void>
+struct has_range : std::false_type {};
+template <class B>
+struct has_range<B, std::void_t<decltype(&B::block_range)>> : std::true_type {};
+
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, min_blocks<Body>::value)
 k_persistent(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
@@ -314,11 +322,23 @@ k_persistent(const __grid_constant__ typename Body::Params P, const __grid_const
             __syncthreads();
             const uint32_t vb = s_vb[it & 1], end = s_end[it & 1];
             if (vb >= end) break;
-            for (uint32_t v = vb; v < end; ++v) {
-                if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v] = gtimer();
-                Body::block(P, st, dsmem, v);
-                if (L.audit && threadIdx.x == 0) atomicAdd(L.audit + v, 1u);
-                if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v + 1] = gtimer();
+            if constexpr (has_range<Body>::value) {
+                const unsigned long long t_a = (L.stamps && threadIdx.x == 0) ? gtimer() : 0ull;
+                Body::block_range(P, st, dsmem, vb, end);
+                if (threadIdx.x == 0) {
+                    const unsigned long long t_b = L.stamps ? gtimer() : 0ull;
+                    for (uint32_t v = vb; v < end; ++v) {
+                        if (L.audit) atomicAdd(L.audit + v, 1u);
+                        if (L.stamps) { L.stamps[2 * (size_t)v] = t_a; L.stamps[2 * (size_t)v + 1] = t_b; }
+                    }
+                }
+            } else {
+                for (uint32_t v = vb; v < end; ++v) {
+                    if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v] = gtimer();
+                    Body::block(P, st, dsmem, v);
+                    if (L.audit && threadIdx.x == 0) atomicAdd(L.audit + v, 1u);
+                    if (L.stamps && threadIdx.x == 0) L.stamps[2 * (size_t)v + 1] = gtimer();
+                }
             }
             nexec += end - vb;
         }
@@ -507,14 +527,20 @@ k_plain_pair(const __grid_constant__ typename Body::Params P, uint32_t offset, u
     Body::fini(P, st, dsmem);
 }
 
-// Plain grid: blockIdx rectified by the slice offset.
+// Plain grid: blockIdx rectified by the slice offset.  A body with block_range
+// runs kChunk virtual blocks per grid block (the same grouping as a persistent fetch).
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads)
-k_plain(const __grid_constant__ typename Body::Params P, uint32_t offset) {
+k_plain(const __grid_constant__ typename Body::Params P, uint32_t offset, uint32_t n) {
     extern __shared__ __align__(1024) char dsmem[];
     typename Body::State st;
     Body::init(P, st, dsmem);
-    Body::block(P, st, dsmem, offset + blockIdx.x);
+    if constexpr (has_range<Body>::value) {
+        const uint32_t v0 = blockIdx.x * (uint32_t)Body::kChunk;
+        Body::block_range(P, st, dsmem, offset + v0, offset + min(n, v0 + (uint32_t)Body::kChunk));
+    } else {
+        Body::block(P, st, dsmem, offset + blockIdx.x);
+    }
     Body::fini(P, st, dsmem);
 }
 
@@ -602,7 +628,8 @@ template <class Body>
 int launch_plain(const void* blob, uint32_t offset, uint32_t n, void* stream) {
     const auto& P = *reinterpret_cast<const typename Body::Params*>(blob);
     if (n == 0) return 0;
-    k_plain<Body><<<n, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, offset);
+    const uint32_t blocks = has_range<Body>::value ? (n + Body::kChunk - 1) / Body::kChunk : n;
+    k_plain<Body><<<blocks, Body::kThreads, Body::kDynSmem, (cudaStream_t)stream>>>(P, offset, n);
     return (int)cudaGetLastError();
 }
 

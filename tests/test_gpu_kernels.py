@@ -226,7 +226,7 @@ def test_mm_ring_fits_beside_the_partner():
     dm = G.gen("MM", "small", mode="int")
     refm = O.run_kernel(dm)
     smem_sm = torch.cuda.get_device_properties(0).shared_memory_per_multiprocessor
-    for partner, cap in (("ST", 8), ("SAD", 8), ("PC", 2), ("ST", 1)):   # feasible in warps and registers
+    for partner, cap in (("ST", 8), ("SAD", 2), ("PC", 2), ("ST", 1)):   # feasible in warps, registers, smem
         dp = G.gen(partner, "small")
         with K.Context(device=0, audit=1) as c:
             pm, pp = c.get_profile("MM"), c.get_profile(partner)
