@@ -393,12 +393,18 @@ class Context:
         n = grid_blocks - offset if n_blocks is None else n_blocks
         self._check(self._L.kl_run_plain(self._h, C.byref(d), s, offset, n))
 
-    def run_capped(self, kind, grid_blocks: int, args, cap: int) -> float:
-        """Whole kernel through the persistent launcher at `cap` blocks/SM; returns device ms."""
+    def run_capped(self, kind, grid_blocks: int, args, cap: int, spin_ns: int = 0) -> float:
+        """Whole kernel through the persistent launcher at `cap` blocks/SM; returns device ms
+        (spin_ns > 0: that long a device delay precedes the launch inside the timed interval)."""
         kid = KIND_ID[kind] if isinstance(kind, str) else int(kind)
         d = KernelDesc(kid, grid_blocks, C.cast(C.pointer(args), _vp), C.sizeof(args), None, 0, None)
         ms = C.c_double()
-        self._check(self._L.kl_run_capped(self._h, C.byref(d), cap, C.byref(ms)))
+        if spin_ns:
+            os.environ["KL_TIMING_SPIN_NS"] = str(int(spin_ns))
+        try:
+            self._check(self._L.kl_run_capped(self._h, C.byref(d), cap, C.byref(ms)))
+        finally:
+            os.environ.pop("KL_TIMING_SPIN_NS", None)
         return ms.value
 
     def run_pair(self, kind1, grid1, args1, cap1, kind2, grid2, args2, cap2):

@@ -1449,11 +1449,19 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     ctx->R.clear();                       // not scheduled: launched directly below
     st = flush_ctl_init(ctx);
     if (st) return st;
+    // the control-block init (batched per queue in the scheduler) is not part of the launch
+    KL_CUDA(cudaStreamSynchronize(ctx->stopper));
     cudaEvent_t e0, e1;
     KL_CUDA(cudaEventCreate(&e0));
     KL_CUDA(cudaEventCreate(&e1));
     int si = pick_stream(ctx);
     KL_CUDA(cudaEventRecord(e0, ctx->pool[si]));
+    // measurement knob (tools/launcher_overhead.py SPIN=1): a device delay queued before the
+    // launch hides the host-side launch work, as inside a scheduled queue; the caller subtracts it
+    if (const char* sp = std::getenv("KL_TIMING_SPIN_NS")) {
+        const unsigned long long ns = std::strtoull(sp, nullptr, 10);
+        if (ns && kl_dev_delay(ns, nullptr, ctx->pool[si])) return ctx->fail(KL_ECUDA, "spin");
+    }
     ctx->pool_busy[si] -= 1000;            // launch_kernel picks the least busy stream: this one
     st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0, variant_of(ctx, k->kind, -1, 0));
     ctx->pool_busy[si] += 1000;
