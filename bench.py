@@ -77,6 +77,9 @@ def parse(argv=None):
                     help="occupancy levels per kernel (kl_config.level_mode): every b with whole warps per virtual "
                          "SM, or the four levels {1/4, 1/2, 3/4, 1} x b_max of config C2")
     ap.add_argument("--speculative", action="store_true", help="enable the speculative start (kl_config.speculative)")
+    ap.add_argument("--critical", type=int, default=0, choices=[0, 1],
+                    help="1: makespan extension of FindCoSchedule (kl_config.critical, reading R29): while one kind's "
+                         "predicted remaining solo time exceeds all others' together, only co-schedules with it")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
@@ -345,6 +348,8 @@ def run_kernelet(args, rank, world, local_rank):
         cfg["alpha_p"], cfg["alpha_m"] = args.alpha
     if args.speculative:
         cfg["speculative"] = 1
+    if args.critical:
+        cfg["critical"] = 1
     if args.age_limit_us is not None:
         cfg["age_limit_us"] = args.age_limit_us
     if args.cp_min is not None:
@@ -773,6 +778,7 @@ def main(argv=None):
               "leases": f"{args.pool} input sets + {args.pool} output sets per kind (distinct device buffers)",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
               "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
+              "pair_choice": "critical-kind restriction (R29)" if args.critical else "max CP (Alg.1 greedy)",
               "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
               else "every b with whole warps per virtual SM"}
     scaling = "strong" if args.workload == "c5" else "weak"

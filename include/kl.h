@@ -168,7 +168,11 @@ typedef struct {
                                   pairs, one of 2 3 4 6 (32 KiB of shared memory each); 0
                                   (default): per co-schedule the deepest ring whose shared memory
                                   fits beside the partner's blocks (6 when MM runs solo) */
-    int32_t pad_cfg;
+    int32_t critical;          /* 1: makespan extension of FindCoSchedule (beyond the paper, reading
+                                  R29): while one pending kind's predicted remaining solo time
+                                  (remaining blocks x I / IPC_solo) exceeds all the others' together,
+                                  only co-schedules that include that kind are considered (the
+                                  model's max CP among them); 0 (default): the paper's greedy */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
     void* stream_b;            /* optional cudaStream_t: second stream of the launch pool      */

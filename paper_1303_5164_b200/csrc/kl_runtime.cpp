@@ -186,11 +186,18 @@ struct kl_ctx {
     KlDecision* dec_dev = nullptr;
     KlDecision* dec_pinned = nullptr;
     std::unordered_map<uint64_t, kl_prediction> cache;
+    double solo_ipc[KL_NKINDS] = {};          // IPC^solo per kind from the model's predictions
+    void note_pred(const KlCand& cd, const kl_prediction& p) {
+        if (p.status) return;
+        if (cd.k1 >= 0 && cd.k1 < KL_NKINDS && p.solo1 > 0) solo_ipc[cd.k1] = p.solo1;
+        if (cd.b2 && cd.k2 >= 0 && cd.k2 < KL_NKINDS && p.solo2 > 0) solo_ipc[cd.k2] = p.solo2;
+    }
     // maximal occupancy splits per ordered kind pair (depend on the profiles only)
     std::vector<std::pair<uint32_t, uint32_t>> splits[KL_NKINDS][KL_NKINDS];
     bool splits_ok[KL_NKINDS][KL_NKINDS] = {};
     void clear_caches() {
         cache.clear();
+        for (double& v : solo_ipc) v = 0.0;
         for (auto& row : splits_ok)
             for (auto& v : row) v = false;
     }
@@ -478,6 +485,7 @@ kl_status run_model(kl_ctx* ctx, int n, int n_pairs, KlDecision* dec_out, Inst* 
     for (int i = 0; i < n; ++i) {
         const KlCand& cd = ctx->cand_pinned[i];
         ctx->cache[cache_key(cd.k1, cd.k2, cd.b1, cd.b2)] = ctx->pred_pinned[i];
+        ctx->note_pred(cd, ctx->pred_pinned[i]);
     }
     if (dec_out) *dec_out = *ctx->dec_pinned;
     return KL_OK;
@@ -633,6 +641,43 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
             if (best < 0 || bp.cp > bcp + band(bp.cp, bcp)) { best = bi; bcp = bp.cp; }
         }
         if (best >= 0 && !(bcp > std::max(1e-12, ctx->cfg.cp_min))) best = -1;
+    }
+    if (ctx->cfg.critical && !ctx->cfg.mc_seed && np > 1) {
+        // makespan extension (R29): the kind with the largest predicted remaining solo time,
+        // if it exceeds all the others' together, is the queue's critical resource and must not
+        // idle -- restrict the choice to co-schedules that include it
+        double T[KL_NKINDS] = {}, tot = 0.0;
+        bool known = true;
+        for (Inst* k : R) {
+            const kl_profile& p = ctx->prof[k->kind];
+            const double ipc = ctx->solo_ipc[k->kind];
+            if (!(ipc > 0)) { known = false; break; }
+            const double t = (double)(k->grid - std::min(k->grid, k->next)) * p.ipb / ipc;
+            T[k->kind] += t;
+            tot += t;
+        }
+        int crit = -1;
+        for (int k = 0; k < KL_NKINDS; ++k)
+            if (known && T[k] > 0.5 * tot && (crit < 0 || T[k] > T[crit])) crit = k;
+        if (crit >= 0) {
+            int rb = -1;
+            double rcp = 0.0;
+            for (int p = 0; p < np; ++p) {
+                const KlCand& c0 = ctx->cand_pinned[ctx->off_pinned[p]];
+                if (c0.k1 != crit && c0.k2 != crit) continue;
+                int bi = -1;
+                kl_prediction bp{};
+                for (int i = ctx->off_pinned[p]; i < ctx->off_pinned[p + 1]; ++i) {
+                    const KlCand& cd = ctx->cand_pinned[i];
+                    kl_prediction a{};
+                    if (!ctx->lookup(cd.k1, cd.k2, cd.b1, cd.b2, &a) || a.status != 0) continue;
+                    if (bi < 0 || better_split(ctx, a, cd, bp, ctx->cand_pinned[bi], ctx->cfg.split_rule)) { bi = i; bp = a; }
+                }
+                if (bi < 0) continue;
+                if (rb < 0 || bp.cp > rcp + band(bp.cp, rcp)) { rb = bi; rcp = bp.cp; }
+            }
+            if (rb >= 0 && rcp > std::max(1e-12, ctx->cfg.cp_min)) { best = rb; bcp = rcp; }
+        }
     }
     if (best < 0) {   // solo: oldest pending kernel at its solo maximum occupancy (R25)
         d->solo = true;
@@ -1568,6 +1613,12 @@ kl_status kl_cache_put(kl_ctx* ctx, const kl_candidate* c, const kl_prediction* 
     for (size_t i = 0; i < n; ++i) {
         if (c[i].k1 < 0 || c[i].k1 >= KL_NKINDS || c[i].k2 < 0 || c[i].k2 >= KL_NKINDS) return KL_EINVAL;
         ctx->cache[cache_key(c[i].k1, c[i].k2, c[i].b1, c[i].b2)] = p[i];
+        KlCand cd{};
+        cd.k1 = c[i].k1;
+        cd.k2 = c[i].k2;
+        cd.b1 = c[i].b1;
+        cd.b2 = c[i].b2;
+        ctx->note_pred(cd, p[i]);
     }
     return KL_OK;
 }
