@@ -151,3 +151,43 @@ def test_pruning_relaxation():
 def test_pairs_of_order_and_dedup():
     pend = [{"kind": "A"}, {"kind": "B"}, {"kind": "A"}, {"kind": "C"}, {"kind": "A"}]
     assert O.pairs_of(pend) == [(0, 1), (0, 2), (0, 3), (1, 3)]
+
+
+def _calibrated():
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "..", "profiles", "kl_profile_b200.json")))
+    c = d["config"]
+    return d["profiles"], O.smcfg(L0=c["L0"], B=c["B"], a0=c["a0"], b0=c["b0"], W=16)
+
+
+@pytest.mark.parametrize("queue", [
+    [("PC", 64), ("BS", 64)],                                  # config C1 (BASELINE configs[0])
+    [("PC", 16384), ("BS", 16384)],                            # the same pair at paper sizes
+    [("MRIQ", 8192), ("PC", 16384), ("TEA", 16384)],           # three kinds of the ALL mix
+    [("MRIQ", 8192), ("ST", 8192), ("BS", 16384)],
+])
+def test_c1_greedy_vs_brute_force_calibrated(queue):
+    """The problem definition's optimum against Alg.1's greedy on the
+    calibrated B200 profile, in the model: the brute-force makespan over every decision sequence
+    bounds the greedy (both split rules: Eq.8's argmin dT, the bench's argmax CP) from below and
+    sequential execution from above; the gaps are reported (KL_WRITE_ARTEFACTS=1 writes
+    profiles/r02_c1_gap.json)."""
+    import json
+    import os
+    profs, cfg = _calibrated()
+    pend = [{"kind": k, "blocks": b} for k, b in queue]
+    t_opt = O.brute_force_makespan(pend, profs, cfg, mode="4")
+    seq = sum(O.alg1_makespan([e], profs, cfg, mode="4")[0] for e in pend)
+    rows = {"queue": queue, "brute_force": t_opt, "sequential": seq}
+    for rule in (0, 1):
+        t_g, _ = O.alg1_makespan(pend, profs, cfg, ap=0.0, am=0.0, mode="4", split_rule=rule)
+        assert t_opt <= t_g * (1 + 1e-9)
+        rows[f"greedy_rule{rule}"] = t_g
+        rows[f"gap_rule{rule}"] = t_g / t_opt - 1.0
+    assert t_opt <= seq * (1 + 1e-9)
+    if os.environ.get("KL_WRITE_ARTEFACTS"):
+        path = os.path.join(os.path.dirname(__file__), "..", "profiles", "r02_c1_gap.json")
+        old = json.load(open(path)) if os.path.exists(path) else []
+        old = [r for r in old if r["queue"] != [list(q) for q in queue]]
+        json.dump(old + [json.loads(json.dumps(rows))], open(path, "w"), indent=1)
