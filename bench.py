@@ -667,7 +667,7 @@ class OracleLeg:
     time."""
 
     def __init__(self, kinds: list[str], size: str, profile_path: str | None = None, split_rule: int = 1,
-                 levels: str = "four", alpha=None, max_decisions: int = 200):
+                 levels: str = "four", alpha=None, max_decisions: int = 200, cp_min=None):
         import oracle as O
         O.build()
         self.O = O
@@ -685,7 +685,8 @@ class OracleLeg:
         self.cfg = O.smcfg(L0=pcfg.get("L0", 800.0), B=pcfg.get("B", 1.0), a0=pcfg.get("a0", 0.0),
                            b0=pcfg.get("b0", 0.0), W=16)
         ap, am = alpha if alpha else (pcfg.get("alpha_p", 0.4), pcfg.get("alpha_m", 0.1))
-        self.sched_kw = dict(ap=ap, am=am, mode="4" if levels == "four" else "all", split_rule=split_rule)
+        self.sched_kw = dict(ap=ap, am=am, mode="4" if levels == "four" else "all", split_rule=split_rule,
+                             cp_min=pcfg.get("cp_min", 0.0) if cp_min is None else cp_min)
         self.max_decisions = max_decisions
         self.config = {"L0": self.cfg.L0, "B": self.cfg.B, "a0": self.cfg.a0, "b0": self.cfg.b0, "W_v": 16,
                        **self.sched_kw}
@@ -777,12 +778,14 @@ def main(argv=None):
               "l2": "256 MiB write between steps; inputs >> L2", "model_cache": "cleared every step",
               "leases": f"{args.pool} input sets + {args.pool} output sets per kind (distinct device buffers)",
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
-              "cp_min": args.cp_min or 0.0, "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
+              "cp_min": args.cp_min if args.cp_min is not None else load_profiles(args.profile)[1].get("cp_min", 0.0),
+              "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
               "pair_choice": "critical-kind restriction (R29)" if args.critical else "max CP (Alg.1 greedy)",
               "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
               else "every b with whole warps per virtual SM"}
     scaling = "strong" if args.workload == "c5" else "weak"
-    leg_kw = dict(profile_path=args.profile, split_rule=args.split_rule, levels=args.levels, alpha=args.alpha)
+    leg_kw = dict(profile_path=args.profile, split_rule=args.split_rule, levels=args.levels, alpha=args.alpha,
+                  cp_min=args.cp_min)
 
     if args.impl == "reference":
         if rank != 0:

@@ -586,7 +586,7 @@ def _rate(prof, ipc, n_vsm):
 
 
 def alg1_makespan(queue: list[dict], profs: dict, cfg, sm=B200_SM, nsched=4, ap=0.4, am=0.1,
-                  mode="all", n_sm=148, launch_overhead=0.0, decide=None, split_rule=0):
+                  mode="all", n_sm=148, launch_overhead=0.0, decide=None, split_rule=0, cp_min=0.0):
     """Alg.1 on an all-pending queue, executed in the model: each co-schedule runs
     until either kernel exhausts its blocks (R11), then the scheduler re-plans.  Returns
     (makespan in cycles, trace)."""
@@ -595,7 +595,7 @@ def alg1_makespan(queue: list[dict], profs: dict, cfg, sm=B200_SM, nsched=4, ap=
     t, trace, cache = 0.0, [], {}
     while pend:
         dec = decide(pend) if decide else find_co_schedule(pend, profs, cfg, sm, nsched, ap, am,
-                                                           mode, n_sm, cache, split_rule=split_rule)
+                                                           mode, n_sm, cache, split_rule=split_rule, cp_min=cp_min)
         if dec["solo"]:
             k = pend[dec["ia"]]
             pr = profs[k["kind"]]

@@ -108,7 +108,8 @@ def test_oracle_leg_uses_the_gpu_runs_model_config():
     O.build()
     kw = dict(profile_path=None, split_rule=1, levels="four", alpha=None)
     leg.__init__(["PC", "BS"], "small", **kw)
-    assert leg.sched_kw == {"ap": pcfg["alpha_p"], "am": pcfg["alpha_m"], "mode": "4", "split_rule": 1}
+    assert leg.sched_kw == {"ap": pcfg["alpha_p"], "am": pcfg["alpha_m"], "mode": "4", "split_rule": 1,
+                            "cp_min": pcfg.get("cp_min", 0.0)}
     assert abs(leg.cfg.L0 - pcfg["L0"]) < 1e-9 and abs(leg.cfg.B - pcfg["B"]) < 1e-12
     r = leg.run(target_s=0.5)
     assert r["kind"] == "oracle" and r["value"] > 0 and r["cores"] >= 1
