@@ -44,8 +44,13 @@ def anatomy(recs, critical="MRIQ"):
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    crit = sys.argv[sys.argv.index("--critical") + 1] if "--critical" in sys.argv else "MRIQ"
+    argv = list(sys.argv[1:])
+    crit = "MRIQ"
+    if "--critical" in argv:
+        i = argv.index("--critical")
+        crit = argv[i + 1]
+        del argv[i:i + 2]
+    args = argv
     recs = [json.loads(line) for line in open(args[0]) if line.strip()]
     out = anatomy(recs, crit)
     s = json.dumps(out, indent=1)
