@@ -50,3 +50,35 @@ def corun(ctx, k1, i1, b1, k2, i2, b2, min_overlap=0.5):
         return progress(tl1, t0, t1) / w, progress(tl2, t0, t1) / w, int(w)
     n1, n2 = float((tl1[:, 1] > 0).sum()), float((tl2[:, 1] > 0).sum())
     return n1 / max(z1 - a1, 1), n2 / max(z2 - a2, 1), 0
+
+
+# ---- steady-state co-runs -----------------------------------------------------------------
+# At paper size the kinds' solo times span 21 us (SPMV) to 2 ms (MRIQ): a co-run of a short and a
+# long kernel ends while the long one still ramps, and the window rates are dominated by ramp and
+# tail blocks (round-2 tables had rates of 1 % of solo for MRIQ beside SAD).  The steady mode runs
+# every kind at a size scaled along its independent dimension so its solo run takes >= target.
+SCALE_DIM = {"PC": "n_threads", "SAD": "height", "SPMV": "n_rows", "ST": "nz", "MM": "M", "MRIQ": "num_x",
+             "BS": "n", "TEA": "n", "SYNTH": "n", "MATADD": None}
+
+
+def scaled_size(kind, s):
+    import kl_inputs as G
+    p = dict(G.PAPER[kind])
+    dim = SCALE_DIM.get(kind)
+    if dim and s > 1:
+        p[dim] = p[dim] * s
+    return p
+
+
+def steady_instances(kinds, solo_ms, target_ms=2.0, device="cuda"):
+    """One instance per kind sized so that its solo run takes about target_ms (solo_ms: paper-size
+    solo time per kind)."""
+    import math
+    import kl_inputs as G
+    from paper_1303_5164_b200.workload import Instance
+    out = {}
+    for k in kinds:
+        s = max(1, int(math.ceil(target_ms / max(solo_ms[k], 1e-3))))
+        out[k] = Instance(G.gen(k, scaled_size(k, s)), device)
+        out[k].scale = s
+    return out

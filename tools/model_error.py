@@ -28,7 +28,7 @@ import bench  # noqa: E402
 import kl_inputs as G  # noqa: E402
 import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
-from tools.corun import corun, solo_rate  # noqa: E402
+from tools.corun import corun, solo_rate, steady_instances  # noqa: E402
 
 KINDS = G.MIXES["ALL"] + (["SYNTH"] if os.environ.get("KL_C3_SYNTH") else [])   # C3: + the streaming kernel
 
@@ -49,7 +49,10 @@ def main(out_path):
     ctx = K.Context(device=0, profiles=profiles, audit=2, **kcfg)
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     smem_sm = torch.cuda.get_device_properties(0).shared_memory_per_multiprocessor
-    insts = {k: Instance(G.gen(k, "paper"), "cuda") for k in KINDS}
+    if os.environ.get("KL_STEADY"):     # every kind scaled to a >= 2 ms solo run (tools/corun.py)
+        insts = steady_instances(KINDS, {k: calib["measured"][k]["ms_solo"] for k in KINDS})
+    else:
+        insts = {k: Instance(G.gen(k, "paper"), "cuda") for k in KINDS}
     prof = {k: ctx.get_profile(k) for k in KINDS}
     lv = {k: [b for b in range(1, prof[k].bmax + 1) if (b * prof[k].wpb) % 4 == 0] for k in KINDS}
     solo_b = {k: lv[k][-1] for k in KINDS}
@@ -89,7 +92,8 @@ def main(out_path):
     e_ipc = [abs(c["pred"][f] - c["meas"][f]) for c in cases for f in ("ipc1", "ipc2")]
     e_cp = [abs(c["pred"]["cp"] - c["meas"]["cp"]) for c in cases]
     solo_err = {k: calib["measured"].get(k, {}).get("fit", {}).get("rmse") for k in KINDS}
-    summary = {"mean_abs_cipc_err_per_vsm": float(np.mean(e_ipc)), "max_abs_cipc_err": float(np.max(e_ipc)),
+    summary = {"steady": bool(os.environ.get("KL_STEADY")),
+               "mean_abs_cipc_err_per_vsm": float(np.mean(e_ipc)), "max_abs_cipc_err": float(np.max(e_ipc)),
                "mean_abs_cp_err": float(np.mean(e_cp)), "n_cases": len(cases),
                "solo_ipc_measured": solo, "solo_fit_rmse": solo_err,
                "paper": "C2050 average absolute IPC error 0.08 (peak 1), GTX680 0.21 (peak 8), P:1299-1303"}

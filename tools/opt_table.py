@@ -19,7 +19,7 @@ import bench  # noqa: E402
 import kl_inputs as G  # noqa: E402
 import paper_1303_5164_b200 as K  # noqa: E402
 from paper_1303_5164_b200.workload import Instance  # noqa: E402
-from tools.corun import corun, solo_rate  # noqa: E402
+from tools.corun import corun, solo_rate, steady_instances  # noqa: E402
 from tools.model_error import fits  # noqa: E402
 
 KINDS = G.MIXES["ALL"]
@@ -32,9 +32,16 @@ def main(out_path):
     ctx = K.Context(device=0, profiles=profiles, audit=2, **kcfg)
     props = torch.cuda.get_device_properties(0)
     n_sm, smem_sm = props.multi_processor_count, props.shared_memory_per_multiprocessor
-    data = {k: G.gen(k, "paper") for k in KINDS}
-    a = {k: Instance(data[k], "cuda") for k in KINDS}
-    b = {k: Instance(data[k], "cuda", inputs=a[k].inputs) for k in KINDS}   # second instance, own outputs
+    if os.environ.get("KL_STEADY"):
+        # steady state: every kind scaled to a >= 2 ms solo run (tools/corun.py steady_instances)
+        calib = json.load(open(path))["measured"]
+        a = steady_instances(KINDS, {k: calib[k]["ms_solo"] for k in KINDS})
+        b = {k: Instance({"kind": k, "params": a[k].params, "grid_blocks": a[k].grid, "key": a[k].params.get("key")},
+                         "cuda", inputs=a[k].inputs) for k in KINDS}
+    else:
+        data = {k: G.gen(k, "paper") for k in KINDS}
+        a = {k: Instance(data[k], "cuda") for k in KINDS}
+        b = {k: Instance(data[k], "cuda", inputs=a[k].inputs) for k in KINDS}   # second instance, own outputs
     prof = {k: ctx.get_profile(k) for k in KINDS}
     lv = {k: [x for x in range(1, prof[k].bmax + 1) if (x * prof[k].wpb) % 4 == 0] for k in KINDS}
 
@@ -58,7 +65,11 @@ def main(out_path):
                           "solo1": solo[k1], "solo2": solo[k2], "cp": cp, "dT": dT, "status": 0 if ok else 2})
         print(k1, k2, len(maxi), "splits; best measured CP",
               round(max([t["cp"] for t in table if t["k1"] == k1 and t["k2"] == k2] or [0]), 3), flush=True)
-    json.dump({"solo_ipc": solo, "table": table, "how": "tools/opt_table.py (kl_run_pair co-runs at paper size, progress inside the common window)"},
+    how = ("tools/opt_table.py KL_STEADY=1 (kl_run_pair co-runs, every kind scaled to a >= 2 ms solo run, progress "
+           "inside the common window)" if os.environ.get("KL_STEADY") else
+           "tools/opt_table.py (kl_run_pair co-runs at paper size, progress inside the common window)")
+    json.dump({"solo_ipc": solo, "table": table, "how": how,
+               "scale": {k: getattr(a[k], "scale", 1) for k in KINDS}},
               open(out_path, "w"), indent=1)
 
 
