@@ -516,13 +516,29 @@ k_plain_pair(const __grid_constant__ typename Body::Params P, uint32_t offset, u
     asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
     typename Body::State st;
     Body::init(P, st, dsmem);
-    for (uint32_t v = cluster_id_x(); v < n; v += ncl) {
-        if (v != cluster_id_x()) {       // the previous tile's hand-off, as in the pair launcher
+    const uint32_t c = cluster_id_x();
+    // full rounds of one tile per pair; a last round that would leave more than half the pairs
+    // idle is split into half tiles (Body::block_part) so that every pair gets work
+    const uint32_t rounds = n / ncl, rem = n - rounds * ncl;
+    const bool split = rem > 0 && 2 * rem <= ncl;
+    const uint32_t full = split ? rounds * ncl : n;
+    bool first = true;
+    for (uint32_t v = c; v < full; v += ncl) {
+        if (!first) {                    // the previous tile's hand-off, as in the pair launcher
             Body::before_pair_sync(st);
             cluster_sync_all();
             Body::after_pair_sync(st);
         }
+        first = false;
         Body::block(P, st, dsmem, offset + v);
+    }
+    if (split && c < 2 * rem) {
+        if (!first) {
+            Body::before_pair_sync(st);
+            cluster_sync_all();
+            Body::after_pair_sync(st);
+        }
+        Body::block_part(P, st, dsmem, offset + full + c / 2, 1 + (int)(c & 1u));
     }
     Body::fini(P, st, dsmem);
 }

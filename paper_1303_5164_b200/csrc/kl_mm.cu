@@ -40,6 +40,7 @@ constexpr int kThreads = 256;      // 8 warps: whole warps per virtual SM (R14)
 constexpr uint32_t kTmemCols = 2 * BN;             // two fp32 accumulators (tile i / epilogue of i-1)
 // instruction descriptor: F32 accumulate, BF16 A/B, K-major A/B, N = 256, M = 256 (pair)
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t kIdescHalf = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)((BN / 2) >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 constexpr int kStageLevels[4] = {2, 3, 4, 6};
 
 constexpr int kEpiBox = 32;                        // C store box: 32 rows x 32 fp32 (128 B rows)
@@ -49,11 +50,12 @@ constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;      // 4 epilogue warps x 2 buf
 struct MMParams {
     CUtensorMap ta;   // A  [M][K] bf16, box 64 x 128
     CUtensorMap tb;   // Bt [N][K] bf16, box 64 x 128
+    CUtensorMap tbh;  // Bt [N][K] bf16, box 64 x 64 (half-width tiles, the plain grid's tail)
     CUtensorMap tc;   // C  [M][N] fp32, box 32 x 32, 128B swizzle (TMA store epilogue)
     float* C;
     int32_t M, N, K;
 };
-static_assert(sizeof(MMParams) <= 512, "blob");
+static_assert(sizeof(MMParams) <= 1024, "blob");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -136,7 +138,8 @@ struct BodyMM {
         uint32_t stage, phase;
         uint32_t tph;       // per-accumulator wait parity bits
         uint32_t ntile;     // tiles issued by this persistent pair
-        int prev_m, prev_n; // tile whose accumulator is still to be drained (-1: none)
+        int prev_m, prev_col, prev_w; // tile whose accumulator is still to be drained (-1: none):
+                                      // row tile, first column, width
     };
     __device__ static void init(const Params&, State& st, char* dsmem) {
         const uint32_t raw = smem_u32(dsmem);
@@ -144,7 +147,8 @@ struct BodyMM {
         st.bars = st.base + kBarOffset;
         st.rank = cluster_rank();
         st.stage = st.phase = st.tph = st.ntile = 0;
-        st.prev_m = st.prev_n = -1;
+        st.prev_m = st.prev_col = -1;
+        st.prev_w = BN;
         const int warp = threadIdx.x >> 5;
         if (threadIdx.x == 0) {
             for (int s = 0; s < S; ++s) {
@@ -172,7 +176,7 @@ struct BodyMM {
     // registers -> shared memory (128B-swizzled 32x32 boxes, two buffers per warp) -> C by TMA
     // bulk-tensor stores (whole 128-byte lines; a thread-per-row STG epilogue issues 32 partial
     // sectors per instruction and was the launch's tail).
-    __device__ static void drain(const Params& P, State& st, int m, int n, uint32_t b) {
+    __device__ static void drain(const Params& P, State& st, int m, int col, int w, uint32_t b) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         mbar_wait(st.bars + 128 + 8 * b, (st.tph >> b) & 1u);
         tc_fence_after();
@@ -181,7 +185,7 @@ struct BodyMM {
         const uint32_t tbase = st.tmem + ((uint32_t)(q * 32) << 16) + b * BN;
         const uint32_t ebuf = st.base + kEpiOffset + (uint32_t)q * 2u * kEpiBufBytes;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < w; c += 32) {
             uint32_t r[32];
             TMEM_LD_X32(tbase + (uint32_t)c, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -203,7 +207,7 @@ struct BodyMM {
             if (lane == 0) {
                 asm volatile(
                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)&P.tc),
-                    "r"(buf), "r"(n * BN + c), "r"(row0)
+                    "r"(buf), "r"(col + c), "r"(row0)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
@@ -211,7 +215,7 @@ struct BodyMM {
         tc_fence_before();
     }
     __device__ static void fini(const Params& P, State& st, char*) {
-        if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_n, (st.ntile - 1) & 1u);
+        if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_col, st.prev_w, (st.ntile - 1) & 1u);
         if ((threadIdx.x >> 5) >= 4 && (threadIdx.x & 31) == 0)
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // C written before the kernel's end
         tc_fence_before();
@@ -220,28 +224,37 @@ struct BodyMM {
         if ((threadIdx.x >> 5) == 1)
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols));
     }
-    __device__ static void block(const Params& P, State& st, char*, uint32_t vb) {
+    __device__ static void block(const Params& P, State& st, char* d, uint32_t vb) { block_part(P, st, d, vb, 0); }
+    // part 0: the whole 256x256 tile vb; part 1 / 2: its left / right 256x128 half (the plain
+    // grid splits its last, partial round of tiles so every pair gets work: wave quantisation).
+    // Every output element is the same k-ordered tensor-core accumulation either way.
+    __device__ static void block_part(const Params& P, State& st, char*, uint32_t vb, int part) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const int tiles_n = P.N / BN;
         const int tm = (int)vb / tiles_n, tn = (int)vb % tiles_n;
         const int nk = P.K / BK;
+        const int w = part ? BN / 2 : BN;                     // tile width (columns)
+        const int col = tn * BN + (part == 2 ? BN / 2 : 0);   // first column
+        const CUtensorMap* tmb = part ? &P.tbh : &P.tb;
+        const uint32_t idesc = part ? kIdescHalf : kIdesc;
+        const uint32_t tx = 2u * (uint32_t)(BM * BK * 2 + (w / 2) * BK * 2);   // both CTAs' bytes
         const uint32_t acc = st.ntile & 1u;                 // accumulator of this tile
         if (warp == 0) {
             if (lane == 0) {
                 uint32_t s = st.stage, ph = st.phase;
-                const int arow = tm * (2 * BM) + (int)st.rank * BM, brow = tn * BN + (int)st.rank * BNH;
+                const int arow = tm * (2 * BM) + (int)st.rank * BM, brow = col + (int)st.rank * (w / 2);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(st.bars + 64 + 8 * s, ph ^ 1u);
                     const uint32_t full = st.bars + 8 * s;
                     const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
 #ifdef KL_MM_DBG_NOTMA   // A/B probe: the MMAs on stale shared memory, no operand traffic
                     if (st.rank == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
-                    (void)sa; (void)sb; (void)arow; (void)brow;
+                    (void)sa; (void)sb; (void)arow; (void)brow; (void)tmb; (void)tx;
 #else
-                    if (st.rank == 0) mbar_expect_tx(full, 2 * kStageBytes);   // both CTAs' bytes
+                    if (st.rank == 0) mbar_expect_tx(full, tx);
                     const uint32_t full_lead = map_rank(full, 0u);
                     tma_load_2d_pair(sa, &P.ta, full_lead, kb * BK, arow);
-                    tma_load_2d_pair(sb, &P.tb, full_lead, kb * BK, brow);
+                    tma_load_2d_pair(sb, tmb, full_lead, kb * BK, brow);
 #endif
                     if (++s == S) { s = 0; ph ^= 1u; }
                 }
@@ -260,10 +273,10 @@ struct BodyMM {
 #ifndef KL_MM_DBG_NOMMA   // A/B probe: operand traffic only
 #pragma unroll
                         for (int k = 0; k < BK / 16; ++k)
-                            umma_bf16_pair(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), kIdesc,
+                            umma_bf16_pair(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc,
                                            (kb | k) != 0 ? 1u : 0u);
 #else
-                        (void)sa; (void)sb; (void)tacc;
+                        (void)sa; (void)sb; (void)tacc; (void)idesc;
 #endif
                         umma_commit_pair(st.bars + 64 + 8 * s);   // stage free in both CTAs
                         if (++s == S) { s = 0; ph ^= 1u; }
@@ -273,14 +286,15 @@ struct BodyMM {
                 __syncwarp();
             }
         } else if (warp >= 4 && st.prev_m >= 0) {
-            drain(P, st, st.prev_m, st.prev_n, acc ^ 1u);    // previous tile, other accumulator
+            drain(P, st, st.prev_m, st.prev_col, st.prev_w, acc ^ 1u);   // previous tile, other accumulator
         }
         // every role advances the shared pipeline state identically
         for (int kb = 0; kb < nk; ++kb)
             if (++st.stage == S) { st.stage = 0; st.phase ^= 1u; }
         if (st.prev_m >= 0) st.tph ^= 1u << (acc ^ 1u);    // that accumulator's wait was consumed
         st.prev_m = tm;
-        st.prev_n = tn;
+        st.prev_col = col;
+        st.prev_w = w;
         st.ntile++;
         tc_fence_before();
         __syncthreads();
@@ -368,6 +382,7 @@ int kl_mm_prepare(const void* args, uint32_t bytes, uint32_t grid, void* blob, u
     std::memset(&p, 0, sizeof p);
     if (!encode_kmajor(&p.ta, a.A, (uint64_t)a.M, (uint64_t)a.K, BM)) return -1;
     if (!encode_kmajor(&p.tb, a.Bt, (uint64_t)a.N, (uint64_t)a.K, BNH)) return -1;
+    if (!encode_kmajor(&p.tbh, a.Bt, (uint64_t)a.N, (uint64_t)a.K, BNH / 2)) return -1;
     if (!encode_c(&p.tc, a.C, (uint64_t)a.M, (uint64_t)a.N)) return -1;
     p.C = a.C;
     p.M = a.M;

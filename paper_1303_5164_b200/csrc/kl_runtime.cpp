@@ -35,7 +35,7 @@ int kl_mm_stage_smem(int stages);
 namespace {
 
 constexpr int kCtlPool = 16384;
-constexpr int kBlob = 512;
+constexpr int kBlob = 1024;
 constexpr int kMaxCand = 8192;
 
 // Pre-calibration defaults of the model inputs per kind (replaced by the B200 ncu calibration,
