@@ -93,6 +93,7 @@ struct KlLaunchRec {
     uint32_t exhausted;   // end == len
     uint32_t executed, admitted, max_per_sm;
     unsigned long long t0, t1;
+    unsigned long long t_entry, t_done;   // -DKL_PROBE_ANATOMY builds: block 0's entry, end of finalize
 };
 
 struct KlLaunch {

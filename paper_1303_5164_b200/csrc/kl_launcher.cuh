@@ -170,6 +170,9 @@ __device__ void finalize_epoch(KlCtl* ctl, uint32_t len, unsigned long long j, c
     }
     KlLaunchRec* r = F.rec;
     if (r) {
+#ifdef KL_PROBE_ANATOMY
+        r->t_done = gtimer();
+#endif
         r->start = start;
         r->end = lim;
         r->exhausted = exh ? 1u : 0u;
@@ -254,6 +257,9 @@ __global__ void __launch_bounds__(Body::kThreads, min_blocks<Body>::value)
 k_persistent(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
     extern __shared__ __align__(1024) char dsmem[];
     __shared__ uint32_t s_vb[2], s_end[2], s_adm;
+#ifdef KL_PROBE_ANATOMY
+    if (blockIdx.x == 0 && threadIdx.x == 0 && L.rec) L.rec->t_entry = gtimer();
+#endif
     KlCtl* ctl = L.ctl;
     const uint32_t len = ctl->len;
     uint32_t sm = 0;

@@ -1005,6 +1005,10 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
         t.grids = 1u + (uint32_t)L->topup_streams.size();
         t.variant = L->variant;
         ctx->trace.push_back(t);
+        if (std::getenv("KL_PROBE_ANATOMY") && r->t_entry)   // -DKL_PROBE_ANATOMY builds (tools/launch_anatomy.py)
+            std::fprintf(stderr, "anatomy kind %d entry->t0 %.2f us  t0->t1 %.2f us  t1->done %.2f us  t_entry %llu\n",
+                         k->kind, ((double)r->t0 - (double)r->t_entry) / 1e3, ((double)r->t1 - (double)r->t0) / 1e3,
+                         ((double)r->t_done - (double)r->t1) / 1e3, (unsigned long long)r->t_entry);
         k->next = r->end;
         k->inflight = nullptr;
         if (r->exhausted) {
@@ -1505,7 +1509,9 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     // launch hides the host-side launch work, as inside a scheduled queue; the caller subtracts it
     if (const char* sp = std::getenv("KL_TIMING_SPIN_NS")) {
         const unsigned long long ns = std::strtoull(sp, nullptr, 10);
-        if (ns && kl_dev_delay(ns, nullptr, ctx->pool[si])) return ctx->fail(KL_ECUDA, "spin");
+        const char* st_env = std::getenv("KL_TIMING_SPIN_STAMP");   // device address: release time
+        unsigned long long* stamp = st_env ? reinterpret_cast<unsigned long long*>(std::strtoull(st_env, nullptr, 10)) : nullptr;
+        if (ns && kl_dev_delay(ns, stamp, ctx->pool[si])) return ctx->fail(KL_ECUDA, "spin");
     }
     ctx->pool_busy[si] -= 1000;            // launch_kernel picks the least busy stream: this one
     st = launch_kernel(ctx, k, cap, k->grid, -1, 0.0, variant_of(ctx, k->kind, -1, 0));
