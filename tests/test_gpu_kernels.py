@@ -118,16 +118,16 @@ def test_integer_modes_exact(ctx, kind, field):
 def test_mriq_num_k_edges(ctx, num_k):
     """MRIQ's k loop: 256-point staging chunks, unrolled groups of KL_MRIQ_G = 8 (of which the last
     KL_MRIQ_P use the FMA-pipe polynomials in the experimental builds) and ragged tails, against
-    the oracle; the phase range reaches |k.x| of ~48 revolutions (kx, ky, kz ~ U[-32, 32),
-    x ~ U[-0.5, 0.5)).  Below 64 k-points the normwise bound has no averaging to lean on, and the
-    fp32 phase t = k.x itself is off by up to ulp(|t|) (~2e-5 rad at 300 rad), so those cases draw
-    k from U[-4, 4)."""
+    the oracle over the paper's full phase range (|k.x| up to ~48 revolutions: kx, ky, kz ~
+    U[-32, 32), x ~ U[-0.5, 0.5)) at every k count, including single terms where no averaging
+    hides the fp32 phase error: the bound is the one derived from the arithmetic
+    (kl_check.mriq_rtol), and the observed error is also held to 1e-5 once the
+    terms are many (num_k >= 256)."""
     d = G.gen("MRIQ", dict(num_x=777, num_k=num_k))
-    if num_k < 64:
-        for f in ("kx", "ky", "kz"):
-            d[f] = (d[f] * np.float32(0.125)).astype(np.float32)
     inst = Instance(d, "cuda")
-    compare("MRIQ", _run_plain(ctx, inst), O.run_kernel(d))
+    errs = compare("MRIQ", _run_plain(ctx, inst), O.run_kernel(d), num_k=num_k)
+    if num_k >= 256:
+        assert max(errs.values()) <= 1e-5, errs
 
 
 def test_mriq_zero_k_closed_form(ctx):
