@@ -410,6 +410,9 @@ k_persistent_pair(const __grid_constant__ typename Body::Params P, const __grid_
     const uint32_t rank = cluster_rank();
     uint32_t sm = 0;
     bool joined = false;
+    // distributed shared memory may only be written once the peer CTA is running
+    // (compute-sanitizer: "a block that might not have entered yet")
+    cluster_sync_all();
     if (threadIdx.x == 0) {
         uint32_t adm = 0;
         joined = join_epoch(L);
@@ -520,6 +523,7 @@ k_plain_pair(const __grid_constant__ typename Body::Params P, uint32_t offset, u
     extern __shared__ __align__(1024) char dsmem[];
     uint32_t ncl;
     asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
+    cluster_sync_all();   // both CTAs running before the pair's TMEM allocation touches either
     typename Body::State st;
     Body::init(P, st, dsmem);
     const uint32_t c = cluster_id_x();

@@ -167,6 +167,7 @@ struct BodyMM {
         }
         tc_fence_before();
         cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
+        __syncthreads();      // (also a CTA barrier for racecheck, which does not model the cluster one)
         tc_fence_after();
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(st.tmem) : "r"(st.bars + 192));
     }
