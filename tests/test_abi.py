@@ -95,3 +95,14 @@ def test_host_only_refuses_device_calls(L):
     with pytest.raises(K.KlError) as e:
         ctx.sync()
     assert e.value.status == K.KL_ECUDA
+
+
+def test_config_validation(L):
+    """kl_create rejects an MM ring depth that is not one of its occupancy levels (R28) and a
+    scheduler count that does not divide the 64 warps of an SM."""
+    for bad in (dict(mm_stages=5), dict(mm_stages=1), dict(n_sched=3)):
+        with pytest.raises(K.KlError) as e:
+            _host_ctx(**bad)
+        assert e.value.status == K.KL_EINVAL, bad
+    for ok in (0, 2, 3, 4, 6):
+        _host_ctx(mm_stages=ok).close()
