@@ -73,9 +73,10 @@ def parse(argv=None):
                     help="pruning thresholds alpha_p alpha_m (default: the profile JSON's, else the paper's 0.4 0.1)")
     ap.add_argument("--age-limit-us", type=int, default=None,
                     help="starvation guard (kl_config.age_limit_us; default 0 = the paper's greedy)")
-    ap.add_argument("--levels", default="four", choices=["all", "four"],
+    ap.add_argument("--levels", default=None, choices=["all", "four"],
                     help="occupancy levels per kernel (kl_config.level_mode): every b with whole warps per virtual "
-                         "SM, or the four levels {1/4, 1/2, 3/4, 1} x b_max of config C2")
+                         "SM, or the four levels {1/4, 1/2, 3/4, 1} x b_max of config C2 (default: four for c2, "
+                         "all for c4/c5, whose configs fix no levels: C5 3442-3452 vs 3401-3411 kernels/s)")
     ap.add_argument("--speculative", action="store_true", help="enable the speculative start (kl_config.speculative)")
     ap.add_argument("--critical", type=int, default=0, choices=[0, 1],
                     help="1: makespan extension of FindCoSchedule (kl_config.critical, reading R29): while one kind's "
@@ -761,6 +762,8 @@ def workload_name(args) -> str:
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
     args = parse(argv)
+    if args.levels is None:
+        args.levels = "four" if args.workload == "c2" else "all"
     cmd = spawn_cmd(args, argv)
     if cmd:                 # --gpus N without a launcher: one process per GPU via torch.distributed.run
         sys.stdout.flush()

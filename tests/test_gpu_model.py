@@ -141,18 +141,20 @@ def _bench_profiles():
     return profs, d.get("config", {})
 
 
+@pytest.mark.parametrize("level_mode", [1, 0])
 @pytest.mark.parametrize("split_rule", [1, 0])
-def test_decisions_match_oracle_bench_config(split_rule):
-    """The bench's decision configuration: calibrated profiles with the resource fields the
+def test_decisions_match_oracle_bench_config(split_rule, level_mode):
+    """The bench's decision configurations: calibrated profiles with the resource fields the
     runtime reads from the compiled kernels (MM: TMEM- and shared-memory-bound, one block per SM),
-    the four C2 occupancy levels (level_mode = 1 <-> oracle mode "4"), alpha = 0 and both split
+    the four C2 occupancy levels (level_mode = 1 <-> oracle mode "4"; C2) or every whole-warp level
+    (level_mode = 0 <-> oracle mode "all"; C4 / C5), alpha = 0, the calibrated cp_min and both split
     rules; queues drawn from the ALL mix always holding MM.  The oracle gets the runtime-resolved
     profiles (kl_get_profile), so this compares the decision logic, not the profile plumbing."""
     K.build()
     profs, kcfg = _bench_profiles()
     cfg = dict(kcfg)
-    cfg.update(split_rule=split_rule, level_mode=1)
-    rng = np.random.default_rng(23 + split_rule)
+    cfg.update(split_rule=split_rule, level_mode=level_mode)
+    rng = np.random.default_rng(23 + split_rule + 7 * level_mode)
     all_mix = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA"]
     for rep in range(16):
         ctx = K.Context(device=0, profiles=profs, **cfg)
@@ -168,7 +170,8 @@ def test_decisions_match_oracle_bench_config(split_rule):
         d1, d2 = _decide_both(ctx)
         ocfg = O.smcfg(W=16, L0=kcfg["L0"], B=kcfg["B"], a0=kcfg.get("a0", 1.0), b0=kcfg.get("b0", 0.0))
         ref = O.find_co_schedule(pend, resolved, ocfg, ap=ctx.config.alpha_p, am=ctx.config.alpha_m,
-                                 mode="4", cp_min=ctx.config.cp_min, split_rule=split_rule)
+                                 mode="4" if level_mode == 1 else "all", cp_min=ctx.config.cp_min,
+                                 split_rule=split_rule)
         for d in (d1, d2):
             assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref["solo"])
             assert d.id1 == pend[ref["ia"]]["id"], (kinds, d.id1, ref)
