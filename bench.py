@@ -81,6 +81,8 @@ def parse(argv=None):
     ap.add_argument("--critical", type=int, default=0, choices=[0, 1],
                     help="1: makespan extension of FindCoSchedule (kl_config.critical, reading R29): while one kind's "
                          "predicted remaining solo time exceeds all others' together, only co-schedules with it")
+    ap.add_argument("--set", action="append", default=[], metavar="FIELD=VALUE",
+                    help="A/B knob: set a kl_config integer/float field (e.g. model_states=3, granularity=1)")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
     ap.add_argument("--opt", default=None, help="OPT comparator: decide from a measured pair table "
                                                "(tools/opt_table.py) instead of the Markov model")
@@ -156,12 +158,13 @@ def ncu_traffic(kind: str, profiles_dir: str | None = None):
             d = json.load(open(path))
         except Exception:
             continue
-        for rep, rows in d.items():
-            if not isinstance(rows, list):
-                continue
+        rows_all = [r for rows in d.values() if isinstance(rows, list) for r in rows]
+        # the persistent slice-launcher variant first: that is what the bench's step launches
+        rows_all.sort(key=lambda r: 0 if "k_persistent" in r.get("kernel", "") else 1)
+        for rows in (rows_all,):
             for r in rows:
                 if f"Body{kind}>" in r.get("kernel", "") or f"Body{kind}E" in r.get("kernel", "") or \
-                        f"::Body{kind}" in r.get("kernel", ""):
+                        f"::Body{kind}" in r.get("kernel", "") or f"Body{kind}<" in r.get("kernel", ""):
                     try:
                         rd = _metric_bytes(r["dram__bytes_read.sum"])
                         wr = _metric_bytes(r["dram__bytes_write.sum"])
@@ -351,6 +354,9 @@ def run_kernelet(args, rank, world, local_rank):
         cfg["speculative"] = 1
     if args.critical:
         cfg["critical"] = 1
+    for kv in args.set:
+        k, _, v = kv.partition("=")
+        cfg[k] = float(v) if "." in v else int(v)
     if args.age_limit_us is not None:
         cfg["age_limit_us"] = args.age_limit_us
     if args.cp_min is not None:
@@ -784,6 +790,7 @@ def main(argv=None):
               "cp_min": args.cp_min if args.cp_min is not None else load_profiles(args.profile)[1].get("cp_min", 0.0),
               "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
               "pair_choice": "critical-kind restriction (R29)" if args.critical else "max CP (Alg.1 greedy)",
+              **({"config_overrides": args.set} if args.set else {}),
               "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
               else "every b with whole warps per virtual SM"}
     scaling = "strong" if args.workload == "c5" else "weak"
