@@ -140,7 +140,6 @@ struct BodySAD {
         const uint32_t v = v0 + (threadIdx.x >> 5);
         if (v < v1) macroblock(a, v);
     }
-    __device__ static void block(const Params& a, State& st, char* d, uint32_t vb) { block_range(a, st, d, vb, vb + 1); }
     // One warp: macroblock vb (its own slice of the block's shared memory).
     __device__ static void macroblock(const Params& a, uint32_t vb) {
         __shared__ uint32_t win_all[4][48 * 12];
@@ -217,7 +216,6 @@ struct BodySPMV {
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (live && lane == 0) a.y[row] = sum;
     }
-    __device__ static void block(const Params& a, State& st, char* d, uint32_t vb) { block_range(a, st, d, vb, vb + 1); }
 };
 
 // ST (Parboil 7-point stencil): 32x4 (x,y) tile, 64 z-points per block; the z

@@ -246,7 +246,8 @@ struct min_blocks<B, std::void_t<decltype(B::kMinBlocks)>> { static constexpr in
 
 // Optional Body::block_range(P, st, dsmem, v0, v1): the body runs a fetched chunk of virtual
 // blocks [v0, v1) together (more independent work in flight per block: SPMV's rows); the
-// per-block result must not depend on how the range is grouped (sliced == unsliced).
+// per-block result must not depend on how the range is grouped (sliced == unsliced).  Such a
+// body needs no Body::block.
 template <class B, class = void>
 struct has_range : std::false_type {};
 template <class B>
