@@ -164,6 +164,8 @@ struct kl_ctx {
     std::vector<std::unique_ptr<Inst>> insts;
     std::unordered_map<uint64_t, Inst*> by_id;
     std::vector<Inst*> R;              // pending set, arrival order (Alg.1 l.1)
+    int n_pending[KL_NKINDS] = {};     // instances of each kind in R (the representatives scan stops
+                                       // once every pending kind has its two)
     std::vector<Inst*> arriving;       // submitted, waiting for their ready event (Alg.1 l.2)
     std::vector<std::pair<void*, bool>> ev_seen;   // per-poll cache of ready-event queries
     uint64_t next_id = 1, seq = 0;
@@ -499,8 +501,10 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
     // representatives: first two instances of each kind, arrival order
     std::vector<int> reps;
     int seen_k[KL_NKINDS] = {0};
-    for (int i = 0; i < (int)R.size(); ++i)
-        if (seen_k[R[i]->kind] < 2) { reps.push_back(i); seen_k[R[i]->kind]++; }
+    int want = 0;                      // representatives still to find (2 per kind, or fewer pending)
+    for (int k = 0; k < KL_NKINDS; ++k) want += std::min(2, ctx->n_pending[k]);
+    for (int i = 0; i < (int)R.size() && want > 0; ++i)
+        if (seen_k[R[i]->kind] < 2) { reps.push_back(i); seen_k[R[i]->kind]++; --want; }
     std::vector<std::pair<int, int>> pairs;
     bool seen_pair[KL_NKINDS][KL_NKINDS] = {};
     for (size_t a = 0; a < reps.size(); ++a)
@@ -931,7 +935,11 @@ void mark_drained(kl_ctx* ctx, Inst* k) {
     if (k->drained) return;
     k->drained = true;
     auto& R = ctx->R;
-    R.erase(std::remove(R.begin(), R.end(), k), R.end());
+    auto it = std::find(R.begin(), R.end(), k);
+    if (it != R.end()) {
+        R.erase(it);
+        ctx->n_pending[k->kind]--;
+    }
 }
 
 // Poll the launch records.  Returns through *replan whether R changed (a kernel drained) and
@@ -967,6 +975,7 @@ kl_status poll(kl_ctx* ctx, bool* replan, bool* progress) {
             auto pos = std::upper_bound(ctx->R.begin(), ctx->R.end(), k, [](Inst* a, Inst* b) { return a->seq < b->seq; });
             k->t_join = now_ns();
             ctx->R.insert(pos, k);
+            ctx->n_pending[k->kind]++;
             ctx->arriving.erase(ctx->arriving.begin() + i);
             *replan = *progress = true;
         }
@@ -1346,6 +1355,7 @@ kl_status kl_submit(kl_ctx* ctx, const kl_kernel_desc* d, uint64_t* out_id) {
     else {
         raw->t_join = now_ns();
         ctx->R.push_back(raw);
+        ctx->n_pending[raw->kind]++;
     }
     ctx->insts.push_back(std::move(k));
     if (out_id) *out_id = raw->id;
@@ -1496,6 +1506,7 @@ kl_status kl_run_capped(kl_ctx* ctx, const kl_kernel_desc* d, uint32_t cap, doub
     if (st) return st;
     Inst* k = ctx->by_id[id];
     ctx->R.clear();                       // not scheduled: launched directly below
+    for (int& c : ctx->n_pending) c = 0;
     st = flush_ctl_init(ctx);
     if (st) return st;
     // the control-block init (batched per queue in the scheduler) is not part of the launch
@@ -1544,6 +1555,7 @@ kl_status kl_run_pair(kl_ctx* ctx, const kl_kernel_desc* d1, uint32_t cap1, cons
     Inst* k1 = ctx->by_id[id1];
     Inst* k2 = ctx->by_id[id2];
     ctx->R.clear();                       // not scheduled: launched directly below
+    for (int& c : ctx->n_pending) c = 0;
     st = flush_ctl_init(ctx);
     if (st) return st;
     const size_t t0 = ctx->trace.size();
