@@ -81,6 +81,10 @@ def parse(argv=None):
     ap.add_argument("--critical", type=int, default=0, choices=[0, 1],
                     help="1: makespan extension of FindCoSchedule (kl_config.critical, reading R29): while one kind's "
                          "predicted remaining solo time exceeds all others' together, only co-schedules with it")
+    ap.add_argument("--bmax", default="sat", choices=["sat", "hw"],
+                    help="b_max with every whole-warp level: the calibrated saturation occupancy (R31) or the hardware limit")
+    ap.add_argument("--prof", action="append", default=[], metavar="KIND.FIELD=VALUE",
+                    help="A/B knob: override one field of a kind's profile (e.g. MRIQ.bmax=3)")
     ap.add_argument("--set", action="append", default=[], metavar="FIELD=VALUE",
                     help="A/B knob: set a kl_config integer/float field (e.g. model_states=3, granularity=1)")
     ap.add_argument("--trace-out", default=None, help="write the last timed step's launch trace (JSON lines)")
@@ -284,13 +288,21 @@ def build_queue(rank: int, world: int, instances: int, workload: str = "c5", mix
 MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
 
 
-def load_profiles(path: str):
+def load_profiles(path: str, levels: str = "four", bmax: str = "sat"):
     """Calibrated model inputs (tools/calibrate.py).  Resource fields (warps, registers, shared
-    memory, TMEM, b_max) are left to the runtime, which reads them from the compiled kernels."""
+    memory, TMEM, b_max) are left to the runtime, which reads them from the compiled kernels --
+    except that with every whole-warp level (C4 / C5, `levels="all"`) b_max is the kind's
+    saturation occupancy `bmax_sat` (reading R31: the smallest cap whose solo time is within 1 %
+    of the best in the calibration's occupancy sweep) unless `bmax="hw"`.  C2 fixes its levels as
+    quarters of the hardware b_max and keeps it."""
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
         profs = {k: {f: v[f] for f in MODEL_FIELDS if f in v} for k, v in d.get("profiles", {}).items()}
+        if levels == "all" and bmax == "sat":
+            for k, v in d.get("profiles", {}).items():
+                if v.get("bmax_sat"):
+                    profs[k]["bmax"] = int(v["bmax_sat"])
         return profs, d.get("config", {})
     return None, {}
 
@@ -317,7 +329,11 @@ def run_kernelet(args, rank, world, local_rank):
     torch.cuda.set_device(dev)
     K.lib()
     kinds = build_queue(rank, world, args.instances, args.workload, args.mix)
-    profiles, kcfg = load_profiles(args.profile)
+    profiles, kcfg = load_profiles(args.profile, args.levels, args.bmax)
+    for kv in args.prof:
+        kf, _, v = kv.partition("=")
+        kind, _, field = kf.partition(".")
+        profiles.setdefault(kind, {})[field] = float(v) if "." in v else int(v)
     t_gen = time.time()
     data = {k: G.gen(k, args.size) for k in sorted(set(kinds))}
     # leases: POOL input sets and POOL output sets per kind (distinct device buffers; input set j
@@ -674,7 +690,7 @@ class OracleLeg:
     time."""
 
     def __init__(self, kinds: list[str], size: str, profile_path: str | None = None, split_rule: int = 1,
-                 levels: str = "four", alpha=None, max_decisions: int = 200, cp_min=None):
+                 levels: str = "four", alpha=None, max_decisions: int = 200, cp_min=None, bmax: str = "sat"):
         import oracle as O
         O.build()
         self.O = O
@@ -688,7 +704,7 @@ class OracleLeg:
                              "BS": lambda: p["n"], "TEA": lambda: p["n"],
                              "SAD": lambda: (p["width"] // 16) * (p["height"] // 16) * 1089,
                              "ST": lambda: p["nx"] * p["ny"] * p["nz"], "MM": lambda: p["M"] * p["N"]}[k]()
-        self.profs, pcfg = _oracle_profiles(profile_path)
+        self.profs, pcfg = _oracle_profiles(profile_path, levels, bmax)
         self.cfg = O.smcfg(L0=pcfg.get("L0", 800.0), B=pcfg.get("B", 1.0), a0=pcfg.get("a0", 0.0),
                            b0=pcfg.get("b0", 0.0), W=16)
         ap, am = alpha if alpha else (pcfg.get("alpha_p", 0.4), pcfg.get("alpha_m", 0.1))
@@ -748,12 +764,19 @@ def _oracle_sample(O, data, sizes, frac, cores) -> dict:
     return out
 
 
-def _oracle_profiles(path: str | None = None):
+def _oracle_profiles(path: str | None = None, levels: str = "four", bmax: str = "sat"):
+    """The oracle's profile table: the calibrated profiles with the b_max the GPU run uses
+    (load_profiles: bmax_sat with every whole-warp level)."""
     path = path or os.path.join(ROOT, "profiles", "kl_profile_b200.json")
     if not os.path.exists(path):
         return None, {}
     d = json.load(open(path))
-    return {k: v for k, v in d["profiles"].items() if k in ALL}, d.get("config", {})
+    out = {k: dict(v) for k, v in d["profiles"].items() if k in ALL}
+    if levels == "all" and bmax == "sat":
+        for v in out.values():
+            if v.get("bmax_sat"):
+                v["bmax"] = int(v["bmax_sat"])
+    return out, d.get("config", {})
 
 
 # ---------------------------------------------------------------------------------------------
@@ -791,11 +814,13 @@ def main(argv=None):
               "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
               "pair_choice": "critical-kind restriction (R29)" if args.critical else "max CP (Alg.1 greedy)",
               **({"config_overrides": args.set} if args.set else {}),
+              **({"profile_overrides": args.prof} if args.prof else {}),
               "occupancy_levels": "{1/4, 1/2, 3/4, 1} x b_max per kernel (config C2)" if args.levels == "four"
-              else "every b with whole warps per virtual SM"}
+              else ("every b with whole warps per virtual SM up to the kind's saturation occupancy (R31)"
+                    if args.bmax == "sat" else "every b with whole warps per virtual SM up to the hardware b_max")}
     scaling = "strong" if args.workload == "c5" else "weak"
     leg_kw = dict(profile_path=args.profile, split_rule=args.split_rule, levels=args.levels, alpha=args.alpha,
-                  cp_min=args.cp_min)
+                  cp_min=args.cp_min, bmax=args.bmax)
 
     if args.impl == "reference":
         if rank != 0:

@@ -59,6 +59,30 @@ static_assert(sizeof(MMParams) <= 1024, "blob");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+#ifdef KL_MM_PROBE
+// Timing probe (tools/mm_stamp_probe.py; not in the product build): per pair (cluster id) and per
+// tile j < 8: [0] MMA issuer sees the first stage full, [1] last MMA of the tile issued,
+// [2] epilogue (rank 0, warp 4) starts waiting for the accumulator, [3] its TMA stores issued;
+// per pair [kProbeTiles*4] kernel entry, [+1] after init, [+2] before fini, [+3] end of fini.
+constexpr int kProbeTiles = 8, kProbeStride = kProbeTiles * 4 + 4;
+__device__ unsigned long long g_mm_probe[96 * kProbeStride];
+__device__ __forceinline__ unsigned long long probe_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t probe_cluster() {
+    uint32_t c;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(c));
+    return c;
+}
+#define MM_PROBE(j, f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96 && (j) < kProbeTiles) g_mm_probe[c_ * kProbeStride + (j) * 4 + (f)] = probe_now(); } while (0)
+#define MM_PROBE_K(f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96) g_mm_probe[c_ * kProbeStride + kProbeTiles * 4 + (f)] = probe_now(); } while (0)
+#else
+#define MM_PROBE(j, f) do { } while (0)
+#define MM_PROBE_K(f) do { } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
@@ -143,6 +167,7 @@ struct BodyMM {
     };
     __device__ static void init(const Params&, State& st, char* dsmem) {
         const uint32_t raw = smem_u32(dsmem);
+        if (threadIdx.x == 0 && cluster_rank() == 0) MM_PROBE_K(0);
         st.base = (raw + 1023u) & ~1023u;
         st.bars = st.base + kBarOffset;
         st.rank = cluster_rank();
@@ -170,6 +195,7 @@ struct BodyMM {
         __syncthreads();      // (also a CTA barrier for racecheck, which does not model the cluster one)
         tc_fence_after();
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(st.tmem) : "r"(st.bars + 192));
+        if (threadIdx.x == 0 && st.rank == 0) MM_PROBE_K(1);
     }
     __device__ static void before_pair_sync(State&) { tc_fence_before(); }
     __device__ static void after_pair_sync(State&) { tc_fence_after(); }
@@ -179,6 +205,7 @@ struct BodyMM {
     // sectors per instruction and was the launch's tail).
     __device__ static void drain(const Params& P, State& st, int m, int col, int w, uint32_t b) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp == 4 && lane == 0 && st.rank == 0) MM_PROBE(st.ntile - 1, 2);
         mbar_wait(st.bars + 128 + 8 * b, (st.tph >> b) & 1u);
         tc_fence_after();
         const int q = warp & 3;                              // TMEM lane quarter of this warp
@@ -213,9 +240,11 @@ struct BodyMM {
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
+        if (warp == 4 && lane == 0 && st.rank == 0) MM_PROBE(st.ntile - 1, 3);
         tc_fence_before();
     }
     __device__ static void fini(const Params& P, State& st, char*) {
+        if (threadIdx.x == 0 && st.rank == 0) MM_PROBE_K(2);
         if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_col, st.prev_w, (st.ntile - 1) & 1u);
         if ((threadIdx.x >> 5) >= 4 && (threadIdx.x & 31) == 0)
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // C written before the kernel's end
@@ -224,6 +253,7 @@ struct BodyMM {
         tc_fence_after();
         if ((threadIdx.x >> 5) == 1)
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols));
+        if (threadIdx.x == 0 && st.rank == 0) MM_PROBE_K(3);
     }
     __device__ static void block(const Params& P, State& st, char* d, uint32_t vb) { block_part(P, st, d, vb, 0); }
     // part 0: the whole 256x256 tile vb; part 1 / 2: its left / right 256x128 half (the plain
@@ -270,6 +300,7 @@ struct BodyMM {
                     for (int kb = 0; kb < nk; ++kb) {
                         mbar_wait(st.bars + 8 * s, ph);
                         tc_fence_after();
+                        if (kb == 0) MM_PROBE(st.ntile, 0);
                         const uint32_t sa = st.base + s * kStageBytes, sb = sa + BM * BK * 2;
 #ifndef KL_MM_DBG_NOMMA   // A/B probe: operand traffic only
 #pragma unroll
@@ -283,6 +314,7 @@ struct BodyMM {
                         if (++s == S) { s = 0; ph ^= 1u; }
                     }
                     umma_commit_pair(st.bars + 128 + 8 * acc);    // accumulator `acc` complete
+                    MM_PROBE(st.ntile, 1);
                 }
                 __syncwarp();
             }
@@ -353,6 +385,18 @@ int stages_of(uint32_t variant) {
 }
 
 }  // namespace
+
+#ifdef KL_MM_PROBE
+extern "C" int kl_mm_probe_read(unsigned long long* out, int n) {
+    const int cap = 96 * kProbeStride;
+    if (n > cap) n = cap;
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_mm_probe, sizeof(unsigned long long) * n);
+    static unsigned long long zero[96 * kProbeStride];
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_mm_probe, zero, sizeof zero);
+    return (int)e;
+}
+extern "C" int kl_mm_probe_stride() { return kProbeStride; }
+#endif
 
 int kl_mm_stage_smem(int stages) {     // dynamic shared memory of one CTA at `stages`
     return stages * kStageBytes + kEpiBytes + 1024 + 256;

@@ -120,3 +120,35 @@ def test_pc_reports_both_atoms():
     p = G.gen("PC", "small")["params"]
     w = bench.algorithmic_work("PC", p)
     assert w["bytes"] - w["bytes_32B"] == p["n_threads"] * p["hops"] * 32
+
+
+def test_saturation_bmax_reading_r31():
+    """R31: b_max for every whole-warp level (C4 / C5) is the smallest cap whose solo time is
+    within 1 % of the best in the calibration sweep; C2 (quarters of b_max) keeps the hardware
+    b_max; the oracle leg sees the same b_max as the GPU run."""
+    import json
+    import os
+    sys_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools")
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("calibrate", os.path.join(sys_path, "calibrate.py"))
+    cal = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(cal)
+    assert cal.saturation_bmax({"1": 2.48, "2": 2.03, "3": 1.981, "4": 1.975, "8": 1.973}) == 3
+    assert cal.saturation_bmax({1: 1.0, 2: 0.5}) == 2
+    assert cal.saturation_bmax({1: 1.0, 2: 0.995}) == 1
+    assert cal.saturation_bmax({1: 1.0, 2: 0.9, 3: 0.89}, tol=0.02) == 2
+    path = os.path.join(bench.ROOT, "profiles", "kl_profile_b200.json")
+    d = json.load(open(path))
+    for k, m in d["measured"].items():
+        if m.get("cap_sweep_ms") and k in d["profiles"]:
+            assert d["profiles"][k]["bmax_sat"] == cal.saturation_bmax(m["cap_sweep_ms"])
+    p_all, _ = bench.load_profiles(path, "all")
+    p_hw, _ = bench.load_profiles(path, "all", "hw")
+    p_four, _ = bench.load_profiles(path, "four")
+    assert p_all["MRIQ"]["bmax"] == d["profiles"]["MRIQ"]["bmax_sat"] < d["profiles"]["MRIQ"]["bmax"]
+    assert "bmax" not in p_hw["MRIQ"] and "bmax" not in p_four["MRIQ"]   # left to the runtime
+    o_all, _ = bench._oracle_profiles(path, "all")
+    o_four, _ = bench._oracle_profiles(path, "four")
+    for k in bench.ALL:
+        assert o_all[k]["bmax"] == p_all[k]["bmax"]
+        assert o_four[k]["bmax"] == d["profiles"][k]["bmax"]

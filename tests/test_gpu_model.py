@@ -130,15 +130,15 @@ def _args_of(kind, keep={}):
     return keep["MM"].grid, keep["MM"].args
 
 
-def _bench_profiles():
-    """The calibrated B200 profile and scheduler config the bench runs (bench.load_profiles)."""
-    import json
+def _bench_profiles(levels="four"):
+    """The calibrated B200 profile and scheduler config the bench runs (bench.load_profiles: with
+    every whole-warp level b_max is the saturation occupancy, R31)."""
     import os
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kl_profile_b200.json")
-    d = json.load(open(path))
-    fields = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
-    profs = {k: {f: v[f] for f in fields if f in v} for k, v in d["profiles"].items()}
-    return profs, d.get("config", {})
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    return bench.load_profiles(os.path.join(root, "profiles", "kl_profile_b200.json"), levels)
 
 
 @pytest.mark.parametrize("level_mode", [1, 0])
@@ -151,7 +151,7 @@ def test_decisions_match_oracle_bench_config(split_rule, level_mode):
     rules; queues drawn from the ALL mix always holding MM.  The oracle gets the runtime-resolved
     profiles (kl_get_profile), so this compares the decision logic, not the profile plumbing."""
     K.build()
-    profs, kcfg = _bench_profiles()
+    profs, kcfg = _bench_profiles("four" if level_mode == 1 else "all")
     cfg = dict(kcfg)
     cfg.update(split_rule=split_rule, level_mode=level_mode)
     rng = np.random.default_rng(23 + split_rule + 7 * level_mode)

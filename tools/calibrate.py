@@ -196,6 +196,30 @@ def run(out_path):
     print("wrote", out_path, "L0", L0, "cycles", "B", B)
 
 
+def saturation_bmax(sweep: dict, tol: float = 0.01) -> int:
+    """Reading R31: the smallest cap (blocks per SM) whose solo time in the occupancy sweep is
+    within `tol` of the best cap's.  Blocks beyond it add nothing to the kernel's own throughput
+    but take warps, registers, shared memory and issue slots from a co-scheduled partner, which
+    the two-state model does not charge for (measured: C5 +4.5 %, R31)."""
+    sw = {int(c): float(ms) for c, ms in sweep.items()}
+    best = min(sw.values())
+    return min(c for c, ms in sw.items() if ms <= best * (1.0 + tol))
+
+
+def add_saturation(path: str, tol: float = 0.01) -> dict:
+    """Write bmax_sat into every profile of an existing calibration file from its recorded
+    occupancy sweep (measured.<kind>.cap_sweep_ms)."""
+    with open(path) as f:
+        d = json.load(f)
+    out = {}
+    for k, m in d["measured"].items():
+        if m.get("cap_sweep_ms") and k in d["profiles"]:
+            d["profiles"][k]["bmax_sat"] = out[k] = saturation_bmax(m["cap_sweep_ms"], tol)
+    with open(path, "w") as f:
+        json.dump(d, f, indent=1)
+    return out
+
+
 def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
     """Occupancy sweep + least-squares fit of (rm, r) with the pipe ceiling from the plateau."""
     import numpy as np
@@ -215,6 +239,7 @@ def fit_effective(ctx0, insts, profiles, measured, cfg, clock_mhz, n_sm):
         ipc = {b: prof["ipb"] * i.grid / (ms * 1e-3 * f * 4 * n_sm) for b, ms in sweep.items()}
         levels = [b for b in ipc if (b * prof["wpb"]) % 4 == 0 and b * prof["wpb"] // 4 <= 16]
         measured[k]["cap_sweep_ms"] = sweep
+        prof["bmax_sat"] = saturation_bmax(sweep)
         measured[k]["ipc_meas"] = ipc
         prof["rm_profiled"], prof["r_profiled"] = prof["rm"], prof["r"]
         prof["pipe"] = PIPES.get(k, 0)
@@ -280,5 +305,7 @@ if __name__ == "__main__":
     mode = sys.argv[1] if len(sys.argv) > 1 else "run"
     if mode == "target":
         target()
+    elif mode == "sat":      # CPU: bmax_sat from an existing file's occupancy sweeps (R31)
+        print(add_saturation(sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "kl_profile_b200.json")))
     else:
         run(sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out", "kl_profile_b200.json"))
