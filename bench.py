@@ -81,8 +81,9 @@ def parse(argv=None):
     ap.add_argument("--critical", type=int, default=0, choices=[0, 1],
                     help="1: makespan extension of FindCoSchedule (kl_config.critical, reading R29): while one kind's "
                          "predicted remaining solo time exceeds all others' together, only co-schedules with it")
-    ap.add_argument("--bmax", default="sat", choices=["sat", "hw"],
-                    help="b_max with every whole-warp level: the calibrated saturation occupancy (R31) or the hardware limit")
+    ap.add_argument("--bmax", default="hw", choices=["sat", "hw"],
+                    help="b_max with every whole-warp level: the hardware limit (default) or the calibrated "
+                         "saturation occupancy with distinct-kind pairs (R31/R31b, measured option)")
     ap.add_argument("--prof", action="append", default=[], metavar="KIND.FIELD=VALUE",
                     help="A/B knob: override one field of a kind's profile (e.g. MRIQ.bmax=3)")
     ap.add_argument("--set", action="append", default=[], metavar="FIELD=VALUE",
@@ -288,13 +289,13 @@ def build_queue(rank: int, world: int, instances: int, workload: str = "c5", mix
 MODEL_FIELDS = ("rm", "r", "ipb", "pur", "mur", "m_min", "ipc_max", "pipe", "uc", "ru")
 
 
-def load_profiles(path: str, levels: str = "four", bmax: str = "sat"):
+def load_profiles(path: str, levels: str = "four", bmax: str = "hw"):
     """Calibrated model inputs (tools/calibrate.py).  Resource fields (warps, registers, shared
     memory, TMEM, b_max) are left to the runtime, which reads them from the compiled kernels --
-    except that with every whole-warp level (C4 / C5, `levels="all"`) b_max is the kind's
-    saturation occupancy `bmax_sat` (reading R31: the smallest cap whose solo time is within 1 %
-    of the best in the calibration's occupancy sweep) unless `bmax="hw"`.  C2 fixes its levels as
-    quarters of the hardware b_max and keeps it."""
+    except that with every whole-warp level (C4 / C5, `levels="all"`) and `bmax="sat"` b_max is
+    the kind's saturation occupancy `bmax_sat` (reading R31: the smallest cap whose solo time is
+    within 1 % of the best in the calibration's occupancy sweep; a measured option, not the
+    default).  C2 fixes its levels as quarters of the hardware b_max and keeps it."""
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
@@ -370,6 +371,8 @@ def run_kernelet(args, rank, world, local_rank):
         cfg["speculative"] = 1
     if args.critical:
         cfg["critical"] = 1
+    if args.levels == "all" and args.bmax == "sat":
+        cfg["distinct_kinds"] = 1      # R31b: a same-kind pair is the kind above its saturation occupancy
     for kv in args.set:
         k, _, v = kv.partition("=")
         cfg[k] = float(v) if "." in v else int(v)
@@ -690,7 +693,7 @@ class OracleLeg:
     time."""
 
     def __init__(self, kinds: list[str], size: str, profile_path: str | None = None, split_rule: int = 1,
-                 levels: str = "four", alpha=None, max_decisions: int = 200, cp_min=None, bmax: str = "sat"):
+                 levels: str = "four", alpha=None, max_decisions: int = 200, cp_min=None, bmax: str = "hw"):
         import oracle as O
         O.build()
         self.O = O
@@ -709,7 +712,8 @@ class OracleLeg:
                            b0=pcfg.get("b0", 0.0), W=16)
         ap, am = alpha if alpha else (pcfg.get("alpha_p", 0.4), pcfg.get("alpha_m", 0.1))
         self.sched_kw = dict(ap=ap, am=am, mode="4" if levels == "four" else "all", split_rule=split_rule,
-                             cp_min=pcfg.get("cp_min", 0.0) if cp_min is None else cp_min)
+                             cp_min=pcfg.get("cp_min", 0.0) if cp_min is None else cp_min,
+                             distinct_kinds=levels == "all" and bmax == "sat")
         self.max_decisions = max_decisions
         self.config = {"L0": self.cfg.L0, "B": self.cfg.B, "a0": self.cfg.a0, "b0": self.cfg.b0, "W_v": 16,
                        **self.sched_kw}
@@ -764,9 +768,9 @@ def _oracle_sample(O, data, sizes, frac, cores) -> dict:
     return out
 
 
-def _oracle_profiles(path: str | None = None, levels: str = "four", bmax: str = "sat"):
+def _oracle_profiles(path: str | None = None, levels: str = "four", bmax: str = "hw"):
     """The oracle's profile table: the calibrated profiles with the b_max the GPU run uses
-    (load_profiles: bmax_sat with every whole-warp level)."""
+    (load_profiles: bmax_sat with every whole-warp level when bmax="sat")."""
     path = path or os.path.join(ROOT, "profiles", "kl_profile_b200.json")
     if not os.path.exists(path):
         return None, {}

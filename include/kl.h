@@ -173,6 +173,12 @@ typedef struct {
                                   (remaining blocks x I / IPC_solo) exceeds all the others' together,
                                   only co-schedules that include that kind are considered (the
                                   model's max CP among them); 0 (default): the paper's greedy */
+    int32_t distinct_kinds;    /* 1: FindCoSchedule pairs two different kinds only (reading R31b:
+                                  with saturation b_max, R31, two instances of one kind at (b1, b2)
+                                  are that kind at b1 + b2 >= b_sat blocks per SM, which its
+                                  occupancy sweep measures as no faster than solo); 0 (default):
+                                  same-kind pairs are candidates */
+    int32_t reserved0;         /* 0 */
     const kl_profile* profiles;   /* KL_NKINDS entries, or NULL for the built-in table */
     void* stream_a;            /* optional cudaStream_t: first stream of the launch pool       */
     void* stream_b;            /* optional cudaStream_t: second stream of the launch pool      */

@@ -466,10 +466,12 @@ def predict_cfg(p1, b1, p2, b2, cfg, nsched=4, states=2, granularity=0) -> Pred:
                     kmodel3_of(p2, states, granularity, nsched), b2, solo_b(p2, nsched), nsched, cfg)
 
 
-def pairs_of(pending: list[dict]) -> list[tuple[int, int]]:
+def pairs_of(pending: list[dict], distinct_kinds: bool = False) -> list[tuple[int, int]]:
     """Candidate pairs over pending instances in arrival order, one pair per
     unordered kind pair (earliest instances), same-kind pairs included when two instances of a
-    kind are pending.  Returns index pairs into `pending`."""
+    kind are pending -- unless `distinct_kinds` (reading R31b: with saturation b_max a same-kind
+    pair is the kind at b1 + b2 >= b_sat blocks, no faster than solo).  Returns index pairs into
+    `pending`."""
     reps, seen_k = [], {}
     for i, e in enumerate(pending):
         c = seen_k.get(e["kind"], 0)
@@ -479,7 +481,7 @@ def pairs_of(pending: list[dict]) -> list[tuple[int, int]]:
     out, seen = [], set()
     for a, b in itertools.combinations(reps, 2):
         key = tuple(sorted((pending[a]["kind"], pending[b]["kind"])))
-        if key in seen:
+        if key in seen or (distinct_kinds and key[0] == key[1]):
             continue
         seen.add(key)
         out.append((a, b))
@@ -531,14 +533,14 @@ def _better_split(a, b, rule=0):
 
 def find_co_schedule(pending: list[dict], profs: dict, cfg: SmCfg, sm=B200_SM, nsched=4,
                      ap=0.4, am=0.1, mode="all", n_sm=148, cache=None, cp_min=0.0, split_rule=0,
-                     states=2, granularity=0) -> dict:
+                     states=2, granularity=0, distinct_kinds=False) -> dict:
     """Proc. FindCoSchedule: candidates -> prune -> model CP -> argmax.
 
     Per surviving pair the slice ratio is the argmin of dT (Eq.8) over maximal splits; across
     pairs the max CP wins (ties: earliest pair).  Best CP <= 0 (R25) or < 2 candidates: the
     oldest pending kernel runs solo at b_max.  Slice sizes: size_i = m * b_i * n_sm with the
     common m = max(m_min) of the p% rule (a9)."""
-    pairs = pairs_of(pending)
+    pairs = pairs_of(pending, distinct_kinds)
     pairs, alphas = prune(pending, pairs, profs, ap, am)
     best = None
     evaluated = []
@@ -586,7 +588,8 @@ def _rate(prof, ipc, n_vsm):
 
 
 def alg1_makespan(queue: list[dict], profs: dict, cfg, sm=B200_SM, nsched=4, ap=0.4, am=0.1,
-                  mode="all", n_sm=148, launch_overhead=0.0, decide=None, split_rule=0, cp_min=0.0):
+                  mode="all", n_sm=148, launch_overhead=0.0, decide=None, split_rule=0, cp_min=0.0,
+                  distinct_kinds=False):
     """Alg.1 on an all-pending queue, executed in the model: each co-schedule runs
     until either kernel exhausts its blocks (R11), then the scheduler re-plans.  Returns
     (makespan in cycles, trace)."""
@@ -595,7 +598,8 @@ def alg1_makespan(queue: list[dict], profs: dict, cfg, sm=B200_SM, nsched=4, ap=
     t, trace, cache = 0.0, [], {}
     while pend:
         dec = decide(pend) if decide else find_co_schedule(pend, profs, cfg, sm, nsched, ap, am,
-                                                           mode, n_sm, cache, split_rule=split_rule, cp_min=cp_min)
+                                                           mode, n_sm, cache, split_rule=split_rule, cp_min=cp_min,
+                                                           distinct_kinds=distinct_kinds)
         if dec["solo"]:
             k = pend[dec["ia"]]
             pr = profs[k["kind"]]

@@ -115,6 +115,7 @@ class Config(C.Structure):
                 ("age_limit_us", C.c_int32), ("mc_seed", C.c_int32), ("speculative", C.c_int32), ("max_regs_per_sm", C.c_int32), ("max_smem_per_sm", C.c_int32),
                 ("max_warps_per_sm", C.c_int32), ("max_blocks_per_sm", C.c_int32),
                 ("mm_stages", C.c_int32), ("critical", C.c_int32),
+                ("distinct_kinds", C.c_int32), ("reserved0", C.c_int32),
                 ("profiles", C.POINTER(Profile)), ("stream_a", _vp), ("stream_b", _vp),
                 ("counters_dev", _vp)]
 

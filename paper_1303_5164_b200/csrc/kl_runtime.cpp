@@ -511,7 +511,7 @@ kl_status find_co_schedule(kl_ctx* ctx, Decision* d) {
         for (size_t b = a + 1; b < reps.size(); ++b) {
             int ka = R[reps[a]]->kind, kb = R[reps[b]]->kind;
             int lo = std::min(ka, kb), hi = std::max(ka, kb);
-            if (seen_pair[lo][hi]) continue;
+            if (seen_pair[lo][hi] || (ctx->cfg.distinct_kinds && ka == kb)) continue;
             seen_pair[lo][hi] = true;
             pairs.push_back({reps[a], reps[b]});
         }
@@ -1169,6 +1169,7 @@ kl_status kl_create(int device, const kl_config* cfg_in, kl_ctx** out) {
     if (cfg.n_sched <= 0 || 64 % cfg.n_sched) return KL_EINVAL;
     if (cfg.mm_stages && cfg.mm_stages != 2 && cfg.mm_stages != 3 && cfg.mm_stages != 4 && cfg.mm_stages != 6)
         return KL_EINVAL;
+    if ((cfg.distinct_kinds != 0 && cfg.distinct_kinds != 1) || cfg.reserved0) return KL_EINVAL;
     for (int k = 0; k < KL_NKINDS; ++k) ctx->prof[k] = cfg.profiles ? cfg.profiles[k] : kDefaultProfiles[k];
     cfg.profiles = nullptr;
     ctx->device = device;

@@ -109,7 +109,11 @@ def test_oracle_leg_uses_the_gpu_runs_model_config():
     kw = dict(profile_path=None, split_rule=1, levels="four", alpha=None)
     leg.__init__(["PC", "BS"], "small", **kw)
     assert leg.sched_kw == {"ap": pcfg["alpha_p"], "am": pcfg["alpha_m"], "mode": "4", "split_rule": 1,
-                            "cp_min": pcfg.get("cp_min", 0.0)}
+                            "cp_min": pcfg.get("cp_min", 0.0), "distinct_kinds": False}
+    leg2 = bench.OracleLeg.__new__(bench.OracleLeg)
+    leg2.__init__(["PC", "BS"], "small", **dict(kw, levels="all", bmax="sat"))
+    assert leg2.sched_kw["mode"] == "all" and leg2.sched_kw["distinct_kinds"] is True
+    assert leg2.profs["MRIQ"]["bmax"] == leg2.profs["MRIQ"]["bmax_sat"]
     assert abs(leg.cfg.L0 - pcfg["L0"]) < 1e-9 and abs(leg.cfg.B - pcfg["B"]) < 1e-12
     r = leg.run(target_s=0.5)
     assert r["kind"] == "oracle" and r["value"] > 0 and r["cores"] >= 1
@@ -123,9 +127,9 @@ def test_pc_reports_both_atoms():
 
 
 def test_saturation_bmax_reading_r31():
-    """R31: b_max for every whole-warp level (C4 / C5) is the smallest cap whose solo time is
-    within 1 % of the best in the calibration sweep; C2 (quarters of b_max) keeps the hardware
-    b_max; the oracle leg sees the same b_max as the GPU run."""
+    """R31 (option --bmax sat): b_max for every whole-warp level is the smallest cap whose solo
+    time is within 1 % of the best in the calibration sweep; C2 (quarters of b_max) keeps the
+    hardware b_max; the oracle leg sees the same b_max as the GPU run."""
     import json
     import os
     sys_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools")
@@ -142,13 +146,13 @@ def test_saturation_bmax_reading_r31():
     for k, m in d["measured"].items():
         if m.get("cap_sweep_ms") and k in d["profiles"]:
             assert d["profiles"][k]["bmax_sat"] == cal.saturation_bmax(m["cap_sweep_ms"])
-    p_all, _ = bench.load_profiles(path, "all")
-    p_hw, _ = bench.load_profiles(path, "all", "hw")
+    p_all, _ = bench.load_profiles(path, "all", "sat")
+    p_hw, _ = bench.load_profiles(path, "all")
     p_four, _ = bench.load_profiles(path, "four")
     assert p_all["MRIQ"]["bmax"] == d["profiles"]["MRIQ"]["bmax_sat"] < d["profiles"]["MRIQ"]["bmax"]
     assert "bmax" not in p_hw["MRIQ"] and "bmax" not in p_four["MRIQ"]   # left to the runtime
-    o_all, _ = bench._oracle_profiles(path, "all")
-    o_four, _ = bench._oracle_profiles(path, "four")
+    o_all, _ = bench._oracle_profiles(path, "all", "sat")
+    o_four, _ = bench._oracle_profiles(path, "four", "sat")
     for k in bench.ALL:
         assert o_all[k]["bmax"] == p_all[k]["bmax"]
         assert o_four[k]["bmax"] == d["profiles"][k]["bmax"]

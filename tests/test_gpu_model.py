@@ -130,20 +130,20 @@ def _args_of(kind, keep={}):
     return keep["MM"].grid, keep["MM"].args
 
 
-def _bench_profiles(levels="four"):
-    """The calibrated B200 profile and scheduler config the bench runs (bench.load_profiles: with
-    every whole-warp level b_max is the saturation occupancy, R31)."""
+def _bench_profiles(levels="four", bmax="hw"):
+    """The calibrated B200 profile and scheduler config the bench runs (bench.load_profiles; with
+    every whole-warp level and bmax="sat", b_max is the saturation occupancy, R31)."""
     import os
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
     import bench
-    return bench.load_profiles(os.path.join(root, "profiles", "kl_profile_b200.json"), levels)
+    return bench.load_profiles(os.path.join(root, "profiles", "kl_profile_b200.json"), levels, bmax)
 
 
-@pytest.mark.parametrize("level_mode", [1, 0])
+@pytest.mark.parametrize("level_mode,bmax", [(1, "hw"), (0, "hw"), (0, "sat")])
 @pytest.mark.parametrize("split_rule", [1, 0])
-def test_decisions_match_oracle_bench_config(split_rule, level_mode):
+def test_decisions_match_oracle_bench_config(split_rule, level_mode, bmax):
     """The bench's decision configurations: calibrated profiles with the resource fields the
     runtime reads from the compiled kernels (MM: TMEM- and shared-memory-bound, one block per SM),
     the four C2 occupancy levels (level_mode = 1 <-> oracle mode "4"; C2) or every whole-warp level
@@ -151,9 +151,9 @@ def test_decisions_match_oracle_bench_config(split_rule, level_mode):
     rules; queues drawn from the ALL mix always holding MM.  The oracle gets the runtime-resolved
     profiles (kl_get_profile), so this compares the decision logic, not the profile plumbing."""
     K.build()
-    profs, kcfg = _bench_profiles("four" if level_mode == 1 else "all")
+    profs, kcfg = _bench_profiles("four" if level_mode == 1 else "all", bmax)
     cfg = dict(kcfg)
-    cfg.update(split_rule=split_rule, level_mode=level_mode)
+    cfg.update(split_rule=split_rule, level_mode=level_mode, distinct_kinds=int(bmax == "sat"))
     rng = np.random.default_rng(23 + split_rule + 7 * level_mode)
     all_mix = ["PC", "SAD", "SPMV", "ST", "MM", "MRIQ", "BS", "TEA"]
     for rep in range(16):
@@ -171,7 +171,7 @@ def test_decisions_match_oracle_bench_config(split_rule, level_mode):
         ocfg = O.smcfg(W=16, L0=kcfg["L0"], B=kcfg["B"], a0=kcfg.get("a0", 1.0), b0=kcfg.get("b0", 0.0))
         ref = O.find_co_schedule(pend, resolved, ocfg, ap=ctx.config.alpha_p, am=ctx.config.alpha_m,
                                  mode="4" if level_mode == 1 else "all", cp_min=ctx.config.cp_min,
-                                 split_rule=split_rule)
+                                 split_rule=split_rule, distinct_kinds=bool(ctx.config.distinct_kinds))
         for d in (d1, d2):
             assert bool(d.solo) == bool(ref["solo"]), (kinds, d.solo, ref["solo"])
             assert d.id1 == pend[ref["ia"]]["id"], (kinds, d.id1, ref)

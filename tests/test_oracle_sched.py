@@ -151,6 +151,7 @@ def test_pruning_relaxation():
 def test_pairs_of_order_and_dedup():
     pend = [{"kind": "A"}, {"kind": "B"}, {"kind": "A"}, {"kind": "C"}, {"kind": "A"}]
     assert O.pairs_of(pend) == [(0, 1), (0, 2), (0, 3), (1, 3)]
+    assert O.pairs_of(pend, distinct_kinds=True) == [(0, 1), (0, 3), (1, 3)]   # R31b: no A+A
 
 
 def _calibrated():
