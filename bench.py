@@ -550,7 +550,10 @@ def sample_parity(insts, data, per_kind: int = 64) -> dict:
     return out
 
 
-def _time_streams(fn, dev, flush, barrier, reps=3):
+def _time_streams(fn, dev, flush, barrier, reps=3, pre=None):
+    """Device time of fn's launches between two events on the current stream, L2 flushed before
+    each rep.  pre(s), if given, is enqueued before the first event (a device-side delay that keeps
+    the host's launch latency out of a single short kernel's interval)."""
     import torch
     ts = []
     for _ in range(reps):
@@ -558,6 +561,8 @@ def _time_streams(fn, dev, flush, barrier, reps=3):
         barrier()
         s = torch.cuda.current_stream(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if pre is not None:
+            pre(s)
         e0.record(s)
         fn(s, e0)
         e1.record(s)
@@ -606,7 +611,10 @@ def per_kernel(ctx, insts, data, dev, flush, barrier) -> dict:
         if i.kind in seen:
             continue
         seen.add(i.kind)
-        ms = _time_streams(lambda s, e0, i=i: ctx.run_plain(i.kind, i.grid, i.args, s), dev, flush, barrier, reps=5)
+        # the GPU is idle after the barrier: without a device-side delay before the first event the
+        # interval would include the host's launch path (~10-17 us, 25 % of MM's 60 us)
+        ms = _time_streams(lambda s, e0, i=i: ctx.run_plain(i.kind, i.grid, i.args, s), dev, flush, barrier, reps=5,
+                           pre=lambda s: ctx.delay(s, 200_000))
         w = algorithmic_work(i.kind, data[i.kind]["params"])
         out[i.kind] = {"ms": ms, "grid": i.grid, **w}
     return out

@@ -401,6 +401,74 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
+// Optional Body::kRun + Body::run(P, st, dsmem, fetcher, L): the pair body owns its tile loop
+// (its roles synchronise through mbarriers instead of one CTA + one cluster barrier per tile)
+// and calls fetcher.next() -- on the leader's thread 0 only -- whenever it wants the next
+// virtual block; next() returns (vb << 2) | part, or 0xFFFFFFFF when the pair is done.
+template <class B, class = void>
+struct has_run : std::false_type {};
+template <class B>
+struct has_run<B, std::void_t<decltype(B::kRun)>> : std::integral_constant<bool, B::kRun> {};
+
+// The persistent launcher's fetch (leave on a lowered cap, stop requests, the drained event),
+// one virtual block at a time out of the fetched chunk; stamps the start of each block.
+struct PairFetcher {
+    const KlLaunch* L;
+    KlCtl* ctl;
+    uint32_t len, sm, cur, end, nexec;
+    bool counted, done;
+    __device__ uint32_t next() {
+        if (done) return 0xFFFFFFFFu;
+        if (cur >= end) {
+            const uint32_t cap = cap_now(*L, ctl);
+            if (cap) {
+                uint32_t c = *(volatile uint32_t*)&ctl->sm_count[sm];
+                while (c > cap) {
+                    const uint32_t prev = atomicCAS(&ctl->sm_count[sm], c, c - 1u);
+                    if (prev == c) { counted = false; done = true; return 0xFFFFFFFFu; }
+                    c = prev;
+                }
+            }
+            const unsigned long long req = ctl->stop_req;
+            unsigned long long old = atomicAdd(&ctl->word, (unsigned long long)L->chunk);
+            if ((req & 1ull) && !(old & KL_W_STOP) && ((req >> 1) & 0x7full) == kl_w_epoch(old)) {
+                stop_word(ctl, kl_w_epoch(old), (uint32_t)(req >> 32));
+                old = (atomicAdd(&ctl->word, 0ull) & ~KL_W_MASK28) | (old & KL_W_MASK28);
+            }
+            const uint32_t vb = kl_w_next(old);
+            const uint32_t lim = word_limit(old, len);
+            if (vb >= len && lim == len && L->rec) {
+                if (atomicCAS(&ctl->drained, 0u, 1u) == 0u) {
+                    L->rec->drained = 1u;
+                    __threadfence_system();
+                }
+            }
+            if (vb >= lim) { done = true; return 0xFFFFFFFFu; }
+            cur = vb;
+            end = min(vb + L->chunk, lim);
+        }
+        const uint32_t v = cur++;
+        ++nexec;
+        if (L->stamps) L->stamps[2 * (size_t)v] = gtimer();
+        return v << 2;
+    }
+};
+
+// The plain pair grid's static schedule: cluster c takes offset + c, c + n_clusters, ... and, when
+// the last round would leave more than half the pairs idle, half tiles of the remainder.
+struct StaticPairFetcher {
+    uint32_t offset, c, ncl, full, rem, i;
+    bool split;
+    __device__ uint32_t next() {
+        const uint32_t v = c + i * ncl;
+        ++i;
+        if (v < full) return (offset + v) << 2;
+        if (split && v - full < ncl && c < 2 * rem && v - full == c)   // the one half-tile item
+            return ((offset + full + c / 2) << 2) | (1u + (c & 1u));
+        return 0xFFFFFFFFu;
+    }
+};
+
 template <class Body>
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(64)
 k_persistent_pair(const __grid_constant__ typename Body::Params P, const __grid_constant__ KlLaunch L) {
@@ -445,6 +513,11 @@ k_persistent_pair(const __grid_constant__ typename Body::Params P, const __grid_
         Body::init(P, st, dsmem);
         uint32_t nexec = 0;
         bool counted = true;
+        if constexpr (has_run<Body>::value) {
+            PairFetcher f{&L, ctl, len, sm, 0u, 0u, 0u, true, false};
+            Body::run(P, st, dsmem, f, &L);
+            if (threadIdx.x == 0 && rank == 0) { nexec = f.nexec; counted = f.counted; }
+        } else
         for (uint32_t it = 0;; ++it) {
             if (threadIdx.x == 0 && rank == 0) {
                 uint32_t vb = 0, end = 0;
@@ -533,6 +606,12 @@ k_plain_pair(const __grid_constant__ typename Body::Params P, uint32_t offset, u
     const uint32_t rounds = n / ncl, rem = n - rounds * ncl;
     const bool split = rem > 0 && 2 * rem <= ncl;
     const uint32_t full = split ? rounds * ncl : n;
+    if constexpr (has_run<Body>::value) {
+        StaticPairFetcher f{offset, c, ncl, full, rem, 0u, split};
+        Body::run(P, st, dsmem, f, (const KlLaunch*)nullptr);
+        Body::fini(P, st, dsmem);
+        return;
+    }
     bool first = true;
     for (uint32_t v = c; v < full; v += ncl) {
         if (!first) {                    // the previous tile's hand-off, as in the pair launcher

@@ -46,6 +46,15 @@ constexpr int kStageLevels[4] = {2, 3, 4, 6};
 constexpr int kEpiBox = 32;                        // C store box: 32 rows x 32 fp32 (128 B rows)
 constexpr int kEpiBufBytes = kEpiBox * kEpiBox * 4;  // 4 KiB
 constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;      // 4 epilogue warps x 2 buffers
+// Barrier block (offsets from State::bars): full[s] 0+8s, empty[s] 64+8s, tfull[b] 128+8b,
+// tempty[b] 144+8b, tile-info full[q] 160+8q, TMEM base address 192, need-next 200,
+// tile-info empty[q] 256+8q, tile-info slots (u32) 320+4q.
+constexpr int kBarBytes = 512;
+constexpr int kTileQ = 4;                            // tile-info ring depth (run loop)
+constexpr uint32_t kItemNone = 0xFFFFFFFFu;          // end of the pair's tile sequence
+// tile-info consumers: producer + MMA issuer + 4 epilogue warps (CTA 0), producer + 4 epilogue
+// warps (CTA 1)
+constexpr uint32_t kTileConsumers = 11;
 
 struct MMParams {
     CUtensorMap ta;   // A  [M][K] bf16, box 64 x 128
@@ -64,7 +73,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // tile j < 8: [0] MMA issuer sees the first stage full, [1] last MMA of the tile issued,
 // [2] epilogue (rank 0, warp 4) starts waiting for the accumulator, [3] its TMA stores issued;
 // per pair [kProbeTiles*4] kernel entry, [+1] after init, [+2] before fini, [+3] end of fini.
-constexpr int kProbeTiles = 8, kProbeStride = kProbeTiles * 4 + 4;
+constexpr int kProbeTiles = 8, kProbeF = 8, kProbeStride = kProbeTiles * kProbeF + 4;
 __device__ unsigned long long g_mm_probe[96 * kProbeStride];
 __device__ __forceinline__ unsigned long long probe_now() {
     unsigned long long t;
@@ -76,9 +85,11 @@ __device__ __forceinline__ uint32_t probe_cluster() {
     asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(c));
     return c;
 }
-#define MM_PROBE(j, f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96 && (j) < kProbeTiles) g_mm_probe[c_ * kProbeStride + (j) * 4 + (f)] = probe_now(); } while (0)
-#define MM_PROBE_K(f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96) g_mm_probe[c_ * kProbeStride + kProbeTiles * 4 + (f)] = probe_now(); } while (0)
+#define MM_PROBE(j, f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96 && (j) < kProbeTiles) g_mm_probe[c_ * kProbeStride + (j) * kProbeF + (f)] = probe_now(); } while (0)
+#define MM_PROBE_K(f) do { const uint32_t c_ = probe_cluster(); if (c_ < 96) g_mm_probe[c_ * kProbeStride + kProbeTiles * kProbeF + (f)] = probe_now(); } while (0)
+#define MM_PROBE_T(f) do { if (probe_tile < kProbeTiles) MM_PROBE(probe_tile, f); } while (0)
 #else
+#define MM_PROBE_T(f) do { } while (0)
 #define MM_PROBE(j, f) do { } while (0)
 #define MM_PROBE_K(f) do { } while (0)
 #endif
@@ -97,6 +108,28 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "@!p bra W_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
+}
+// Waits whose barrier receives arrivals from the peer CTA (acquire at cluster scope: the peer's
+// shared::cluster writes before its release-arrive are visible after the wait).
+__device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// Arrive on this CTA's barrier with CTA-scope release.  Not cluster scope: a cluster-scope
+// release issued by the MMA thread waits for its outstanding tcgen05 MMAs (device stamps,
+// tools/mm_stamp_probe.py: ~1.8 us per tile boundary -- the same stall the per-tile
+// barrier.cluster.arrive.release of the block() path pays).
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// arrive on the barrier at shared::cluster address `bar_cl` (this CTA's or the peer's)
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
 }
 // TMA 2-D load into this CTA's shared memory; completion bytes land on `bar_cluster` (a
 // shared::cluster address: the leader CTA's full barrier).
@@ -151,7 +184,7 @@ struct BodyMM {
     static_assert(S >= 2 && S <= 6, "stages");
     using Params = MMParams;
     static constexpr int kThreads = ::kThreads, kChunk = 1;
-    static constexpr int kDynSmem = S * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kDynSmem = S * kStageBytes + kEpiBytes + 1024 /*align*/ + kBarBytes;
     static constexpr int kEpiOffset = S * kStageBytes;
     static constexpr int kBarOffset = S * kStageBytes + kEpiBytes;
     struct State {
@@ -182,6 +215,13 @@ struct BodyMM {
             }
             mbar_init(st.bars + 128, 1);
             mbar_init(st.bars + 136, 1);
+            mbar_init(st.bars + 144, 8);     // tempty[b]: the 4 epilogue warps of both CTAs drained b
+            mbar_init(st.bars + 152, 8);
+            mbar_init(st.bars + 200, 1);     // need-next: the leader's producer asks for the next tile
+            for (int q = 0; q < kTileQ; ++q) {
+                mbar_init(st.bars + 160 + 8 * q, 1);
+                mbar_init(st.bars + 256 + 8 * q, kTileConsumers);
+            }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
@@ -204,9 +244,14 @@ struct BodyMM {
     // bulk-tensor stores (whole 128-byte lines; a thread-per-row STG epilogue issues 32 partial
     // sectors per instruction and was the launch's tail).
     __device__ static void drain(const Params& P, State& st, int m, int col, int w, uint32_t b) {
+        drain_tile(P, st, m, col, w, b, (st.tph >> b) & 1u, st.ntile - 1);
+        if ((threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0 && st.rank == 0) MM_PROBE(st.ntile - 1, 3);
+    }
+    __device__ static void drain_tile(const Params& P, State& st, int m, int col, int w, uint32_t b, uint32_t parity,
+                                      uint32_t probe_tile = 0xFFFFu) {
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (warp == 4 && lane == 0 && st.rank == 0) MM_PROBE(st.ntile - 1, 2);
-        mbar_wait(st.bars + 128 + 8 * b, (st.tph >> b) & 1u);
+        mbar_wait(st.bars + 128 + 8 * b, parity);
+        if (warp == 4 && lane == 0 && st.rank == 0) MM_PROBE_T(2);
         tc_fence_after();
         const int q = warp & 3;                              // TMEM lane quarter of this warp
         const int row0 = m * (2 * BM) + (int)st.rank * BM + q * 32;
@@ -218,7 +263,9 @@ struct BodyMM {
             TMEM_LD_X32(tbase + (uint32_t)c, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const uint32_t buf = ebuf + (uint32_t)((c >> 5) & 1) * kEpiBufBytes;
+#ifdef KL_MM_EPI_TMA
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // buf's last store read it
+#endif
             __syncwarp();
 #ifdef KL_MM_DBG_NOEPI      // A/B probe: no C stores
             if (r[0] == 0x7fffffffu && r[1] == 0x7fffffffu)
@@ -230,6 +277,7 @@ struct BodyMM {
                              "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
                              : "memory");
             }
+#ifdef KL_MM_EPI_TMA
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
@@ -239,21 +287,175 @@ struct BodyMM {
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
+#else
+            // coalesced stores from the staged 32x32 box: 8 lanes per 128-byte row, 4 rows per
+            // instruction (whole lines; no TMA store queued behind the operand loads, no bulk-group
+            // wait before the buffer's reuse -- the accumulator frees at the TMEM-load rate)
+            __syncwarp();
+            {
+                const int seg = lane & 7;
+                float* cbase = P.C + (size_t)row0 * (size_t)P.N + (size_t)(col + c) + (size_t)seg * 4;
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int row = it * 4 + (lane >> 3);
+                    const uint32_t a = buf + (uint32_t)row * 128u + (uint32_t)((seg ^ (row & 7)) * 16);
+                    uint32_t v0, v1, v2, v3;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3) : "r"(a));
+                    float* g = cbase + (size_t)row * (size_t)P.N;
+                    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(g), "r"(v0), "r"(v1), "r"(v2), "r"(v3)
+                                 : "memory");
+                }
+            }
+#endif
         }
-        if (warp == 4 && lane == 0 && st.rank == 0) MM_PROBE(st.ntile - 1, 3);
         tc_fence_before();
     }
     __device__ static void fini(const Params& P, State& st, char*) {
         if (threadIdx.x == 0 && st.rank == 0) MM_PROBE_K(2);
         if (st.prev_m >= 0 && (threadIdx.x >> 5) >= 4) drain(P, st, st.prev_m, st.prev_col, st.prev_w, (st.ntile - 1) & 1u);
+#ifdef KL_MM_EPI_TMA
         if ((threadIdx.x >> 5) >= 4 && (threadIdx.x & 31) == 0)
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // C written before the kernel's end
+#endif
         tc_fence_before();
         cluster_sync_all();   // both CTAs drained: the pair's columns can go
         tc_fence_after();
         if ((threadIdx.x >> 5) == 1)
             asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols));
         if (threadIdx.x == 0 && st.rank == 0) MM_PROBE_K(3);
+    }
+    // ---- decoupled tile loop (the launchers' Body::run path) ---------------------------------
+    // The pair's roles run their own loops over the pair's tile sequence, synchronised only by
+    // mbarriers: the leader's producer takes each tile from `f` (the launcher's fetch, or the
+    // plain grid's static schedule) as soon as it has issued the previous tile's last operand
+    // load, publishes it through a 4-deep tile-info ring in both CTAs' shared memory, and keeps
+    // streaming operands into the ring of stages across the tile boundary; the MMA issuer waits
+    // for an accumulator only until both CTAs' epilogues released it (tempty); the epilogue of
+    // tile i overlaps the mainloop of tile i+1.  Against the per-tile block() (one CTA barrier and
+    // one cluster barrier per tile, the producer idle until both) this removes the ~2.2 us gap
+    // between a tile's last MMA and the next tile's first full stage (tools/mm_stamp_probe.py).
+    // Item = (virtual block << 2) | part (0: 256x256 tile, 1 / 2: its left / right 256x128 half).
+    static constexpr bool kRun = true;
+    __device__ static uint32_t tile_item(State& st, uint32_t i) {   // consumer side of the tile-info ring
+        const uint32_t q = i % kTileQ;
+        mbar_wait_cl(st.bars + 160 + 8 * q, (i / kTileQ) & 1u);
+        uint32_t item;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(item) : "r"(st.bars + 320 + 4 * q) : "memory");
+        return item;
+    }
+    __device__ static void tile_release(State& st, uint32_t i) {   // one arrival per consumer
+        const uint32_t bar = st.bars + 256 + 8 * (i % kTileQ);
+        if (st.rank == 0) mbar_arrive_local(bar);
+        else mbar_arrive_cl(map_rank(bar, 0u));
+    }
+    __device__ static void load_tile(const Params& P, State& st, uint32_t item, uint32_t probe_i = 0xFFFFu) {   // producer lanes
+        const uint32_t vb = item >> 2;
+        const int part = (int)(item & 3u);
+        const int tiles_n = P.N / BN;
+        const int tm = (int)vb / tiles_n, tn = (int)vb % tiles_n;
+        const int nk = P.K / BK;
+        const int w = part ? BN / 2 : BN;
+        const int col = tn * BN + (part == 2 ? BN / 2 : 0);
+        const CUtensorMap* tmb = part ? &P.tbh : &P.tb;
+        const uint32_t tx = 2u * (uint32_t)(BM * BK * 2 + (w / 2) * BK * 2);
+        const int arow = tm * (2 * BM) + (int)st.rank * BM, brow = col + (int)st.rank * (w / 2);
+        const int kneed = nk > S ? nk - S : 0;
+        for (int kb = 0; kb < nk; ++kb) {
+            // the leader asks for the next tile S stages before this one's last load, so the
+            // scheduler's fetch overlaps the loads still to come (a just-in-time claim)
+            if (kb == kneed && st.rank == 0) mbar_arrive_local(st.bars + 200);
+            mbar_wait(st.bars + 64 + 8 * st.stage, st.phase ^ 1u);
+            if (kb == 0 && st.rank == 0 && probe_i < 8) MM_PROBE(probe_i, 5);
+            const uint32_t full = st.bars + 8 * st.stage;
+            const uint32_t sa = st.base + st.stage * kStageBytes, sb = sa + BM * BK * 2;
+            if (st.rank == 0) mbar_expect_tx(full, tx);
+            const uint32_t full_lead = map_rank(full, 0u);
+            tma_load_2d_pair(sa, &P.ta, full_lead, kb * BK, arow);
+            tma_load_2d_pair(sb, tmb, full_lead, kb * BK, brow);
+            if (++st.stage == S) { st.stage = 0; st.phase ^= 1u; }
+        }
+    }
+    template <class F>
+    __device__ static void run(const Params& P, State& st, char*, F& f, const KlLaunch* L) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const int nk = P.K / BK;
+        if (warp == 0 && lane == 0 && st.rank == 0) {
+            // scheduler (the leader's thread 0, which owns the launcher's fetch state): the first
+            // tile at once, each next one when the leader's producer asks; publishing needs a
+            // cluster-scope release, which this thread -- unlike the producer with its TMA loads
+            // in flight -- pays without waiting
+            for (uint32_t i = 0;; ++i) {
+                if (i >= 1) mbar_wait(st.bars + 200, (i - 1u) & 1u);
+                const uint32_t item = f.next();
+                const uint32_t q = i % kTileQ;
+                if (i >= kTileQ) mbar_wait_cl(st.bars + 256 + 8 * q, (i / kTileQ - 1u) & 1u);
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(st.bars + 320 + 4 * q), "r"(item) : "memory");
+                st_cluster_u32(map_rank(st.bars + 320 + 4 * q, 1u), item);
+                mbar_arrive_local(st.bars + 160 + 8 * q);
+                mbar_arrive_cl(map_rank(st.bars + 160 + 8 * q, 1u));
+                if (i < 8) MM_PROBE(i, 4);
+                if (item == kItemNone) break;
+            }
+        } else if (warp == 2 && lane == 0) {
+            for (uint32_t i = 0;; ++i) {                     // producers (both CTAs)
+                const uint32_t item = tile_item(st, i);
+                tile_release(st, i);
+                if (item == kItemNone) break;
+                load_tile(P, st, item, i);
+            }
+        } else if (warp == 1 && lane == 0 && st.rank == 0) {
+            tc_fence_after();
+            for (uint32_t i = 0;; ++i) {                     // MMA issuer
+                const uint32_t item = tile_item(st, i);
+                if (i < 8) MM_PROBE(i, 6);
+                tile_release(st, i);
+                if (item == kItemNone) break;
+                const uint32_t acc = i & 1u, u = i >> 1;
+                if (u >= 1) mbar_wait_cl(st.bars + 144 + 8 * acc, (u - 1u) & 1u);
+                if (i < 8) MM_PROBE(i, 7);
+                tc_fence_after();
+                const uint32_t idesc = (item & 3u) ? kIdescHalf : kIdesc;
+                const uint32_t tacc = st.tmem + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(st.bars + 8 * st.stage, st.phase);
+                    tc_fence_after();
+                    if (kb == 0 && i < 8) MM_PROBE(i, 0);
+                    const uint32_t sa = st.base + st.stage * kStageBytes, sb = sa + BM * BK * 2;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_bf16_pair(tacc, umma_desc(sa + k * 32), umma_desc(sb + k * 32), idesc,
+                                       (kb | k) != 0 ? 1u : 0u);
+                    umma_commit_pair(st.bars + 64 + 8 * st.stage);
+                    if (++st.stage == S) { st.stage = 0; st.phase ^= 1u; }
+                }
+                umma_commit_pair(st.bars + 128 + 8 * acc);
+                if (i < 8) MM_PROBE(i, 1);
+            }
+        } else if (warp >= 4) {
+            const int tiles_n = P.N / BN;
+            for (uint32_t i = 0;; ++i) {                     // epilogue warps
+                const uint32_t item = tile_item(st, i);
+                __syncwarp();
+                if (lane == 0) tile_release(st, i);
+                if (item == kItemNone) break;
+                const uint32_t vb = item >> 2;
+                const int part = (int)(item & 3u);
+                const int tm = (int)vb / tiles_n, tn = (int)vb % tiles_n;
+                const uint32_t acc = i & 1u;
+                drain_tile(P, st, tm, tn * BN + (part == 2 ? BN / 2 : 0), part ? BN / 2 : BN, acc, (i >> 1) & 1u, i);
+                __syncwarp();
+                if (lane == 0) {
+                    if (st.rank == 0) mbar_arrive_local(st.bars + 144 + 8 * acc);
+                    else mbar_arrive_cl(map_rank(st.bars + 144 + 8 * acc, 0u));
+                    if (warp == 4 && st.rank == 0) {
+                        if (i < 8) MM_PROBE(i, 3);
+                        if (L && L->audit) atomicAdd(L->audit + vb, 1u);
+                        if (L && L->stamps) L->stamps[2 * (size_t)vb + 1] = gtimer();
+                    }
+                }
+            }
+        }
+        __syncwarp();
     }
     __device__ static void block(const Params& P, State& st, char* d, uint32_t vb) { block_part(P, st, d, vb, 0); }
     // part 0: the whole 256x256 tile vb; part 1 / 2: its left / right 256x128 half (the plain
@@ -399,7 +601,7 @@ extern "C" int kl_mm_probe_stride() { return kProbeStride; }
 #endif
 
 int kl_mm_stage_smem(int stages) {     // dynamic shared memory of one CTA at `stages`
-    return stages * kStageBytes + kEpiBytes + 1024 + 256;
+    return stages * kStageBytes + kEpiBytes + 1024 + kBarBytes;
 }
 
 int kl_mm_info(KlKindInfo* o) {

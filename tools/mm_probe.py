@@ -25,13 +25,14 @@ for sh in shapes:
             torch.cuda.synchronize()
             if mode == "plain":
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ctx.delay(torch.cuda.current_stream(), 200_000)   # host launch latency outside the interval
                 e0.record()
                 ctx.run_plain("MM", i.grid, i.args, 0)
                 e1.record()
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
             else:
-                ts.append(ctx.run_capped("MM", i.grid, i.args, 0))
+                ts.append(ctx.run_capped("MM", i.grid, i.args, 0, spin_ns=200_000) - 0.2)   # spin inside the interval
         res[mode] = statistics.median(ts[1:])
     fl = 2.0 * M * N * Kd
     print(f"MM {sh:>16s} tiles {i.grid:5d}  plain {res['plain'] * 1e3:8.1f} us ({fl / res['plain'] / 1e9:6.0f} TF/s)  "

@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Where an MM launch's time goes: device time stamps from a -DKL_MM_PROBE build (kl_mm.cu): per
 CTA pair, kernel entry, end of init, per tile the MMA issuer's first-stage-full and last-MMA-issued
-times and the epilogue's wait/stores-issued times, and fini.  Plain grid (the solo roofline and
+times, the epilogue's accumulator-ready / stores-issued times, the leader producer's publish and
+first-load times and the MMA issuer's tile-item / accumulator-free times, and fini.  Plain grid (the solo roofline and
 the sequential baseline) and the uncapped persistent launcher.
 usage: KL_LIB_PATH=variants/libkl_mmprobe.so python tools/mm_stamp_probe.py [MxNxK]   (needs a GPU)"""
 import ctypes as C
@@ -21,7 +22,8 @@ M, N, Kd = (int(x) for x in sh.split("x"))
 L = K.lib()
 L.kl_mm_probe_read.argtypes = [C.c_void_p, C.c_int]
 stride = L.kl_mm_probe_stride()
-ntile = (stride - 4) // 4
+NF = 8
+ntile = (stride - 4) // NF
 ctx = K.Context(device=0)
 i = Instance(G.gen("MM", dict(M=M, N=N, K=Kd)), "cuda")
 buf = (C.c_ulonglong * (96 * stride))()
@@ -34,12 +36,12 @@ def read():
 
 
 def report(name, a, ev_ms):
-    live = a[:, ntile * 4] > 0
+    live = a[:, ntile * NF] > 0
     a = a[live]
-    t0 = a[:, ntile * 4].min()
+    t0 = a[:, ntile * NF].min()
     a = np.where(a > 0, (a - t0) / 1e3, np.nan)   # us from the first pair's entry
-    ent, ini, pre, end = (a[:, ntile * 4 + f] for f in range(4))
-    tiles = a[:, :ntile * 4].reshape(-1, ntile, 4)
+    ent, ini, pre, end = (a[:, ntile * NF + f] for f in range(4))
+    tiles = a[:, :ntile * NF].reshape(-1, ntile, NF)
     print(f"== {name}: {len(a)} pairs, event-timed {ev_ms * 1e3:.1f} us, device span (first entry -> last fini) "
           f"{np.nanmax(end):.1f} us")
     print(f"  entry spread {np.nanmin(ent):.2f}..{np.nanmax(ent):.2f}  init done {np.nanmedian(ini):.2f} (max {np.nanmax(ini):.2f})")
@@ -50,7 +52,10 @@ def report(name, a, ev_ms):
         d = t[:, 1] - t[:, 0]
         print(f"  tile {j}: n {np.sum(~np.isnan(t[:, 0])):3d}  mma start med {np.nanmedian(t[:, 0]):6.2f} "
               f"[{np.nanmin(t[:, 0]):6.2f}, {np.nanmax(t[:, 0]):6.2f}]  mma span med {np.nanmedian(d):6.2f}  "
-              f"epi wait->stores med {np.nanmedian(t[:, 3] - t[:, 2]):5.2f} (stores issued max {np.nanmax(t[:, 3]):6.2f})")
+              f"epi drain (acc ready -> stores issued) med {np.nanmedian(t[:, 3] - t[:, 2]):5.2f} (stores issued max {np.nanmax(t[:, 3]):6.2f})")
+        if not np.all(np.isnan(t[:, 4])):
+            print(f"          producer: published {np.nanmedian(t[:, 4]):6.2f}  first load issued {np.nanmedian(t[:, 5]):6.2f};  "
+                  f"MMA: got item {np.nanmedian(t[:, 6]):6.2f}  accumulator free {np.nanmedian(t[:, 7]):6.2f}  first stage full {np.nanmedian(t[:, 0]):6.2f}")
         if j > 0:
             g = t[:, 0] - tiles[:, j - 1, 1]
             print(f"          gap last MMA issued (tile {j - 1}) -> first stage full (tile {j}): med {np.nanmedian(g):5.2f} max {np.nanmax(g):5.2f}")
