@@ -210,8 +210,26 @@ struct BodySPMV {
         const bool live = r_local < (int)(v1 - v0) * 8 && row < a.n_rows;   // the warp takes the shuffles
         const int s = live ? __ldg(a.rowptr + row) : 0, e = live ? __ldg(a.rowptr + row + 1) : 0;
         float sum = 0.f;
-#pragma unroll 2
-        for (int j = s + lane; j < e; j += kLanes) sum = fmaf(__ldg(a.vals + j), __ldg(a.x + __ldg(a.cols + j)), sum);
+        // batches of kB products per lane: all kB (column, value) loads in flight together, then
+        // all kB x gathers, then the fmaf chain in j order (the same order as a plain loop over
+        // j = s + lane, s + lane + kLanes, ...): two dependent memory round trips per batch instead
+        // of two per product (rows of <= kB * kLanes = 24 nonzeros take one batch)
+        constexpr int kB = 6;
+        for (int j0 = s + lane; j0 < e; j0 += kB * kLanes) {
+            int c[kB];
+            float v[kB], xv[kB];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                const int j = j0 + b * kLanes;
+                c[b] = j < e ? __ldg(a.cols + j) : 0;
+                v[b] = j < e ? __ldg(a.vals + j) : 0.f;
+            }
+#pragma unroll
+            for (int b = 0; b < kB; ++b) xv[b] = (j0 + b * kLanes < e) ? __ldg(a.x + c[b]) : 0.f;
+#pragma unroll
+            for (int b = 0; b < kB; ++b)
+                if (j0 + b * kLanes < e) sum = fmaf(v[b], xv[b], sum);
+        }
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         if (live && lane == 0) a.y[row] = sum;
@@ -309,6 +327,7 @@ struct BodyST {
 #ifndef KL_MRIQ_P
 #define KL_MRIQ_P 0
 #endif
+#if KL_MRIQ_P > 0 || defined(KL_MRIQ_SCALAR)
 // sin(2 pi t), cos(2 pi t) on the FMA pipe: r = t - rint(t) in [-1/2, 1/2] (rint by the
 // 1.5*2^23 rounding trick, exact for |t| < 2^22), then sin = r P(r^2) (degree 5 in r^2) and
 // cos = Q(r^2) (degree 6), near-minimax coefficients (Lawson-weighted least squares on
@@ -331,6 +350,7 @@ __device__ __forceinline__ void sincos_2pi_poly(float t, float& s, float& c) {
     pc = fmaf(u, pc, -19.73920440673828f);
     c = fmaf(u, pc, 1.0f);
 }
+#endif
 
 struct BodyMRIQ {
     using Params = kl_args_mriq;
@@ -340,6 +360,71 @@ struct BodyMRIQ {
     static_assert(kP >= 0 && kP < kG, "KL_MRIQ_P in [0, KL_MRIQ_G)");
     __device__ static void init(const Params&, State&, char*) {}
     __device__ static void fini(const Params&, State&, char*) {}
+#if KL_MRIQ_P == 0 && !defined(KL_MRIQ_SCALAR)
+    // Paired k-points on the sm_100 FP32x2 path (FFMA2 / FMUL2): k-points 2p and 2p+1 of a chunk
+    // are staged as sk[2p] = (kx0, kx1, ky0, ky1), sk[2p+1] = (kz0, kz1, phi0, phi1) (x 2 pi), so
+    // one FMUL2 + two FFMA2 give both phases and two FFMA2 both accumulates: 13 instructions per
+    // two terms instead of 18 (SASS: 2 LDS.128, FMUL2, 4 FFMA2, 2 FMUL.RZ, 4 MUFU).  The MUFU
+    // work is unchanged (MRIQ stays MUFU-bound solo); the issue slots it frees are the
+    // co-scheduled partner's.  Sums: even and odd k-points accumulate in the two halves (each in
+    // k order, one fmaf per term) and meet once at the end -- the order is fixed by num_k alone,
+    // so sliced == unsliced stays bit-identical; the fp32 error bound of DESIGN §3 holds (two
+    // sums of n_k / 2 terms).
+    __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
+        __shared__ float4 sk[256];
+        const int i = (int)vb * 256 + threadIdx.x;
+        const bool live = i < a.num_x;
+        const float x = live ? __ldg(a.x + i) : 0.f, y = live ? __ldg(a.y + i) : 0.f,
+                    z = live ? __ldg(a.z + i) : 0.f;
+        const float2 x2 = make_float2(x, x), y2 = make_float2(y, y), z2 = make_float2(z, z);
+        float2 qr = make_float2(0.f, 0.f), qi = make_float2(0.f, 0.f);
+        float* skf = reinterpret_cast<float*>(sk);
+        for (int k0 = 0; k0 < a.num_k; k0 += 256) {
+            const int n = min(256, a.num_k - k0);
+            __syncthreads();
+            if ((int)threadIdx.x < n) {
+                const int k = k0 + threadIdx.x, p = threadIdx.x >> 1, h = threadIdx.x & 1;
+                const float sc = 6.28318530717958647692f;
+                skf[8 * p + h] = sc * __ldg(a.kx + k);
+                skf[8 * p + 2 + h] = sc * __ldg(a.ky + k);
+                skf[8 * p + 4 + h] = sc * __ldg(a.kz + k);
+                skf[8 * p + 6 + h] = __ldg(a.phimag + k);
+            }
+            __syncthreads();
+            const int np = n >> 1;
+            int p = 0;
+            for (; p + 4 <= np; p += 4) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) pair(sk[2 * (p + j)], sk[2 * (p + j) + 1], x2, y2, z2, qr, qi);
+            }
+            for (; p < np; ++p) pair(sk[2 * p], sk[2 * p + 1], x2, y2, z2, qr, qi);
+            if (n & 1) {                                    // odd tail: the even half's term
+                const float4 aa = sk[2 * np], bb = sk[2 * np + 1];
+                const float t = fmaf(aa.x, x, fmaf(aa.z, y, bb.x * z));
+                float sn, cs;
+                __sincosf(t, &sn, &cs);
+                qr.x = fmaf(bb.z, cs, qr.x);
+                qi.x = fmaf(bb.z, sn, qi.x);
+            }
+        }
+        if (live) {
+            a.qr[i] = qr.x + qr.y;
+            a.qi[i] = qi.x + qi.y;
+        }
+    }
+    __device__ static __forceinline__ void pair(const float4 aa, const float4 bb, const float2 x2, const float2 y2,
+                                                const float2 z2, float2& qr, float2& qi) {
+        float2 t = __fmul2_rn(make_float2(bb.x, bb.y), z2);
+        t = __ffma2_rn(make_float2(aa.z, aa.w), y2, t);
+        t = __ffma2_rn(make_float2(aa.x, aa.y), x2, t);
+        float s0, c0, s1, c1;
+        __sincosf(t.x, &s0, &c0);
+        __sincosf(t.y, &s1, &c1);
+        const float2 ph = make_float2(bb.z, bb.w);
+        qr = __ffma2_rn(ph, make_float2(c0, c1), qr);
+        qi = __ffma2_rn(ph, make_float2(s0, s1), qi);
+    }
+#else
     __device__ static __forceinline__ void term(const float4 q, float x, float y, float z, bool poly,
                                                 float& qr, float& qi) {
         const float t = fmaf(q.x, x, fmaf(q.y, y, q.z * z));
@@ -380,6 +465,7 @@ struct BodyMRIQ {
             a.qi[i] = qi;
         }
     }
+#endif
 };
 
 // BS (SDK BlackScholes): 128 threads x 5 float4 = 2560 options per block.

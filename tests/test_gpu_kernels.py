@@ -114,6 +114,26 @@ def test_integer_modes_exact(ctx, kind, field):
     assert np.array_equal(res[field], ref[field])
 
 
+@pytest.mark.parametrize("mode", ["int", "random"])
+def test_spmv_long_and_empty_rows(ctx, mode):
+    """SPMV rows of 0..100 nonzeros: empty rows, rows inside one load batch (<= 24 = 6 products
+    x 4 lanes) and rows spanning several batches; bit-exact in integer mode, normwise otherwise,
+    and the persistent (chunked) launch bit-identical to the plain grid."""
+    d = G.gen("SPMV", dict(n_rows=2051, n_cols=3000, nnz_min=0, nnz_max=100), mode=mode)
+    inst = Instance(d, "cuda")
+    res = _run_plain(ctx, inst)
+    ref = O.run_kernel(d)
+    if mode == "int":
+        assert np.array_equal(res["y"], ref["y"])
+    else:
+        compare("SPMV", res, ref)
+    for o in inst.outputs.values():
+        o.fill_(0)
+    torch.cuda.synchronize()
+    ctx.run_capped("SPMV", inst.grid, inst.args, 3)
+    assert np.array_equal(inst.result()["y"], res["y"])
+
+
 @pytest.mark.parametrize("num_k", [1, 7, 8, 9, 255, 256, 263, 2048])
 def test_mriq_num_k_edges(ctx, num_k):
     """MRIQ's k loop: 256-point staging chunks, unrolled groups of KL_MRIQ_G = 8 (of which the last
@@ -132,17 +152,21 @@ def test_mriq_num_k_edges(ctx, num_k):
 
 def test_mriq_zero_k_closed_form(ctx):
     """k = 0 for every k-point: cos = 1 and sin = 0 exactly, so Qr = sum phiMag and Qi = 0 (the
-    oracle's closed-form pin), bit-exact in fp32 (fmaf(phi, 1, q) = phi + q)."""
-    d = G.gen("MRIQ", dict(num_x=300, num_k=16))
-    for f in ("kx", "ky", "kz"):
-        d[f][:] = 0
-    inst = Instance(d, "cuda")
-    res = _run_plain(ctx, inst)
-    acc = np.float32(0)
-    for v in np.asarray(d["phimag"], np.float32):
-        acc = np.float32(acc + v)
-    assert np.all(np.asarray(res["qi"]) == 0)
-    assert np.all(np.asarray(res["qr"]) == acc)
+    oracle's closed-form pin), bit-exact in fp32 (fmaf(phi, 1, q) = phi + q) in the
+    kernel's summation order: the FP32x2 path accumulates even and odd k-points in two halves
+    (each in k order) and adds them at the end (kl_kernels.cu BodyMRIQ); num_k odd puts the last
+    term in the even half."""
+    for num_k in (16, 17):
+        d = G.gen("MRIQ", dict(num_x=300, num_k=num_k))
+        for f in ("kx", "ky", "kz"):
+            d[f][:] = 0
+        inst = Instance(d, "cuda")
+        res = _run_plain(ctx, inst)
+        acc = [np.float32(0), np.float32(0)]
+        for k, v in enumerate(np.asarray(d["phimag"], np.float32)):
+            acc[k & 1] = np.float32(acc[k & 1] + v)
+        assert np.all(np.asarray(res["qi"]) == 0)
+        assert np.all(np.asarray(res["qr"]) == np.float32(acc[0] + acc[1]))
 
 
 # ---- paths the SMALL sizes never reach -------------------------------------------------------
