@@ -279,6 +279,30 @@ struct BodyST {
                 if (lane == 0 && x0 > 0) xm = __ldg(in + f - 1);
                 if ((lane == 31 || x0 + 4 >= nx) && x0 + 4 < nx) xp = __ldg(in + f + 4);
                 const float4 ym = ld4(in + f - nx), yp = ld4(in + f + nx);
+#ifdef KL_ST_X2
+                // FP32x2 path (measured, not the default): elements (0, 1) and (2, 3) in pairs --
+                // FADD2 / FMUL2 / FFMA2 round each lane exactly like the scalar fadd / fmul / fmaf
+                // below, same operand order (bit-identical); 14 instead of 28 FP instructions per
+                // float4.  Plain grid 0.190 -> 0.186 ms, but the persistent variant 0.213 -> 0.241
+                // ms solo and C5 within noise (+0.6 %), so the scalar body stays the default.
+                float2 s0 = __fadd2_rn(make_float2(zm.x, zm.y), make_float2(zp.x, zp.y));
+                float2 s1 = __fadd2_rn(make_float2(zm.z, zm.w), make_float2(zp.z, zp.w));
+                s0 = __fadd2_rn(s0, make_float2(ym.x, ym.y));
+                s1 = __fadd2_rn(s1, make_float2(ym.z, ym.w));
+                s0 = __fadd2_rn(s0, make_float2(yp.x, yp.y));
+                s1 = __fadd2_rn(s1, make_float2(yp.z, yp.w));
+                s0 = __fadd2_rn(s0, make_float2(xm, c.x));
+                s1 = __fadd2_rn(s1, make_float2(c.y, c.z));
+                s0 = __fadd2_rn(s0, make_float2(c.y, c.z));
+                s1 = __fadd2_rn(s1, make_float2(c.w, xp));
+                const float2 n0 = __fmul2_rn(make_float2(a.c0, a.c0), make_float2(c.x, c.y));
+                const float2 n1 = __fmul2_rn(make_float2(a.c0, a.c0), make_float2(c.z, c.w));
+                const float2 r0 = __ffma2_rn(make_float2(a.c1, a.c1), s0, make_float2(-n0.x, -n0.y));
+                const float2 r1 = __ffma2_rn(make_float2(a.c1, a.c1), s1, make_float2(-n1.x, -n1.y));
+                const bool e0 = x0 > 0, e3 = x0 + 3 < nx - 1;          // x = x0 + 1, x0 + 2 are interior
+                *reinterpret_cast<float4*>(a.out + f) =
+                    make_float4(e0 ? r0.x : c.x, r0.y, r1.x, e3 ? r1.y : c.w);
+#else
                 const float cc[4] = {c.x, c.y, c.z, c.w};
                 const float am[4] = {zm.x, zm.y, zm.z, zm.w}, ap[4] = {zp.x, zp.y, zp.z, zp.w};
                 const float bm[4] = {ym.x, ym.y, ym.z, ym.w}, bp[4] = {yp.x, yp.y, yp.z, yp.w};
@@ -298,6 +322,7 @@ struct BodyST {
                     }
                 }
                 *reinterpret_cast<float4*>(a.out + f) = make_float4(o[0], o[1], o[2], o[3]);
+#endif
             } else if (act) {
                 *reinterpret_cast<float4*>(a.out + f) = c;
             }
@@ -471,6 +496,7 @@ struct BodyMRIQ {
 // BS (SDK BlackScholes): 128 threads x 5 float4 = 2560 options per block.
 // The SDK sample's formula with the hardware approximations (MUFU ex2/lg2/rcp, ~2 ulp): BS is
 // issue-bound at paper size, and the result stays far inside the normwise 1e-5 tolerance.
+#ifdef KL_BS_SCALAR
 __device__ __forceinline__ float cnd_f(float d) {
     const float A1 = 0.31938153f, A2 = -0.356563782f, A3 = 1.781477937f, A4 = -1.821255978f,
                 A5 = 1.330274429f, RSQRT2PI = 0.39894228040143267793994605993438f;
@@ -487,6 +513,43 @@ __device__ __forceinline__ void bs_one(float S, float X, float T, float R, float
     call = S * c1 - X * e * c2;
     put = X * e * (1.0f - c2) - S * (1.0f - c1);
 }
+#endif
+#ifndef KL_BS_SCALAR
+// Two options at a time on the sm_100 FP32x2 path (FFMA2 / FMUL2 / FADD2): the arithmetic of
+// bs_one in pairs, the MUFU-based functions (sqrtf, __fdividef, __logf, __expf, __frcp_rn) per
+// option.  BS was issue-bound (ncu: issue 82 %, fma pipe 49 %); the pairs halve its FP32 issue
+// slots.  Same operations per option as bs_one up to contraction choices (normwise tolerance).
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 cnd_f2(float2 d) {
+    const float A1 = 0.31938153f, A2 = -0.356563782f, A3 = 1.781477937f, A4 = -1.821255978f,
+                A5 = 1.330274429f, RSQRT2PI = 0.39894228040143267793994605993438f;
+    const float2 den = __ffma2_rn(f2(0.2316419f), make_float2(fabsf(d.x), fabsf(d.y)), f2(1.0f));
+    const float2 K = make_float2(__frcp_rn(den.x), __frcp_rn(den.y));
+    const float2 dd = __fmul2_rn(__fmul2_rn(f2(-0.5f), d), d);
+    const float2 ex = make_float2(__expf(dd.x), __expf(dd.y));
+    float2 p = __ffma2_rn(K, f2(A5), f2(A4));
+    p = __ffma2_rn(K, p, f2(A3));
+    p = __ffma2_rn(K, p, f2(A2));
+    p = __ffma2_rn(K, p, f2(A1));
+    const float2 c = __fmul2_rn(__fmul2_rn(f2(RSQRT2PI), ex), __fmul2_rn(K, p));
+    return make_float2(d.x > 0.f ? 1.0f - c.x : c.x, d.y > 0.f ? 1.0f - c.y : c.y);
+}
+__device__ __forceinline__ void bs_two(float2 S, float2 X, float2 T, float R, float V, float2& call, float2& put) {
+    const float2 sqrtT = make_float2(sqrtf(T.x), sqrtf(T.y));
+    const float2 lg = make_float2(__logf(__fdividef(S.x, X.x)), __logf(__fdividef(S.y, X.y)));
+    const float2 vs = __fmul2_rn(f2(V), sqrtT);
+    const float2 num = __ffma2_rn(f2(R + 0.5f * V * V), T, lg);
+    const float2 d1 = make_float2(__fdividef(num.x, vs.x), __fdividef(num.y, vs.y));
+    const float2 d2 = __fadd2_rn(d1, make_float2(-vs.x, -vs.y));
+    const float2 c1 = cnd_f2(d1), c2 = cnd_f2(d2);
+    const float2 rt = __fmul2_rn(f2(-R), T);
+    const float2 xe = __fmul2_rn(X, make_float2(__expf(rt.x), __expf(rt.y)));
+    const float2 u = __fmul2_rn(xe, c2);
+    call = __ffma2_rn(S, c1, make_float2(-u.x, -u.y));
+    const float2 v = __fmul2_rn(xe, __fadd2_rn(f2(1.0f), make_float2(-c2.x, -c2.y)));
+    put = __ffma2_rn(make_float2(-S.x, -S.y), __fadd2_rn(f2(1.0f), make_float2(-c1.x, -c1.y)), v);
+}
+#endif
 struct BodyBS {
     using Params = kl_args_bs;
     using State = Empty;
@@ -505,10 +568,18 @@ struct BodyBS {
             int64_t i = (int64_t)vb * 640 + j * 128 + threadIdx.x;
             if (i >= n4) break;
             float4 s = __ldg(S + i), x = __ldg(X + i), t = __ldg(T + i), c, p;
+#ifdef KL_BS_SCALAR
             bs_one(s.x, x.x, t.x, a.R, a.V, c.x, p.x);
             bs_one(s.y, x.y, t.y, a.R, a.V, c.y, p.y);
             bs_one(s.z, x.z, t.z, a.R, a.V, c.z, p.z);
             bs_one(s.w, x.w, t.w, a.R, a.V, c.w, p.w);
+#else
+            float2 c0, p0, c1, p1;
+            bs_two(make_float2(s.x, s.y), make_float2(x.x, x.y), make_float2(t.x, t.y), a.R, a.V, c0, p0);
+            bs_two(make_float2(s.z, s.w), make_float2(x.z, x.w), make_float2(t.z, t.w), a.R, a.V, c1, p1);
+            c = make_float4(c0.x, c0.y, c1.x, c1.y);
+            p = make_float4(p0.x, p0.y, p1.x, p1.y);
+#endif
             C[i] = c;
             P[i] = p;
         }
