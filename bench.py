@@ -869,7 +869,11 @@ def main(argv=None):
         seq = bl.get("sequential", {}).get("kernels_per_s")
         ms4 = max((v["kernels_per_s"] for k, v in bl.items() if k.startswith("multistream")), default=None)
         pk = res.get("per_kernel", {})
+        # ALU peaks scale with the SM clock: the solo kernels (timed alone, outside the timed
+        # region) against the maximum clock, the in-step roofline against the median clock the
+        # nvidia-smi samples saw during the timed steps (sw_power_cap lowers it under the queue)
         sm_mhz = (res["clocks"].get("sm_mhz") or 1965.0)
+        sm_max = (res["clocks"].get("sm_max_mhz") or 1965.0)
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
         roof_all = {}
@@ -883,10 +887,10 @@ def main(argv=None):
                 roof_all[k] = {"bound": "tensor", "achieved": a, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                                "frac": a / peaks["bf16_tflops"], "ms": v["ms"]}
             else:
-                pk_, what = alu_peak(k, sm_mhz)
+                pk_, what = alu_peak(k, sm_max)
                 a = v["ops"] / (v["ms"] / 1e3)
                 roof_all[k] = {"bound": "alu", "achieved": a / 1e12, "peak": pk_ / 1e12, "unit": f"T{what}",
-                               "frac": a / pk_, "ms": v["ms"]}
+                               "frac": a / pk_, "ms": v["ms"], "peak_clock_mhz": sm_max}
         qk = build_queue(0, 1, args.instances, args.workload, args.mix)
         dom = max(pk, key=lambda k: pk[k]["ms"] * sum(1 for x in qk if x == k)) if pk else None
         roof = None
@@ -900,8 +904,10 @@ def main(argv=None):
             scale = {"alu": 1e12, "tensor": 1e12, "hbm": 1e9}[solo["bound"]]
             ach = units * tk["blocks"] / w["grid"] / (tk["busy_ms"] / 1e3) / scale
             tr = ncu_traffic(dom)
-            roof = {"bound": solo["bound"], "achieved": ach, "peak": solo["peak"], "unit": solo["unit"],
-                    "frac": ach / solo["peak"], "traffic": tr["bytes_per_instance"] if tr else None,
+            peak_step = alu_peak(dom, sm_mhz)[0] / 1e12 if solo["bound"] == "alu" else solo["peak"]
+            roof = {"bound": solo["bound"], "achieved": ach, "peak": peak_step, "unit": solo["unit"],
+                    "frac": ach / peak_step,
+                    **({"peak_clock_mhz": sm_mhz} if solo["bound"] == "alu" else {}), "traffic": tr["bytes_per_instance"] if tr else None,
                     "traffic_source": (f"dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture "
                                        f"of the kind's whole-instance persistent launch ({tr['source']})") if tr else None,
                     "kernel": dom,
