@@ -380,7 +380,11 @@ __device__ __forceinline__ void sincos_2pi_poly(float t, float& s, float& c) {
 struct BodyMRIQ {
     using Params = kl_args_mriq;
     using State = Empty;
+#ifdef KL_MRIQ_V2
+    static constexpr int kThreads = 256, kChunk = 2, kDynSmem = 0, kMinBlocks = KL_MINB_MRIQ;
+#else
     static constexpr int kThreads = 256, kChunk = 1, kDynSmem = 0, kMinBlocks = KL_MINB_MRIQ;
+#endif
     static constexpr int kG = KL_MRIQ_G, kP = KL_MRIQ_P;
     static_assert(kP >= 0 && kP < kG, "KL_MRIQ_P in [0, KL_MRIQ_G)");
     __device__ static void init(const Params&, State&, char*) {}
@@ -395,6 +399,72 @@ struct BodyMRIQ {
     // k order, one fmaf per term) and meet once at the end -- the order is fixed by num_k alone,
     // so sliced == unsliced stays bit-identical; the fp32 error bound of DESIGN §3 holds (two
     // sums of n_k / 2 terms).
+#ifdef KL_MRIQ_V2
+    // Two virtual blocks per grid block (a fetched chunk of 2, block_range): every thread runs
+    // voxel t of each, so one pair of k-points from shared memory feeds four terms (half the LDS
+    // per term); each voxel's arithmetic is exactly the one-voxel path's (sliced == unsliced).
+    __device__ static void block_range(const Params& a, State&, char*, uint32_t v0, uint32_t v1) {
+        __shared__ float4 sk[256];
+        const int i0 = (int)v0 * 256 + threadIdx.x, i1 = i0 + 256;
+        const bool l0 = i0 < a.num_x, l1 = v1 > v0 + 1 && i1 < a.num_x;
+        const float2 xa = f2(l0 ? __ldg(a.x + i0) : 0.f), ya = f2(l0 ? __ldg(a.y + i0) : 0.f),
+                     za = f2(l0 ? __ldg(a.z + i0) : 0.f);
+        const float2 xb = f2(l1 ? __ldg(a.x + i1) : 0.f), yb = f2(l1 ? __ldg(a.y + i1) : 0.f),
+                     zb = f2(l1 ? __ldg(a.z + i1) : 0.f);
+        float2 qra = make_float2(0.f, 0.f), qia = qra, qrb = qra, qib = qra;
+        float* skf = reinterpret_cast<float*>(sk);
+        for (int k0 = 0; k0 < a.num_k; k0 += 256) {
+            const int n = min(256, a.num_k - k0);
+            __syncthreads();
+            if ((int)threadIdx.x < n) {
+                const int k = k0 + threadIdx.x, p = threadIdx.x >> 1, h = threadIdx.x & 1;
+                const float sc = 6.28318530717958647692f;
+                skf[8 * p + h] = sc * __ldg(a.kx + k);
+                skf[8 * p + 2 + h] = sc * __ldg(a.ky + k);
+                skf[8 * p + 4 + h] = sc * __ldg(a.kz + k);
+                skf[8 * p + 6 + h] = __ldg(a.phimag + k);
+            }
+            __syncthreads();
+            const int np = n >> 1;
+            int p = 0;
+            for (; p + 4 <= np; p += 4) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 aa = sk[2 * (p + j)], bb = sk[2 * (p + j) + 1];
+                    pair(aa, bb, xa, ya, za, qra, qia);
+                    pair(aa, bb, xb, yb, zb, qrb, qib);
+                }
+            }
+            for (; p < np; ++p) {
+                const float4 aa = sk[2 * p], bb = sk[2 * p + 1];
+                pair(aa, bb, xa, ya, za, qra, qia);
+                pair(aa, bb, xb, yb, zb, qrb, qib);
+            }
+            if (n & 1) {
+                const float4 aa = sk[2 * np], bb = sk[2 * np + 1];
+                tail(aa, bb, xa.x, ya.x, za.x, qra, qia);
+                tail(aa, bb, xb.x, yb.x, zb.x, qrb, qib);
+            }
+        }
+        if (l0) {
+            a.qr[i0] = qra.x + qra.y;
+            a.qi[i0] = qia.x + qia.y;
+        }
+        if (l1) {
+            a.qr[i1] = qrb.x + qrb.y;
+            a.qi[i1] = qib.x + qib.y;
+        }
+    }
+    __device__ static __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+    __device__ static __forceinline__ void tail(const float4 aa, const float4 bb, float x, float y, float z,
+                                                float2& qr, float2& qi) {
+        const float t = fmaf(aa.x, x, fmaf(aa.z, y, bb.x * z));
+        float sn, cs;
+        __sincosf(t, &sn, &cs);
+        qr.x = fmaf(bb.z, cs, qr.x);
+        qi.x = fmaf(bb.z, sn, qi.x);
+    }
+#else
     __device__ static void block(const Params& a, State&, char*, uint32_t vb) {
         __shared__ float4 sk[256];
         const int i = (int)vb * 256 + threadIdx.x;
@@ -437,6 +507,7 @@ struct BodyMRIQ {
             a.qi[i] = qi.x + qi.y;
         }
     }
+#endif
     __device__ static __forceinline__ void pair(const float4 aa, const float4 bb, const float2 x2, const float2 y2,
                                                 const float2 z2, float2& qr, float2& qi) {
         float2 t = __fmul2_rn(make_float2(bb.x, bb.y), z2);
