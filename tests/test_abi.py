@@ -98,11 +98,15 @@ def test_host_only_refuses_device_calls(L):
 
 
 def test_config_validation(L):
-    """kl_create rejects an MM ring depth that is not one of its occupancy levels (R28) and a
-    scheduler count that does not divide the 64 warps of an SM."""
-    for bad in (dict(mm_stages=5), dict(mm_stages=1), dict(n_sched=3)):
+    """kl_create rejects an MM ring depth that is not one of its occupancy levels (R28), a
+    scheduler count that does not divide the 64 warps of an SM, a distinct_kinds flag (R31b)
+    other than 0 / 1 and a non-zero reserved field."""
+    for bad in (dict(mm_stages=5), dict(mm_stages=1), dict(n_sched=3), dict(distinct_kinds=2),
+                dict(reserved0=1)):
         with pytest.raises(K.KlError) as e:
             _host_ctx(**bad)
         assert e.value.status == K.KL_EINVAL, bad
     for ok in (0, 2, 3, 4, 6):
         _host_ctx(mm_stages=ok).close()
+    for ok in (0, 1):
+        _host_ctx(distinct_kinds=ok).close()
