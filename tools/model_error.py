@@ -13,7 +13,7 @@ timestamps), so neither the ramp-up nor the survivor's solo tail enters the co-r
 (0.08 on C2050), and the CP error.
 KL_C3_SYNTH=1 adds the synthetic streaming kernel (4 FMAs per element), i.e. config C3's
 tensor-core MM vs streaming pair among 8 more.
-usage: python tools/model_error.py [out.json]"""
+usage: python tools/model_error.py [out.json]      (KL_PROFILE=path: another calibration file)"""
 import itertools
 import json
 import os
@@ -42,7 +42,7 @@ def fits(p1, b1, p2, b2, sm):
 
 
 def main(out_path):
-    path = os.path.join(ROOT, "profiles", "kl_profile_b200.json")
+    path = os.environ.get("KL_PROFILE") or os.path.join(ROOT, "profiles", "kl_profile_b200.json")
     profiles, kcfg = bench.load_profiles(path)
     calib = json.load(open(path))
     clock = calib.get("clock_mhz_under_ncu", 1965.0) * 1e6
