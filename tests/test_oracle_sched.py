@@ -181,12 +181,15 @@ def test_c1_greedy_vs_brute_force_calibrated(queue):
     t_opt = O.brute_force_makespan(pend, profs, cfg, mode="4")
     seq = sum(O.alg1_makespan([e], profs, cfg, mode="4")[0] for e in pend)
     rows = {"queue": queue, "brute_force": t_opt, "sequential": seq}
+    # both walks drop a kernel once its remaining blocks fall below 1e-9 of its grid (the
+    # oracle's completion threshold), so equal plans agree to ~1e-9 per kernel, not to rounding
+    tol = 1e-9 * (len(pend) + 1)
     for rule in (0, 1):
         t_g, _ = O.alg1_makespan(pend, profs, cfg, ap=0.0, am=0.0, mode="4", split_rule=rule)
-        assert t_opt <= t_g * (1 + 1e-9)
+        assert t_opt <= t_g * (1 + tol)
         rows[f"greedy_rule{rule}"] = t_g
         rows[f"gap_rule{rule}"] = t_g / t_opt - 1.0
-    assert t_opt <= seq * (1 + 1e-9)
+    assert t_opt <= seq * (1 + tol)
     if os.environ.get("KL_WRITE_ARTEFACTS"):
         path = os.path.join(os.path.dirname(__file__), "..", "profiles", "r02_c1_gap.json")
         old = json.load(open(path)) if os.path.exists(path) else []
