@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define KL_ABI_VERSION 2
+#define KL_ABI_VERSION 3   /* 3: kl_config.distinct_kinds + reserved0 */
 #define KL_MAX_SMS 256
 
 typedef struct kl_ctx kl_ctx;

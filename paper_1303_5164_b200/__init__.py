@@ -49,6 +49,7 @@ KIND_ID = {k: i for i, k in enumerate(KINDS)}
 NKINDS = len(KINDS)
 
 _vp = C.c_void_p
+ABI_VERSION = 3   # include/kl.h KL_ABI_VERSION
 
 
 class ArgsPC(C.Structure):
@@ -186,6 +187,8 @@ def lib() -> C.CDLL:
     L = C.CDLL(LIB_PATH)
     P = C.POINTER
     L.kl_abi_version.restype = C.c_int
+    if L.kl_abi_version() != ABI_VERSION:   # the structs below mirror include/kl.h of this version
+        raise RuntimeError(f"{LIB_PATH} has ABI {L.kl_abi_version()}, the binding expects {ABI_VERSION}: rebuild")
     L.kl_config_default.argtypes = [P(Config)]
     L.kl_create.argtypes = [C.c_int, P(Config), P(_vp)]
     L.kl_destroy.argtypes = [_vp]

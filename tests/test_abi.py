@@ -26,7 +26,7 @@ def test_exports_every_declared_symbol(L):
     assert declared == set(K.ABI_SYMBOLS)
     for s in declared:
         assert hasattr(L, s), s
-    assert L.kl_abi_version() == 2
+    assert L.kl_abi_version() == 3
 
 
 def test_struct_layouts_match(L):
