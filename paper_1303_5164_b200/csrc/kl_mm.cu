@@ -4,18 +4,23 @@
 // One virtual thread block = one 256x256 fp32 output tile computed by a CTA pair (a cluster of 2
 // on one TPC; kl_launcher.cuh k_persistent_pair): tcgen05.mma.cta_group::2 (M=256, N=256, K=16)
 // reads A's 256 rows as 128 rows from each CTA's shared memory and B's 256 columns as 128 rows
-// of Bt from each, and accumulates CTA r's 128 rows in CTA r's TMEM.  Per tile, in both CTAs,
-//   warp 0 lane 0 : TMA producer  -- its CTA's 128x64 (A) and 128x64 (B) bf16 tiles, 128B swizzle,
-//                   into a ring of S shared-memory stages; completion (.cta_group::2) on the
-//                   LEADER's full barrier, which expects both CTAs' bytes;
-//   warp 1 lane 0 : MMA issuer (leader only) -- 4 MMAs per stage into one of two 256-column fp32
-//                   accumulators; tcgen05.commit multicast frees the stage in both CTAs and, after
-//                   the last k-block, signals both CTAs' epilogues;
-//   warps 4..7    : epilogue -- drain the PREVIOUS tile's accumulator (tcgen05.ld 32x32b.x32, each
-//                   warp its 32 TMEM lanes) while warps 0-1 run this tile's mainloop.
+// of Bt from each, and accumulates CTA r's 128 rows in CTA r's TMEM.  The launchers run the
+// decoupled tile loop (BodyMM::run; the per-tile block() path is kept for reference):
+//   leader thread 0 : scheduler -- claims each tile from the launcher's fetch (or the plain grid's
+//                   static schedule) when the leader's producer asks for it, and publishes it
+//                   through a 4-deep tile-info ring in both CTAs' shared memory;
+//   warp 2 lane 0 : TMA producer (both CTAs) -- its CTA's 128x64 (A) and 128x64 (B) bf16 tiles,
+//                   128B swizzle, into a ring of S shared-memory stages, streaming across tile
+//                   boundaries; completion (.cta_group::2) on the LEADER's full barrier;
+//   warp 1 lane 0 : MMA issuer (leader only) -- waits for a drained accumulator (tempty), then 4
+//                   MMAs per stage into one of two 256-column fp32 accumulators; tcgen05.commit
+//                   multicast frees the stage in both CTAs and, after the last k-block, signals
+//                   both CTAs' epilogues;
+//   warps 4..7    : epilogue (both CTAs) -- drain the previous tile's accumulator (tcgen05.ld
+//                   32x32b.x32, each warp its 32 TMEM lanes) through a swizzled shared-memory box
+//                   into coalesced 128-byte STG lines while the next tile's mainloop runs.
 // Against one-CTA 128x256 tiles this halves the operand bytes each SM pulls from L2 per MMA
-// (the one-CTA kernel is L2-feed-bound at 48 % of the bf16 peak).  The per-tile cluster barrier of
-// the pair launcher orders accumulator reuse across the two CTAs.
+// (the one-CTA kernel is L2-feed-bound at 48 % of the bf16 peak).
 // The stage count S in {2, 3, 4, 6} (32 KiB of shared memory each) is the kernel's occupancy
 // knob: MM's occupancy levels; one instantiation per level.
 // Numerics: bf16 products are exact in fp32; only the fp32 accumulation order differs from the
