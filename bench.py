@@ -776,6 +776,16 @@ def _oracle_sample(O, data, sizes, frac, cores) -> dict:
     return out
 
 
+def profile_label(path: str) -> str:
+    """The calibration file the model decides from: its name and calibration time."""
+    try:
+        with open(path) as f:
+            when = json.load(f).get("when", "?")
+    except (OSError, ValueError):
+        return f"{os.path.basename(path)} (missing: built-in defaults)"
+    return f"{os.path.relpath(path, ROOT)} (calibrated {when})"
+
+
 def _oracle_profiles(path: str | None = None, levels: str = "four", bmax: str = "hw"):
     """The oracle's profile table: the calibrated profiles with the b_max the GPU run uses
     (load_profiles: bmax_sat with every whole-warp level when bmax="sat")."""
@@ -824,6 +834,7 @@ def main(argv=None):
               "split_rule": "argmax CP over (pair, ratio)" if args.split_rule == 1 else "argmin dT (Eq.8)",
               "cp_min": args.cp_min if args.cp_min is not None else load_profiles(args.profile)[1].get("cp_min", 0.0),
               "decisions_from": "measured pair table (OPT)" if args.opt else "Markov model",
+              "profile": profile_label(args.profile),
               "pair_choice": "critical-kind restriction (R29)" if args.critical else "max CP (Alg.1 greedy)",
               **({"config_overrides": args.set} if args.set else {}),
               **({"profile_overrides": args.prof} if args.prof else {}),
