@@ -349,6 +349,9 @@ struct BodyST {
 #ifndef KL_MRIQ_G
 #define KL_MRIQ_G 8
 #endif
+#ifndef KL_MRIQ_U
+#define KL_MRIQ_U 8      // k-point pairs per unrolled group of the FP32x2 loop (4: C5 -0.5 %)
+#endif
 #ifndef KL_MRIQ_P
 #define KL_MRIQ_P 0
 #endif
@@ -488,9 +491,9 @@ struct BodyMRIQ {
             __syncthreads();
             const int np = n >> 1;
             int p = 0;
-            for (; p + 4 <= np; p += 4) {
+            for (; p + KL_MRIQ_U <= np; p += KL_MRIQ_U) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) pair(sk[2 * (p + j)], sk[2 * (p + j) + 1], x2, y2, z2, qr, qi);
+                for (int j = 0; j < KL_MRIQ_U; ++j) pair(sk[2 * (p + j)], sk[2 * (p + j) + 1], x2, y2, z2, qr, qi);
             }
             for (; p < np; ++p) pair(sk[2 * p], sk[2 * p + 1], x2, y2, z2, qr, qi);
             if (n & 1) {                                    // odd tail: the even half's term
